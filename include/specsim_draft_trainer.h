@@ -1,0 +1,257 @@
+/*
+ * specsim draft trainer — C ABI of the B200-native TIDE draft-training hot path.
+ *
+ * The reference (arxiv 2602.05145, /root/reference/proj) ships no trainer:
+ * its `train_sim` module is SPEC prose with an analytic body
+ * (SPEC.md:380-446), and `proj/include/specsim/` holds only errors.hpp,
+ * rng.hpp, perf_model.hpp and workload.hpp.  This header is the drop-in for
+ * the seams SPEC names:
+ *
+ *   - SignalGeometry / extract_signals / record_sample (SPEC.md:237-241,
+ *     SPEC.md:267-275)        -> specsim_hsbuf_*
+ *   - train(job) -> TrainingOutcome, called by
+ *     maybe_trigger_training -> specsim_trainer_train
+ *   - the step inside train(): forward / backward / AdamW / DP all-reduce of
+ *     the EAGLE-3 style draft head
+ *                                              -> specsim_trainer_step
+ *   - accept-length bookkeeping (perf_model.hpp:52-80, rng.hpp:13-39)
+ *                                              -> specsim_rng_*, specsim_*accept*
+ *
+ * Conventions (mirroring the reference):
+ *   - Status codes: SPECSIM_EDOMAIN is the reference's std::invalid_argument
+ *     (domain error, CLI exit 1), SPECSIM_ECONFIG is specsim::ConfigError
+ *     (errors.hpp:8-13, CLI exit 2).  Every function returns a
+ *     status; the message of the last failure on the calling thread is
+ *     available from specsim_last_error().
+ *   - Validation collects every problem into one message, like
+ *     LatencyProfile's constructor (perf_model.cpp:57-82).
+ *   - Handles are single-owner and not thread-safe (workload.hpp:60,
+ *     SPEC.md:296).  One trainer per GPU; at most one job in flight
+ *     (SPEC.md:367).
+ *   - Plain pointers and sizes only; no framework types cross this boundary.
+ *   - There is no CPU fallback: on a machine without a usable sm_100 GPU the
+ *     GPU entry points fail with SPECSIM_ECUDA.
+ */
+#ifndef SPECSIM_DRAFT_TRAINER_H
+#define SPECSIM_DRAFT_TRAINER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+typedef enum specsim_status {
+  SPECSIM_OK = 0,
+  SPECSIM_EDOMAIN = 1, /* std::invalid_argument in the reference (exit 1)  */
+  SPECSIM_ECONFIG = 2, /* specsim::ConfigError, errors.hpp:10-13 (exit 2)  */
+  SPECSIM_ECUDA = 3,   /* CUDA runtime / kernel failure, or no GPU         */
+  SPECSIM_ENCCL = 4    /* NCCL failure in the data-parallel exchange       */
+} specsim_status;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* specsim_last_error(void);
+const char* specsim_version(void);
+
+/* ------------------------------------------------- bookkeeping (host only) */
+/* Seeded mt19937_64 with the reference's hand-rolled conversions
+ * (rng.hpp:13-39): uniform = (x >> 11) * 2^-53, Box-Muller cosine branch,
+ * inverse-CDF geometric. */
+typedef struct specsim_rng specsim_rng;
+int specsim_rng_create(uint64_t seed, specsim_rng** out);
+int specsim_rng_destroy(specsim_rng* rng);
+int specsim_rng_uniform(specsim_rng* rng, double* out);
+int specsim_rng_normal(specsim_rng* rng, double mean, double sd, double* out);
+int specsim_rng_geometric(specsim_rng* rng, double mean, int64_t* out);
+int specsim_rng_next_u64(specsim_rng* rng, uint64_t* out);
+
+/* perf_model.cpp:159-169 */
+int specsim_expected_accept_length(double alpha, int32_t gamma, double* out);
+/* perf_model.cpp:171-177: k in [1, gamma+1] (accepted drafts + bonus token) */
+int specsim_sample_accept_length(specsim_rng* rng, double alpha, int32_t gamma, int32_t* out);
+/* perf_model.cpp:213-224 (bisection to kBisectionTol = 1e-6) */
+int specsim_alpha_from_accept_length(double ell, int32_t gamma, double* out);
+/* SPEC.md:348 chronological 9:1 split: the oldest floor(9n/10) samples train. */
+int specsim_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
+
+/* ------------------------------------------------------ signal geometry */
+/* bytes per token = layers_tapped * hidden_dim * bytes_per_element */
+typedef struct specsim_signal_geometry {
+  int32_t hidden_dim;
+  int32_t layers_tapped;     /* default 3 (low / mid / high) */
+  int32_t bytes_per_element; /* default 2 (bf16); only 2 is trainable */
+} specsim_signal_geometry;
+
+int specsim_bytes_per_token(const specsim_signal_geometry* g, int64_t* out);
+
+/* Synthetic captured request; stream = Rng(seed + index):
+ *   accept lengths k = sample_accept_length(alpha, gamma), the last one
+ *   truncated so that sum k == length;
+ *   ids[i] = floor(uniform() * vocab);
+ *   features[i, j] = bf16_rne(normal(0, 1)), j in [0, layers*hidden) in
+ *   low | mid | high order;
+ *   alpha_s = alpha_from_accept_length(length / steps, gamma).
+ * Any output pointer may be NULL.  Host-only, multithreaded over samples. */
+int specsim_synth_capture(uint64_t seed, int64_t index, int32_t length, int32_t vocab,
+                          int32_t hidden, int32_t layers, double alpha, int32_t gamma,
+                          int32_t* ids, uint16_t* features, int32_t* accept_lengths,
+                          int32_t* n_steps, double* alpha_s);
+
+/* --------------------------------------------------- hidden-state buffer */
+/* Device-resident ring of captured samples: per token one packed
+ * [layers * hidden] bf16 record plus its int32 token id.  Byte accounting
+ * follows extract_signals: bytes grow by
+ * records * bytes_per_token (ids are not counted) and move to the
+ * cumulative total when they exceed the flush threshold (default 64 MiB,
+ * SPEC.md:293). */
+typedef struct specsim_hsbuf specsim_hsbuf;
+
+typedef struct specsim_hsbuf_stats {
+  int64_t records;          /* tokens appended since creation           */
+  int64_t bytes;            /* bytes currently buffered (not flushed)   */
+  int64_t flushes;          /* flush events                             */
+  int64_t cumulative_bytes; /* bytes moved to storage by flushes        */
+  int64_t samples;          /* samples recorded (record_sample calls)   */
+  int64_t resident_tokens;  /* tokens currently held in the device ring */
+} specsim_hsbuf_stats;
+
+/* flush_threshold_bytes <= 0 selects 64 MiB. */
+int specsim_hsbuf_create(const specsim_signal_geometry* geometry, int64_t capacity_tokens,
+                         int64_t flush_threshold_bytes, int device, specsim_hsbuf** out);
+int specsim_hsbuf_destroy(specsim_hsbuf* buf);
+
+/* extract_signals for one verify step of one request + record_sample.
+ * layer_ptrs[l] points at a [rows, ld] bf16 matrix of layer l's hidden
+ * states (host memory unless on_device != 0); the n accepted positions are
+ * rows accepted_idx[0..n) (or rows 0..n if accepted_idx is NULL).
+ * token_ids[i] is the id at accepted position i.  Appending to a sample_id
+ * different from the open one closes the open sample (its records stay
+ * contiguous in the ring).  alpha is the per-sample alpha label
+ * (SPEC.md:365); the last value given for a sample wins.
+ * Host pointers are only read during the call. */
+int specsim_hsbuf_append(specsim_hsbuf* buf, int64_t sample_id, double alpha,
+                         const void* const* layer_ptrs, int64_t rows, int64_t ld,
+                         const int32_t* token_ids, const int32_t* accepted_idx, int32_t n,
+                         int on_device);
+
+/* Same, with records already packed [n, layers*hidden] (host or device). */
+int specsim_hsbuf_append_packed(specsim_hsbuf* buf, int64_t sample_id, double alpha,
+                                const uint16_t* features, const int32_t* token_ids, int32_t n,
+                                int on_device);
+
+int specsim_hsbuf_stats_get(const specsim_hsbuf* buf, specsim_hsbuf_stats* out);
+int specsim_hsbuf_sample_info(const specsim_hsbuf* buf, int64_t sample_id, int32_t* length,
+                              double* alpha);
+/* Copies a sample's packed records / ids back to host (tests). */
+int specsim_hsbuf_read_sample(const specsim_hsbuf* buf, int64_t sample_id, uint16_t* features,
+                              int32_t* token_ids);
+
+/* ---------------------------------------------------------- draft trainer */
+/* EAGLE-3 style draft head:
+ *   g = W_fc f, u = [RMSNorm(E[x_{t+1}]); RMSNorm(g)], one decoder layer
+ *   (GQA attention with NeoX RoPE, SwiGLU MLP, residual from g), final norm,
+ *   LM head over the full target vocabulary. */
+typedef struct specsim_draft_shape {
+  int32_t hidden;        /* H                                       */
+  int32_t vocab;         /* V                                       */
+  int32_t seq_len;       /* S training positions per sample         */
+  int32_t n_heads;       /* query heads                             */
+  int32_t n_kv_heads;    /* key/value heads                         */
+  int32_t head_dim;      /* 64 or 128                               */
+  int32_t ffn;           /* I                                       */
+  int32_t layers_tapped; /* 3                                       */
+  int32_t micro_batch;   /* B samples per rank per step             */
+  float rms_eps;
+  double rope_theta;
+} specsim_draft_shape;
+
+/* PyTorch AdamW semantics. */
+typedef struct specsim_adamw {
+  float lr, beta1, beta2, eps, weight_decay;
+} specsim_adamw;
+
+typedef struct specsim_trainer specsim_trainer;
+
+typedef struct specsim_step_result {
+  double loss;          /* sum_t m_t (lse_t - logit_t[y_t]) / global valid */
+  int64_t valid_tokens; /* sum_t m_t on this rank                          */
+  int64_t top1_correct; /* sum_t m_t [argmax_t == y_t] on this rank        */
+  int64_t positions;    /* B * S processed positions on this rank          */
+  double ms;            /* device time of the step (CUDA events)           */
+} specsim_step_result;
+
+typedef struct specsim_training_outcome {
+  double duration_hours; /* measured wall time of the job     */
+  double alpha_eval;     /* top-1 accuracy on D_eval (replaces current_alpha) */
+  int64_t new_version;   /* draft version produced by this job            */
+  double mean_loss;      /* mean training loss over the job's steps       */
+  int64_t steps;
+} specsim_training_outcome;
+
+/* 128-byte NCCL unique id for world > 1 (rank 0 creates, caller broadcasts). */
+int specsim_nccl_unique_id(uint8_t* out128);
+
+/* Parameters are initialised from Rng(seed + 1) normal(0, 0.02) (norm
+ * weights 1.0); the frozen embedding E from Rng(seed + 2) normal(0, 0.02).
+ * nccl_id may be NULL when world == 1. */
+int specsim_trainer_create(const specsim_draft_shape* shape, const specsim_adamw* opt,
+                           uint64_t seed, int rank, int world, const uint8_t* nccl_id,
+                           int device, specsim_trainer** out);
+int specsim_trainer_destroy(specsim_trainer* t);
+
+/* One optimiser step over n <= micro_batch samples of buf (missing rows are
+ * padding with zero mask).  global_valid_tokens is sum m_t over all ranks'
+ * samples of this step (0 = use this rank's own count).  Synchronous. */
+int specsim_trainer_step(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* sample_ids,
+                         int32_t n, int64_t global_valid_tokens, specsim_step_result* out);
+
+/* Forward only: loss and top-1 over n <= micro_batch samples. */
+int specsim_trainer_eval(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* sample_ids,
+                         int32_t n, specsim_step_result* out);
+
+/* train(job) -> TrainingOutcome with the real step as its
+ * body: `epochs` passes over train_ids (sample i -> rank i mod world), then
+ * top-1 accuracy on eval_ids.  The draft is trained in place; callers keep
+ * get_param copies when they need the deploy/reject gate. */
+int specsim_trainer_train(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* train_ids,
+                          int64_t n_train, const int64_t* eval_ids, int64_t n_eval,
+                          int32_t epochs, specsim_training_outcome* out);
+
+/* Parameter registry (fp32 master copies; names: fc, w_in, w_hid, qkv, o,
+ * w_post, gate_up, down, w_fin, lm_head).  Frozen embedding: "embed". */
+int specsim_trainer_num_params(const specsim_trainer* t, int32_t* count, int64_t* total_elems);
+int specsim_trainer_param_info(const specsim_trainer* t, int32_t index, const char** name,
+                               int64_t* rows, int64_t* cols);
+int specsim_trainer_get_param(const specsim_trainer* t, const char* name, float* host_out);
+int specsim_trainer_set_param(specsim_trainer* t, const char* name, const float* host_in);
+/* Gradient of the last step (after the DP all-reduce). */
+int specsim_trainer_get_grad(const specsim_trainer* t, const char* name, float* host_out);
+int specsim_trainer_set_embedding(specsim_trainer* t, const uint16_t* host_bf16);
+int specsim_trainer_get_embedding(const specsim_trainer* t, uint16_t* host_bf16);
+int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step);
+
+/* Per-phase device timing of the last step (CUDA events on the step stream).
+ * Phases: 0 ingest/gather, 1 GEMMs (sum over all tcgen05 GEMM launches),
+ * 2 attention, 3 norms/elementwise, 4 LM-head+CE GEMMs, 5 AdamW,
+ * 6 all-reduce.  flops[i] = algorithmic FLOPs of the phase (GEMM phases). */
+int specsim_trainer_set_timing(specsim_trainer* t, int enabled);
+int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
+                                int32_t* launches7);
+
+/* ------------------------------------------------------ kernel test hooks */
+/* Host-buffer wrappers around single kernels, used by the parity tests.
+ * GEMM: epi 0 bf16 out, 1 f32 out, 2 f32 accumulate (C in/out), 3 bf16 out
+ * plus residual R.  A is [M, lda] (K-major) or [K, lda] (MN-major); B is
+ * [N, ldb] or [K, ldb].  iters > 1 re-launches and reports mean kernel ms. */
+int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_t N, int32_t K,
+                       const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb, void* C,
+                       int64_t ldc, const uint16_t* R, int64_t ldr, int32_t iters,
+                       float* mean_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECSIM_DRAFT_TRAINER_H */

@@ -1,0 +1,780 @@
+/*
+ * CPU ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.h for the parity status).
+ *
+ * Bookkeeping restates /root/reference/proj:
+ *   Rng                      rng.hpp:13-39
+ *   expected_accept_length   perf_model.cpp:159-169
+ *   sample_accept_length     perf_model.cpp:171-177
+ *   bisect_increasing        perf_model.cpp:30-41
+ *   alpha_from_accept_length perf_model.cpp:213-224
+ *   SignalGeometry / extract_signals byte accounting
+ *   chronological 9:1 split
+ * The neural step follows SURVEY.md Appendix A (no reference code exists).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+/* ======================================================== mt19937_64 + Rng */
+#define MT_N 312
+#define MT_M 156
+#define MT_MATRIX_A 0xB5026F5AA96619E9ULL
+#define MT_UPPER 0xFFFFFFFF80000000ULL
+#define MT_LOWER 0x7FFFFFFFULL
+
+void orc_rng_seed(orc_rng* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < MT_N; ++i)
+    r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+  r->idx = MT_N;
+}
+
+uint64_t orc_rng_next(orc_rng* r) {
+  if (r->idx >= MT_N) {
+    for (int i = 0; i < MT_N; ++i) {
+      uint64_t x = (r->mt[i] & MT_UPPER) | (r->mt[(i + 1) % MT_N] & MT_LOWER);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= MT_MATRIX_A;
+      r->mt[i] = r->mt[(i + MT_M) % MT_N] ^ xa;
+    }
+    r->idx = 0;
+  }
+  uint64_t y = r->mt[r->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+/* rng.hpp:18 — 53 high bits scaled by 2^-53 */
+double orc_uniform(orc_rng* r) { return (double)(orc_rng_next(r) >> 11) * 0x1.0p-53; }
+
+/* rng.hpp:21-26 — Box-Muller, cosine branch, u1 in (0, 1] */
+double orc_normal(orc_rng* r, double mean, double sd) {
+  double u1 = 1.0 - orc_uniform(r);
+  double u2 = orc_uniform(r);
+  return mean + sd * sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+}
+
+/* rng.hpp:29-35 — inverse-CDF geometric on {1, 2, ...} */
+int64_t orc_geometric(orc_rng* r, double mean) {
+  if (mean <= 1.0) return 1;
+  const double p = 1.0 / mean;
+  const double u = orc_uniform(r);
+  const double k = floor(log1p(-u) / log1p(-p));
+  return 1 + (int64_t)(k > 0.0 ? k : 0.0);
+}
+
+/* ====================================================== accept-length math */
+static int bad_alpha(double a) { return !(a >= 0.0 && a <= 1.0); }
+
+int orc_expected_accept_length(double alpha, int gamma, double* out) {
+  if (bad_alpha(alpha) || gamma < 1) return 1;
+  double sum = 1.0, term = 1.0;
+  for (int k = 1; k <= gamma; ++k) {
+    term *= alpha;
+    sum += term;
+  }
+  *out = sum;
+  return 0;
+}
+
+int orc_sample_accept_length(orc_rng* r, double alpha, int gamma, int* out) {
+  if (bad_alpha(alpha) || gamma < 1) return 1;
+  int accepted = 0;
+  while (accepted < gamma && orc_uniform(r) < alpha) ++accepted;
+  *out = accepted + 1;
+  return 0;
+}
+
+int orc_alpha_from_accept_length(double ell, int gamma, double* out) {
+  if (gamma < 1) return 1;
+  if (!(ell >= 1.0 && ell <= gamma + 1.0)) return 1;
+  if (ell <= 1.0) {
+    *out = 0.0;
+    return 0;
+  }
+  if (ell >= gamma + 1.0) {
+    *out = 1.0;
+    return 0;
+  }
+  double lo = 0.0, hi = 1.0;
+  while (hi - lo > 1e-6) { /* kBisectionTol, perf_model.hpp:83 */
+    const double mid = 0.5 * (lo + hi);
+    double f;
+    orc_expected_accept_length(mid, gamma, &f);
+    if (f < ell)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  *out = 0.5 * (lo + hi);
+  return 0;
+}
+
+void orc_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval) {
+  const int64_t t = n > 0 ? (9 * n) / 10 : 0;
+  *n_train = t;
+  *n_eval = n > 0 ? n - t : 0;
+}
+
+int64_t orc_bytes_per_token(int hidden, int layers, int bytes_per_element) {
+  return (int64_t)layers * hidden * bytes_per_element;
+}
+
+void orc_extract_signals(int64_t* st, int64_t n, int64_t bpt, int64_t flush_threshold) {
+  if (n <= 0) return;
+  st[0] += n;
+  st[1] += n * bpt;
+  if (st[1] > flush_threshold) {
+    st[3] += st[1];
+    st[1] = 0;
+    st[2] += 1;
+  }
+}
+
+/* ============================================================ bf16 helpers */
+uint16_t orc_f32_to_bf16(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (uint16_t)((u >> 16) | 0x40); /* NaN */
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+float orc_bf16_to_f32(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+static inline float rb(float x) { return orc_bf16_to_f32(orc_f32_to_bf16(x)); }
+
+static void round_vec(float* x, int64_t n, int on) {
+  if (!on) return;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) x[i] = rb(x[i]);
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* ======================================================= synthetic capture */
+int orc_synth_capture(uint64_t seed, int64_t index, int length, int vocab, int hidden,
+                      int layers, double alpha, int gamma, int32_t* ids, uint16_t* features,
+                      int32_t* accept_lengths, int32_t* n_steps, double* alpha_s) {
+  if (length < 1 || vocab < 1 || hidden < 1 || layers < 1) return 1;
+  if (bad_alpha(alpha) || gamma < 1) return 1;
+  orc_rng r;
+  orc_rng_seed(&r, seed + (uint64_t)index);
+  int total = 0, steps = 0;
+  while (total < length) {
+    int k;
+    orc_sample_accept_length(&r, alpha, gamma, &k);
+    if (k > length - total) k = length - total; /* SPEC.md:294 truncation */
+    if (accept_lengths) accept_lengths[steps] = k;
+    total += k;
+    ++steps;
+  }
+  if (n_steps) *n_steps = steps;
+  if (alpha_s) orc_alpha_from_accept_length((double)length / steps, gamma, alpha_s);
+  for (int i = 0; i < length; ++i) {
+    int32_t id = (int32_t)floor(orc_uniform(&r) * vocab);
+    if (ids) ids[i] = id;
+  }
+  if (features) {
+    const int64_t w = (int64_t)layers * hidden;
+    for (int64_t i = 0; i < (int64_t)length * w; ++i)
+      features[i] = orc_f32_to_bf16((float)orc_normal(&r, 0.0, 1.0));
+  }
+  return 0;
+}
+
+void orc_init_normal_block(uint64_t seed_base, int p, int64_t n, float* out) {
+  const int64_t nblk = (n + (1 << 20) - 1) >> 20;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t j = 0; j < nblk; ++j) {
+    orc_rng r;
+    orc_rng_seed(&r, seed_base + ((uint64_t)p << 32) + (uint64_t)j);
+    const int64_t e0 = j << 20, e1 = (e0 + (1 << 20)) < n ? e0 + (1 << 20) : n;
+    for (int64_t e = e0; e < e1; ++e) out[e] = (float)orc_normal(&r, 0.0, 0.02);
+  }
+}
+
+/* ========================================================== param layout */
+int64_t orc_param_layout(const orc_shape* s, const char** names, int64_t* rows, int64_t* cols,
+                         int64_t* offsets) {
+  static const char* N[ORC_NPARAMS] = {"fc",     "w_in",    "w_hid", "qkv",   "o",
+                                       "w_post", "gate_up", "down",  "w_fin", "lm_head"};
+  const int64_t H = s->H, Q = (int64_t)s->nh * s->hd, KV = (int64_t)s->nkv * s->hd;
+  const int64_t R[ORC_NPARAMS] = {H, 1, 1, Q + 2 * KV, H, 1, 2 * (int64_t)s->I, H, 1, s->V};
+  const int64_t Cc[ORC_NPARAMS] = {(int64_t)s->layers * H, H, H, 2 * H, Q, H, H, s->I, H, H};
+  int64_t off = 0;
+  for (int p = 0; p < ORC_NPARAMS; ++p) {
+    if (names) names[p] = N[p];
+    if (rows) rows[p] = R[p];
+    if (cols) cols[p] = Cc[p];
+    if (offsets) offsets[p] = off;
+    off += R[p] * Cc[p];
+  }
+  return off;
+}
+
+/* ========================================================= batch assembly */
+void orc_gather_batch(const orc_shape* s, int nsamples, const int32_t* const* ids,
+                      const uint16_t* const* feats, const int32_t* lens, uint16_t* F,
+                      int32_t* u, int32_t* y, int32_t* m) {
+  const int64_t w = (int64_t)s->layers * s->H;
+  for (int b = 0; b < s->B; ++b) {
+    const int L = b < nsamples ? lens[b] : 0;
+    for (int t = 0; t < s->S; ++t) {
+      const int64_t row = (int64_t)b * s->S + t;
+      if (t < L)
+        memcpy(F + row * w, feats[b] + (int64_t)t * w, (size_t)w * 2);
+      else
+        memset(F + row * w, 0, (size_t)w * 2);
+      u[row] = (t + 1 < L) ? ids[b][t + 1] : 0;
+      y[row] = (t + 2 < L) ? ids[b][t + 2] : 0;
+      m[row] = (t + 2 < L) ? 1 : 0;
+    }
+  }
+}
+
+/* ============================================================== dense math */
+/* C[M,N] (+)= A[M,K] . B[N,K]^T, fp32, cache-blocked. */
+static void mm_nt(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                  int64_t ldb, float* C, int64_t ldc, int accumulate) {
+  enum { MB = 32, NB = 64, KB = 256 };
+  const int64_t nbm = (M + MB - 1) / MB, nbn = (N + NB - 1) / NB;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t blk = 0; blk < nbm * nbn; ++blk) {
+    const int64_t i0 = (blk / nbn) * MB, j0 = (blk % nbn) * NB;
+    const int64_t i1 = i0 + MB < M ? i0 + MB : M, j1 = j0 + NB < N ? j0 + NB : N;
+    float acc[MB][NB];
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t j = j0; j < j1; ++j)
+        acc[i - i0][j - j0] = accumulate ? C[i * ldc + j] : 0.f;
+    for (int64_t k0 = 0; k0 < K; k0 += KB) {
+      const int64_t kl = (k0 + KB < K ? KB : K - k0);
+      for (int64_t i = i0; i < i1; ++i) {
+        const float* a = A + i * lda + k0;
+        for (int64_t j = j0; j < j1; ++j) {
+          const float* b = B + j * ldb + k0;
+          float part[16] = {0};
+          int64_t k = 0;
+          for (; k + 16 <= kl; k += 16)
+            for (int t = 0; t < 16; ++t) part[t] += a[k + t] * b[k + t];
+          float sum = 0.f;
+          for (int t = 0; t < 16; ++t) sum += part[t];
+          for (; k < kl; ++k) sum += a[k] * b[k];
+          acc[i - i0][j - j0] += sum;
+        }
+      }
+    }
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t j = j0; j < j1; ++j) C[i * ldc + j] = acc[i - i0][j - j0];
+  }
+}
+
+static float* transpose(const float* X, int64_t rows, int64_t cols, int64_t ld) {
+  float* T = (float*)malloc(sizeof(float) * rows * cols);
+  enum { TB = 64 };
+#pragma omp parallel for schedule(static)
+  for (int64_t i0 = 0; i0 < rows; i0 += TB)
+    for (int64_t j0 = 0; j0 < cols; j0 += TB)
+      for (int64_t i = i0; i < i0 + TB && i < rows; ++i)
+        for (int64_t j = j0; j < j0 + TB && j < cols; ++j) T[j * rows + i] = X[i * ld + j];
+  return T;
+}
+
+/* C[M,K'] (+)= A[M,N'] . B[N',K']  (data-gradient form) */
+static void mm_nn(int64_t M, int64_t Kp, int64_t Np, const float* A, int64_t lda, const float* B,
+                  int64_t ldb, float* C, int64_t ldc, int accumulate) {
+  float* Bt = transpose(B, Np, Kp, ldb); /* [K', N'] */
+  mm_nt(M, Kp, Np, A, lda, Bt, Np, C, ldc, accumulate);
+  free(Bt);
+}
+
+/* C[N,K] = A[T,N]^T . X[T,K]  (weight-gradient form) */
+static void mm_tn(int64_t N, int64_t K, int64_t T, const float* A, int64_t lda, const float* X,
+                  int64_t ldx, float* C, int64_t ldc) {
+  float* At = transpose(A, T, N, lda); /* [N, T] */
+  float* Xt = transpose(X, T, K, ldx); /* [K, T] */
+  mm_nt(N, K, T, At, T, Xt, T, C, ldc, 0);
+  free(At);
+  free(Xt);
+}
+
+static float* falloc(int64_t n) { return (float*)calloc((size_t)n, sizeof(float)); }
+
+/* y = x * rstd * w ; returns rstd per row */
+static void rmsnorm_fwd(int64_t T, int64_t H, const float* x, int64_t ldx, const float* w,
+                        float eps, float* y, int64_t ldy, float* rstd) {
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    const float* xr = x + t * ldx;
+    double ss = 0.0;
+    for (int64_t i = 0; i < H; ++i) ss += (double)xr[i] * xr[i];
+    const float r = 1.0f / sqrtf((float)(ss / (double)H) + eps);
+    rstd[t] = r;
+    for (int64_t i = 0; i < H; ++i) y[t * ldy + i] = xr[i] * r * w[i];
+  }
+}
+
+/* dx (+)= rstd * (dy*w) - x * rstd^3 * mean((dy*w) * x) ; dw += sum_t dy * x * rstd */
+static void rmsnorm_bwd(int64_t T, int64_t H, const float* dy, int64_t lddy, const float* x,
+                        int64_t ldx, const float* w, const float* rstd, float* dx, int64_t lddx,
+                        int accumulate_dx, float* dw) {
+  if (dx) {
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < T; ++t) {
+      const float* g = dy + t * lddy;
+      const float* xr = x + t * ldx;
+      double dot = 0.0;
+      for (int64_t i = 0; i < H; ++i) dot += (double)g[i] * w[i] * xr[i];
+      const float r = rstd[t];
+      const float c = (float)(dot / (double)H) * r * r * r;
+      for (int64_t i = 0; i < H; ++i) {
+        const float v = r * g[i] * w[i] - xr[i] * c;
+        if (accumulate_dx)
+          dx[t * lddx + i] += v;
+        else
+          dx[t * lddx + i] = v;
+      }
+    }
+  }
+  if (dw) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < H; ++i) {
+      double s = 0.0;
+      for (int64_t t = 0; t < T; ++t) s += (double)dy[t * lddy + i] * x[t * ldx + i] * rstd[t];
+      dw[i] = (float)s;
+    }
+  }
+}
+
+/* NeoX rotate-half tables: cos/sin[pos * half + i], angle = pos * theta^(-2i/hd) in double */
+static void rope_tables(int S, int hd, double theta, float* cs, float* sn) {
+  const int half = hd / 2;
+  for (int p = 0; p < S; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double inv = pow(theta, -2.0 * (double)i / (double)hd);
+      const double a = (double)p * inv;
+      cs[p * half + i] = (float)cos(a);
+      sn[p * half + i] = (float)sin(a);
+    }
+}
+
+/* in-place rotation of n_heads vectors of one row; inverse = transpose rotation */
+static void rope_row(float* x, int n_heads, int hd, const float* cs, const float* sn, int inverse) {
+  const int half = hd / 2;
+  for (int h = 0; h < n_heads; ++h) {
+    float* v = x + (int64_t)h * hd;
+    for (int i = 0; i < half; ++i) {
+      const float c = cs[i], s = sn[i];
+      const float x1 = v[i], x2 = v[i + half];
+      if (!inverse) {
+        v[i] = x1 * c - x2 * s;
+        v[i + half] = x2 * c + x1 * s;
+      } else {
+        v[i] = x1 * c + x2 * s;
+        v[i + half] = x2 * c - x1 * s;
+      }
+    }
+  }
+}
+
+static float silu(float x) { return x / (1.0f + expf(-x)); }
+
+/* ============================================================ model state */
+typedef struct acts {
+  int64_t T, H, Q, KV, NQKV, I, V, W3;
+  float *F, *E_rows, *g, *U, *rstd_a, *rstd_b, *qkv, *o, *lse_attn, *r, *z, *rstd_post, *gu,
+      *act, *h, *nrm, *rstd_fin, *lse, *dlog;
+  int32_t* argmax;
+  float *cs, *sn;
+} acts;
+
+static void acts_free(acts* a) {
+  float** ptrs[] = {&a->F,   &a->E_rows, &a->g,   &a->U,   &a->rstd_a,   &a->rstd_b, &a->qkv,
+                    &a->o,   &a->lse_attn, &a->r, &a->z,   &a->rstd_post, &a->gu,    &a->act,
+                    &a->h,   &a->nrm,    &a->rstd_fin, &a->lse, &a->dlog, &a->cs,     &a->sn};
+  for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) {
+    free(*ptrs[i]);
+    *ptrs[i] = NULL;
+  }
+  free(a->argmax);
+}
+
+static float* wcopy(const float* p, int64_t n, int round) {
+  float* w = (float*)malloc(sizeof(float) * n);
+  memcpy(w, p, sizeof(float) * n);
+  round_vec(w, n, round);
+  return w;
+}
+
+/* Forward through the LM-head logits; fills dlog with logits [T, V]. */
+static void forward_core(const orc_shape* s, const float* P, const int64_t* off,
+                         const uint16_t* E, const uint16_t* F16, const int32_t* u, int rnd,
+                         acts* a, float** Wb /* bf16-rounded GEMM weights by param index */) {
+  const int64_t T = (int64_t)s->B * s->S, H = s->H, Q = (int64_t)s->nh * s->hd,
+                KV = (int64_t)s->nkv * s->hd, I = s->I, V = s->V, W3 = (int64_t)s->layers * H;
+  a->T = T; a->H = H; a->Q = Q; a->KV = KV; a->NQKV = Q + 2 * KV; a->I = I; a->V = V; a->W3 = W3;
+  a->F = falloc(T * W3);
+  for (int64_t i = 0; i < T * W3; ++i) a->F[i] = orc_bf16_to_f32(F16[i]);
+  a->g = falloc(T * H);
+  mm_nt(T, H, W3, a->F, W3, Wb[ORC_FC], W3, a->g, H, 0);
+  round_vec(a->g, T * H, rnd);
+  a->E_rows = falloc(T * H);
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t i = 0; i < H; ++i) a->E_rows[t * H + i] = orc_bf16_to_f32(E[(int64_t)u[t] * H + i]);
+  a->U = falloc(T * 2 * H);
+  a->rstd_a = falloc(T);
+  a->rstd_b = falloc(T);
+  rmsnorm_fwd(T, H, a->E_rows, H, P + off[ORC_W_IN], s->eps, a->U, 2 * H, a->rstd_a);
+  rmsnorm_fwd(T, H, a->g, H, P + off[ORC_W_HID], s->eps, a->U + H, 2 * H, a->rstd_b);
+  round_vec(a->U, T * 2 * H, rnd);
+  const int64_t NQ = a->NQKV;
+  a->qkv = falloc(T * NQ);
+  mm_nt(T, NQ, 2 * H, a->U, 2 * H, Wb[ORC_QKV], 2 * H, a->qkv, NQ, 0);
+  round_vec(a->qkv, T * NQ, rnd);
+  a->cs = falloc((int64_t)s->S * s->hd / 2);
+  a->sn = falloc((int64_t)s->S * s->hd / 2);
+  rope_tables(s->S, s->hd, s->theta, a->cs, a->sn);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    const int pos = (int)(t % s->S);
+    float* row = a->qkv + t * NQ;
+    rope_row(row, s->nh, s->hd, a->cs + (int64_t)pos * s->hd / 2, a->sn + (int64_t)pos * s->hd / 2, 0);
+    rope_row(row + Q, s->nkv, s->hd, a->cs + (int64_t)pos * s->hd / 2,
+             a->sn + (int64_t)pos * s->hd / 2, 0);
+    if (rnd)
+      for (int64_t i = 0; i < Q + KV; ++i) row[i] = rb(row[i]);
+  }
+  /* causal GQA attention within each sample */
+  a->o = falloc(T * Q);
+  a->lse_attn = falloc(T * s->nh);
+  const float scale = 1.0f / sqrtf((float)s->hd);
+  const int grp = s->nh / s->nkv;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+  for (int b = 0; b < s->B; ++b)
+    for (int h = 0; h < s->nh; ++h) {
+      const int kvh = h / grp;
+      float* p = (float*)malloc(sizeof(float) * s->S);
+      for (int i = 0; i < s->S; ++i) {
+        const int64_t ti = (int64_t)b * s->S + i;
+        const float* q = a->qkv + ti * NQ + (int64_t)h * s->hd;
+        float mx = -INFINITY;
+        for (int j = 0; j <= i; ++j) {
+          const float* k = a->qkv + ((int64_t)b * s->S + j) * NQ + Q + (int64_t)kvh * s->hd;
+          float d = 0.f;
+          for (int c = 0; c < s->hd; ++c) d += q[c] * k[c];
+          p[j] = d * scale;
+          if (p[j] > mx) mx = p[j];
+        }
+        double sum = 0.0;
+        for (int j = 0; j <= i; ++j) {
+          p[j] = expf(p[j] - mx);
+          sum += p[j];
+        }
+        a->lse_attn[ti * s->nh + h] = mx + (float)log(sum);
+        const float inv = (float)(1.0 / sum);
+        float* out = a->o + ti * Q + (int64_t)h * s->hd;
+        for (int c = 0; c < s->hd; ++c) out[c] = 0.f;
+        for (int j = 0; j <= i; ++j) {
+          const float* vv = a->qkv + ((int64_t)b * s->S + j) * NQ + Q + KV + (int64_t)kvh * s->hd;
+          const float pj = p[j] * inv;
+          for (int c = 0; c < s->hd; ++c) out[c] += pj * vv[c];
+        }
+      }
+      free(p);
+    }
+  round_vec(a->o, T * Q, rnd);
+  a->r = falloc(T * H);
+  memcpy(a->r, a->g, sizeof(float) * T * H);
+  mm_nt(T, H, Q, a->o, Q, Wb[ORC_O], Q, a->r, H, 1);
+  round_vec(a->r, T * H, rnd);
+  a->z = falloc(T * H);
+  a->rstd_post = falloc(T);
+  rmsnorm_fwd(T, H, a->r, H, P + off[ORC_W_POST], s->eps, a->z, H, a->rstd_post);
+  round_vec(a->z, T * H, rnd);
+  a->gu = falloc(T * 2 * I);
+  mm_nt(T, 2 * I, H, a->z, H, Wb[ORC_GATE_UP], H, a->gu, 2 * I, 0);
+  round_vec(a->gu, T * 2 * I, rnd);
+  a->act = falloc(T * I);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t i = 0; i < I; ++i) {
+      const float gt = a->gu[t * 2 * I + i], up = a->gu[t * 2 * I + I + i];
+      a->act[t * I + i] = silu(gt) * up;
+    }
+  round_vec(a->act, T * I, rnd);
+  a->h = falloc(T * H);
+  memcpy(a->h, a->r, sizeof(float) * T * H);
+  mm_nt(T, H, I, a->act, I, Wb[ORC_DOWN], I, a->h, H, 1);
+  round_vec(a->h, T * H, rnd);
+  a->nrm = falloc(T * H);
+  a->rstd_fin = falloc(T);
+  rmsnorm_fwd(T, H, a->h, H, P + off[ORC_W_FIN], s->eps, a->nrm, H, a->rstd_fin);
+  round_vec(a->nrm, T * H, rnd);
+  a->dlog = falloc(T * V);
+  mm_nt(T, V, H, a->nrm, H, Wb[ORC_LM], H, a->dlog, V, 0);
+}
+
+/* lse / loss / top-1 from the logits in a->dlog */
+static void ce_stats(const orc_shape* s, acts* a, const int32_t* y, const int32_t* mask,
+                     int64_t global_valid, orc_step_out* out) {
+  const int64_t T = a->T, V = a->V;
+  a->lse = falloc(T);
+  a->argmax = (int32_t*)calloc((size_t)T, sizeof(int32_t));
+  double loss = 0.0;
+  int64_t valid = 0, top1 = 0;
+#pragma omp parallel for schedule(static) reduction(+ : loss, valid, top1)
+  for (int64_t t = 0; t < T; ++t) {
+    const float* l = a->dlog + t * V;
+    float mx = -INFINITY;
+    int32_t am = 0;
+    for (int64_t v = 0; v < V; ++v)
+      if (l[v] > mx) {
+        mx = l[v];
+        am = (int32_t)v;
+      }
+    double sum = 0.0;
+    for (int64_t v = 0; v < V; ++v) sum += exp((double)l[v] - mx);
+    const float lse = mx + (float)log(sum);
+    a->lse[t] = lse;
+    a->argmax[t] = am;
+    if (mask[t]) {
+      loss += (double)lse - l[y[t]];
+      valid += 1;
+      top1 += (am == y[t]);
+    }
+  }
+  const double denom = global_valid > 0 ? (double)global_valid : (double)(valid > 0 ? valid : 1);
+  out->loss = loss / denom;
+  out->valid = valid;
+  out->top1 = top1;
+  (void)s;
+}
+
+static void weights_bf16(const orc_shape* s, const float* P, const int64_t* off, int rnd,
+                         float** Wb) {
+  int64_t rows[ORC_NPARAMS], cols[ORC_NPARAMS];
+  orc_param_layout(s, NULL, rows, cols, NULL);
+  for (int p = 0; p < ORC_NPARAMS; ++p) Wb[p] = wcopy(P + off[p], rows[p] * cols[p], rnd);
+}
+
+int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, const uint16_t* F,
+                const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
+                int round_bf16, orc_step_out* out, float* lse_out, int32_t* argmax_out) {
+  int64_t off[ORC_NPARAMS];
+  orc_param_layout(s, NULL, NULL, NULL, off);
+  float* Wb[ORC_NPARAMS];
+  weights_bf16(s, params, off, round_bf16, Wb);
+  acts a;
+  memset(&a, 0, sizeof(a));
+  forward_core(s, params, off, E, F, u, round_bf16, &a, Wb);
+  ce_stats(s, &a, y, mask, global_valid, out);
+  if (lse_out) memcpy(lse_out, a.lse, sizeof(float) * a.T);
+  if (argmax_out) memcpy(argmax_out, a.argmax, sizeof(int32_t) * a.T);
+  acts_free(&a);
+  for (int p = 0; p < ORC_NPARAMS; ++p) free(Wb[p]);
+  return 0;
+}
+
+void orc_adamw(int64_t n, float* p, float* m, float* v, const float* g, const float* hp,
+               int64_t step_k) {
+  const float lr = hp[0], b1 = hp[1], b2 = hp[2], eps = hp[3], wd = hp[4];
+  const double bc1 = 1.0 - pow((double)b1, (double)step_k);
+  const double bc2 = 1.0 - pow((double)b2, (double)step_k);
+  const float step_size = (float)(lr / bc1);
+  const float bc2_sqrt = (float)sqrt(bc2);
+  const float decay = 1.0f - lr * wd;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const float gi = g[i];
+    float pi = p[i] * decay;
+    const float mi = m[i] + (gi - m[i]) * (1.0f - b1);
+    const float vi = v[i] * b2 + (1.0f - b2) * gi * gi;
+    const float denom = sqrtf(vi) / bc2_sqrt + eps;
+    pi = pi - step_size * (mi / denom);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
+int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, float* params,
+                   float* mst, float* vst, float* grads, const uint16_t* E, const uint16_t* F16,
+                   const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
+                   int rnd, int do_update, orc_step_out* out) {
+  if (s->nh % s->nkv != 0 || s->hd % 2 != 0) return 1;
+  int64_t off[ORC_NPARAMS], rows[ORC_NPARAMS], cols[ORC_NPARAMS];
+  const int64_t total = orc_param_layout(s, NULL, rows, cols, off);
+  float* Wb[ORC_NPARAMS];
+  weights_bf16(s, params, off, rnd, Wb);
+  acts a;
+  memset(&a, 0, sizeof(a));
+  forward_core(s, params, off, E, F16, u, rnd, &a, Wb);
+  ce_stats(s, &a, y, mask, global_valid, out);
+  const int64_t T = a.T, H = a.H, Q = a.Q, KV = a.KV, NQ = a.NQKV, I = a.I, V = a.V, W3 = a.W3;
+  int64_t nvalid = 0;
+  for (int64_t t = 0; t < T; ++t) nvalid += mask[t] ? 1 : 0;
+  const double denom = global_valid > 0 ? (double)global_valid : (double)(nvalid > 0 ? nvalid : 1);
+  memset(grads, 0, sizeof(float) * total);
+
+  /* ---- LM head + CE backward: dlogits = (softmax - onehot) * m / N */
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    float* l = a.dlog + t * V;
+    const float coef = mask[t] ? (float)(1.0 / denom) : 0.f;
+    for (int64_t v = 0; v < V; ++v) {
+      const float p = expf(l[v] - a.lse[t]);
+      float gval = (p - (v == y[t] ? 1.f : 0.f)) * coef;
+      l[v] = rnd ? rb(gval) : gval;
+    }
+  }
+  float* dn = falloc(T * H);
+  mm_nn(T, H, V, a.dlog, V, Wb[ORC_LM], H, dn, H, 0);
+  mm_tn(V, H, T, a.dlog, V, a.nrm, H, grads + off[ORC_LM], H);
+
+  /* ---- final norm */
+  float* dh = falloc(T * H);
+  rmsnorm_bwd(T, H, dn, H, a.h, H, params + off[ORC_W_FIN], a.rstd_fin, dh, H, 0,
+              grads + off[ORC_W_FIN]);
+  float* dh_b = wcopy(dh, T * H, rnd);
+
+  /* ---- MLP */
+  float* dact = falloc(T * I);
+  mm_nn(T, I, H, dh_b, H, Wb[ORC_DOWN], I, dact, I, 0);
+  round_vec(dact, T * I, rnd);
+  mm_tn(H, I, T, dh_b, H, a.act, I, grads + off[ORC_DOWN], I);
+  float* dgu = falloc(T * 2 * I);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t i = 0; i < I; ++i) {
+      const float gt = a.gu[t * 2 * I + i], up = a.gu[t * 2 * I + I + i];
+      const float sg = 1.0f / (1.0f + expf(-gt));
+      const float d = dact[t * I + i];
+      dgu[t * 2 * I + i] = d * up * sg * (1.0f + gt * (1.0f - sg));
+      dgu[t * 2 * I + I + i] = d * gt * sg;
+    }
+  round_vec(dgu, T * 2 * I, rnd);
+  float* dz = falloc(T * H);
+  mm_nn(T, H, 2 * I, dgu, 2 * I, Wb[ORC_GATE_UP], H, dz, H, 0);
+  mm_tn(2 * I, H, T, dgu, 2 * I, a.z, H, grads + off[ORC_GATE_UP], H);
+
+  /* ---- post-attention norm; residual */
+  float* dr = falloc(T * H);
+  memcpy(dr, dh, sizeof(float) * T * H);
+  rmsnorm_bwd(T, H, dz, H, a.r, H, params + off[ORC_W_POST], a.rstd_post, dr, H, 1,
+              grads + off[ORC_W_POST]);
+  float* dr_b = wcopy(dr, T * H, rnd);
+
+  /* ---- o projection */
+  float* dO = falloc(T * Q);
+  mm_nn(T, Q, H, dr_b, H, Wb[ORC_O], Q, dO, Q, 0);
+  round_vec(dO, T * Q, rnd);
+  mm_tn(H, Q, T, dr_b, H, a.o, Q, grads + off[ORC_O], Q);
+
+  /* ---- attention backward */
+  float* dqkv = falloc(T * NQ);
+  const float scale = 1.0f / sqrtf((float)s->hd);
+  const int grp = s->nh / s->nkv;
+  /* dq per (b, h) rows; dk/dv accumulated per (b, kv head) over the group */
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+  for (int b = 0; b < s->B; ++b)
+    for (int kvh = 0; kvh < s->nkv; ++kvh) {
+      float* p = (float*)malloc(sizeof(float) * s->S);
+      float* dp = (float*)malloc(sizeof(float) * s->S);
+      for (int hh = 0; hh < grp; ++hh) {
+        const int h = kvh * grp + hh;
+        for (int i = 0; i < s->S; ++i) {
+          const int64_t ti = (int64_t)b * s->S + i;
+          const float* q = a.qkv + ti * NQ + (int64_t)h * s->hd;
+          const float* dout = dO + ti * Q + (int64_t)h * s->hd;
+          const float* oo = a.o + ti * Q + (int64_t)h * s->hd;
+          const float lse = a.lse_attn[ti * s->nh + h];
+          float Di = 0.f;
+          for (int c = 0; c < s->hd; ++c) Di += dout[c] * oo[c];
+          for (int j = 0; j <= i; ++j) {
+            const int64_t tj = (int64_t)b * s->S + j;
+            const float* k = a.qkv + tj * NQ + Q + (int64_t)kvh * s->hd;
+            const float* vv = a.qkv + tj * NQ + Q + KV + (int64_t)kvh * s->hd;
+            float d = 0.f, e = 0.f;
+            for (int c = 0; c < s->hd; ++c) {
+              d += q[c] * k[c];
+              e += dout[c] * vv[c];
+            }
+            p[j] = expf(d * scale - lse);
+            dp[j] = e;
+          }
+          float* dq = dqkv + ti * NQ + (int64_t)h * s->hd;
+          for (int j = 0; j <= i; ++j) {
+            const int64_t tj = (int64_t)b * s->S + j;
+            const float* k = a.qkv + tj * NQ + Q + (int64_t)kvh * s->hd;
+            float* dk = dqkv + tj * NQ + Q + (int64_t)kvh * s->hd;
+            float* dv = dqkv + tj * NQ + Q + KV + (int64_t)kvh * s->hd;
+            const float ds = p[j] * (dp[j] - Di) * scale;
+            for (int c = 0; c < s->hd; ++c) {
+              dq[c] += ds * k[c];
+              dk[c] += ds * q[c];
+              dv[c] += p[j] * dout[c];
+            }
+          }
+        }
+      }
+      free(p);
+      free(dp);
+    }
+  /* RoPE backward on dq, dk; round to bf16 (GEMM operand) */
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    const int pos = (int)(t % s->S);
+    float* row = dqkv + t * NQ;
+    if (rnd)
+      for (int64_t i = 0; i < NQ; ++i) row[i] = rb(row[i]);
+    rope_row(row, s->nh, s->hd, a.cs + (int64_t)pos * s->hd / 2, a.sn + (int64_t)pos * s->hd / 2, 1);
+    rope_row(row + Q, s->nkv, s->hd, a.cs + (int64_t)pos * s->hd / 2,
+             a.sn + (int64_t)pos * s->hd / 2, 1);
+    if (rnd)
+      for (int64_t i = 0; i < Q + KV; ++i) row[i] = rb(row[i]);
+  }
+  float* dU = falloc(T * 2 * H);
+  mm_nn(T, 2 * H, NQ, dqkv, NQ, Wb[ORC_QKV], 2 * H, dU, 2 * H, 0);
+  mm_tn(NQ, 2 * H, T, dqkv, NQ, a.U, 2 * H, grads + off[ORC_QKV], 2 * H);
+
+  /* ---- input norms (embedding frozen: only dw_in) */
+  rmsnorm_bwd(T, H, dU, 2 * H, a.E_rows, H, params + off[ORC_W_IN], a.rstd_a, NULL, 0, 0,
+              grads + off[ORC_W_IN]);
+  float* dg = dr; /* residual path: dg = dr + d(hidden norm) */
+  rmsnorm_bwd(T, H, dU + H, 2 * H, a.g, H, params + off[ORC_W_HID], a.rstd_b, dg, H, 1,
+              grads + off[ORC_W_HID]);
+  round_vec(dg, T * H, rnd);
+  mm_tn(H, W3, T, dg, H, a.F, W3, grads + off[ORC_FC], W3);
+
+  if (do_update) orc_adamw(total, params, mst, vst, grads, adamw5, step_k);
+
+  free(dn); free(dh); free(dh_b); free(dact); free(dgu); free(dz); free(dr); free(dr_b);
+  free(dO); free(dqkv); free(dU);
+  acts_free(&a);
+  for (int p = 0; p < ORC_NPARAMS; ++p) free(Wb[p]);
+  (void)rows; (void)cols;
+  return 0;
+}

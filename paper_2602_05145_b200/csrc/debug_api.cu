@@ -1,0 +1,80 @@
+// Kernel test hooks: host-buffer wrappers around single device kernels so the
+// parity tests can exercise them through the C ABI (no framework types).
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+#include "gemm.h"
+
+namespace specsim {
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) SPECSIM_CUDA(cudaMalloc(&p, bytes));
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+}  // namespace
+}  // namespace specsim
+
+extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_t N, int32_t K,
+                                  const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb,
+                                  void* C, int64_t ldc, const uint16_t* R, int64_t ldr,
+                                  int32_t iters, float* mean_ms) {
+  using namespace specsim;
+  return guard([&] {
+    Problems pr("specsim_debug_gemm");
+    pr.check(M > 0 && N > 0 && K > 0, "M, N, K must be > 0");
+    pr.check(A && B && C, "A, B, C must be non-null");
+    pr.check(epi >= 0 && epi <= 3, "epi must be 0..3");
+    pr.check(epi != 3 || R, "epi 3 needs R");
+    pr.throw_if_any();
+    const size_t a_elems = static_cast<size_t>(a_mn ? K : M) * lda;
+    const size_t b_elems = static_cast<size_t>(b_mn ? K : N) * ldb;
+    const size_t c_esz = (epi == 1 || epi == 2) ? 4 : 2;
+    const size_t c_bytes = static_cast<size_t>(M) * ldc * c_esz;
+    DevBuf dA(a_elems * 2), dB(b_elems * 2), dC(c_bytes), dR(R ? static_cast<size_t>(M) * ldr * 2 : 0);
+    SPECSIM_CUDA(cudaMemcpy(dA.p, A, a_elems * 2, cudaMemcpyHostToDevice));
+    SPECSIM_CUDA(cudaMemcpy(dB.p, B, b_elems * 2, cudaMemcpyHostToDevice));
+    SPECSIM_CUDA(cudaMemcpy(dC.p, C, c_bytes, cudaMemcpyHostToDevice));
+    if (R) SPECSIM_CUDA(cudaMemcpy(dR.p, R, static_cast<size_t>(M) * ldr * 2, cudaMemcpyHostToDevice));
+    gemm::Args args{};
+    args.C = dC.p;
+    args.ldc = ldc;
+    args.R = static_cast<const __nv_bfloat16*>(dR.p);
+    args.ldr = ldr;
+    gemm::GemmPlan plan = gemm::make_plan({dA.p, lda, a_mn != 0}, {dB.p, ldb, b_mn != 0}, M, N,
+                                          K, epi, args);
+    cudaStream_t s;
+    SPECSIM_CUDA(cudaStreamCreate(&s));
+    plan.launch(s);
+    SPECSIM_CHECK_LAUNCH();
+    SPECSIM_CUDA(cudaStreamSynchronize(s));
+    // Copy the single-launch result out before any timing re-launches
+    // (accumulating epilogues would otherwise compound).
+    SPECSIM_CUDA(cudaMemcpy(C, dC.p, c_bytes, cudaMemcpyDeviceToHost));
+    if (iters > 1 && mean_ms) {
+      cudaEvent_t e0, e1;
+      SPECSIM_CUDA(cudaEventCreate(&e0));
+      SPECSIM_CUDA(cudaEventCreate(&e1));
+      for (int i = 0; i < 3; ++i) plan.launch(s);
+      SPECSIM_CUDA(cudaEventRecord(e0, s));
+      for (int i = 0; i < iters; ++i) plan.launch(s);
+      SPECSIM_CUDA(cudaEventRecord(e1, s));
+      SPECSIM_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      SPECSIM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      *mean_ms = ms / iters;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    SPECSIM_CUDA(cudaStreamDestroy(s));
+  });
+}

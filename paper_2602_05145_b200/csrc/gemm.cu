@@ -1,0 +1,133 @@
+// Host side of the tcgen05 GEMM: TMA tensor-map encoding, plan construction
+// and launch.  A GemmPlan is built once per (operands, shape, epilogue) when a
+// trainer is created; the training step only replays plan.launch().
+#include "gemm.h"
+
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+
+namespace specsim {
+namespace gemm {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading
+// dimension ld (elements), box = {box_cols (inner), box_rows}, 128-byte swizzle.
+CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                     int box_rows) {
+  if ((ld * 2) % 16 != 0) throw std::invalid_argument("gemm: leading dimension not 16B aligned");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    throw std::invalid_argument("gemm: operand pointer not 16B aligned");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
+                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+void launch_t(const GemmPlan& p, cudaStream_t s) {
+  auto k = gemm_kernel<A_MN, B_MN, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_set = true;
+  }
+  k<<<p.grid, NUM_THREADS, SMEM_BYTES, s>>>(p.map_a, p.map_b, p.args);
+}
+
+template <bool A_MN, bool B_MN>
+void dispatch_epi(const GemmPlan& p, cudaStream_t s) {
+  switch (p.epi) {
+    case EPI_BF16: launch_t<A_MN, B_MN, EPI_BF16>(p, s); break;
+    case EPI_F32: launch_t<A_MN, B_MN, EPI_F32>(p, s); break;
+    case EPI_F32_ACC: launch_t<A_MN, B_MN, EPI_F32_ACC>(p, s); break;
+    case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID>(p, s); break;
+    case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD>(p, s); break;
+    case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD>(p, s); break;
+    default: throw std::invalid_argument("gemm: bad epilogue");
+  }
+}
+
+}  // namespace
+
+GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
+                   const Args& extra) {
+  if (M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: empty shape");
+  GemmPlan p;
+  p.a_mn = A.mn_major;
+  p.b_mn = B.mn_major;
+  p.epi = epi;
+  // A: K-major = [M, K] rows; MN-major = [K, M] rows.
+  p.map_a = A.mn_major ? make_map(A.ptr, K, M, A.ld, 64, 64) : make_map(A.ptr, M, K, A.ld, 64, BM);
+  p.map_b = B.mn_major ? make_map(B.ptr, K, N, B.ld, 64, 64) : make_map(B.ptr, N, K, B.ld, 64, BN);
+  p.args = extra;
+  p.args.M = M;
+  p.args.N = N;
+  p.args.K = K;
+  p.args.num_m_blocks = (M + BM - 1) / BM;
+  p.args.num_n_blocks = (N + BN - 1) / BN;
+  p.args.num_tiles = p.args.num_m_blocks * p.args.num_n_blocks;
+  p.grid = p.args.num_tiles < num_sms() ? p.args.num_tiles : num_sms();
+  p.flops = 2.0 * M * static_cast<double>(N) * K;
+  if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
+      epi == EPI_F32_ACC) {
+    if (!p.args.C) throw std::invalid_argument("gemm: missing output");
+    if ((p.args.ldc * (epi == EPI_F32 || epi == EPI_F32_ACC ? 4 : 2)) % 16 != 0)
+      throw std::invalid_argument("gemm: ldc not 16B aligned");
+  }
+  return p;
+}
+
+void GemmPlan::launch(cudaStream_t s) const {
+  if (!a_mn && !b_mn)
+    dispatch_epi<false, false>(*this, s);
+  else if (!a_mn && b_mn)
+    dispatch_epi<false, true>(*this, s);
+  else if (a_mn && b_mn)
+    dispatch_epi<true, true>(*this, s);
+  else
+    dispatch_epi<true, false>(*this, s);
+}
+
+}  // namespace gemm
+}  // namespace specsim

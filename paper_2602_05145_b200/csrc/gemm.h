@@ -1,0 +1,72 @@
+// Host interface of the tcgen05 GEMM (kernel in gemm.cuh).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+namespace specsim {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+
+enum Epi : int {
+  EPI_BF16 = 0,        // C(bf16) = acc
+  EPI_F32 = 1,         // C(f32)  = acc
+  EPI_F32_ACC = 2,     // C(f32) += acc
+  EPI_BF16_RESID = 3,  // C(bf16) = acc + R(bf16)
+  EPI_CE_FWD = 4,      // per-row partial (max, sum exp, target logit, argmax) per N tile
+  EPI_CE_BWD = 5,      // C(bf16) = (exp(acc - lse[row]) - [col == y[row]]) * coef[row]
+};
+
+// Per-(row, N-tile) partial softmax statistics written by EPI_CE_FWD.
+struct CePartial {
+  float max;       // max logit over the tile's valid columns
+  float sum;       // sum exp(logit - max)
+  float target;    // logit of the target column if it lies in this tile, else -inf
+  int32_t argmax;  // global vocabulary index of the (first) max
+};
+
+struct Args {
+  int M, N, K;
+  void* C;
+  long long ldc;  // elements
+  const __nv_bfloat16* R;
+  long long ldr;
+  // cross-entropy epilogues
+  const int32_t* targets;  // [M] target vocabulary ids
+  const float* lse;        // [M] log-sum-exp (bwd)
+  const float* coef;       // [M] mask / global token count (bwd)
+  CePartial* partials;     // [num_n_blocks, M] (fwd)
+  int vocab_offset;        // vocabulary index of output column 0
+  int num_m_blocks, num_n_blocks, num_tiles;
+};
+
+// A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).
+// MN-major: stored [K, MN] row-major (MN contiguous).  ld in elements.
+struct Operand {
+  const void* ptr;
+  long long ld;
+  bool mn_major;
+};
+
+struct GemmPlan {
+  CUtensorMap map_a, map_b;
+  Args args;
+  int epi = 0;
+  bool a_mn = false, b_mn = false;
+  int grid = 0;
+  double flops = 0;
+  void launch(cudaStream_t s) const;
+};
+
+// Throws std::invalid_argument on bad shapes / alignment.
+GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
+                   const Args& extra);
+
+}  // namespace gemm
+}  // namespace specsim
