@@ -1,0 +1,169 @@
+// C++ API of the B200-native TIDE draft-training hot path.
+//
+// Namespace, error taxonomy (ConfigError vs std::invalid_argument,
+// errors.hpp:8-13) and the seeded Rng semantics (rng.hpp:13-39) follow the
+// reference; the classes implement the seams SPEC.md describes but the
+// reference never implemented: the signal buffer (SPEC.md:237-241, 267-275,
+// 341-344) and the trainer actor train(job) -> TrainingOutcome
+// (SPEC.md:380-405).  The C ABI in ../specsim_draft_trainer.h wraps these.
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace specsim {
+
+// ------------------------------------------------------------------ Rng
+// Seeded mt19937_64 with hand-rolled conversions so a seed reproduces the
+// same stream as the reference's specsim::Rng.
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : eng_(seed) {}
+  uint64_t next_u64() { return eng_(); }
+  double uniform();                       // [0, 1), 53 bits
+  double normal(double mean, double sd);  // Box-Muller, cosine branch
+  long long geometric(double mean);       // {1, 2, ...}
+
+ private:
+  std::mt19937_64 eng_;
+};
+
+double expected_accept_length(double alpha, int gamma);
+int sample_accept_length(Rng& rng, double alpha, int gamma);
+double alpha_from_accept_length(double ell, int gamma);
+// oldest floor(9n/10) samples train, the rest evaluate.
+void split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
+
+struct SignalGeometry {
+  int hidden_dim = 0;
+  int layers_tapped = 3;
+  int bytes_per_element = 2;
+  int64_t bytes_per_token() const;
+  void validate() const;  // throws std::invalid_argument
+};
+
+// Synthetic captured request; stream Rng(seed + index).
+struct SynthCapture {
+  std::vector<int32_t> ids;
+  std::vector<uint16_t> features;  // [length, layers * hidden] bf16 bits
+  std::vector<int32_t> accept_lengths;
+  double alpha_s = 0;
+};
+void synth_capture(uint64_t seed, int64_t index, int length, int vocab, int hidden, int layers,
+                   double alpha, int gamma, int32_t* ids, uint16_t* features,
+                   int32_t* accept_lengths, int32_t* n_steps, double* alpha_s);
+
+// ---------------------------------------------------- hidden-state buffer
+class HiddenStateBuffer {
+ public:
+  struct Stats {
+    int64_t records = 0, bytes = 0, flushes = 0, cumulative_bytes = 0, samples = 0,
+            resident_tokens = 0;
+  };
+  struct Sample {
+    int64_t start = 0;  // ring row of token 0
+    int32_t length = 0;
+    double alpha = 0;
+  };
+
+  HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_tokens, int64_t flush_threshold,
+                    int device);
+  ~HiddenStateBuffer();
+  HiddenStateBuffer(const HiddenStateBuffer&) = delete;
+  HiddenStateBuffer& operator=(const HiddenStateBuffer&) = delete;
+
+  // extract_signals + record_sample (one verify step of one request).
+  void append(int64_t sample_id, double alpha, const void* const* layer_ptrs, int64_t rows,
+              int64_t ld, const int32_t* token_ids, const int32_t* accepted_idx, int n,
+              bool on_device);
+  void append_packed(int64_t sample_id, double alpha, const uint16_t* features,
+                     const int32_t* token_ids, int n, bool on_device);
+
+  Stats stats() const { return stats_; }
+  const Sample& sample(int64_t id) const;  // throws std::out_of_range if evicted/unknown
+  void read_sample(int64_t id, uint16_t* features, int32_t* ids) const;
+
+  const SignalGeometry& geometry() const { return geom_; }
+  int64_t capacity() const { return cap_; }
+  const void* ring_features() const { return ring_feat_; }
+  const int32_t* ring_ids() const { return ring_ids_; }
+  int device() const { return device_; }
+  void* stream() const { return stream_; }
+
+ private:
+  void open_sample(int64_t sample_id, double alpha);
+  void reserve(int n);  // evict oldest samples so n more tokens fit
+  void account(int n);  // extract_signals byte accounting
+
+  SignalGeometry geom_;
+  int64_t cap_, flush_threshold_;
+  int device_;
+  void* stream_ = nullptr;
+  void* ring_feat_ = nullptr;
+  int32_t* ring_ids_ = nullptr;
+  void* staging_dev_ = nullptr;   // device staging for host appends
+  void* staging_host_ = nullptr;  // pinned staging
+  size_t staging_bytes_ = 0;
+  int64_t head_ = 0;  // next free ring row (monotonic; row = head % cap)
+  int64_t tail_ = 0;  // oldest resident row (monotonic)
+  int64_t open_id_ = -1;
+  std::unordered_map<int64_t, Sample> samples_;  // resident samples by id
+  std::deque<int64_t> order_;                   // resident sample ids, oldest first
+  Stats stats_;
+};
+
+// ------------------------------------------------------------- trainer
+struct DraftShape {
+  int hidden = 0, vocab = 0, seq_len = 0, n_heads = 0, n_kv_heads = 0, head_dim = 0, ffn = 0,
+      layers_tapped = 3, micro_batch = 1;
+  float rms_eps = 1e-5f;
+  double rope_theta = 10000.0;
+  void validate() const;  // collects every problem, throws std::invalid_argument
+};
+
+struct AdamWConfig {
+  float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.f;
+};
+
+struct StepResult {
+  double loss = 0;
+  int64_t valid_tokens = 0, top1_correct = 0, positions = 0;
+  double ms = 0;
+};
+
+struct TrainJob {
+  std::vector<int64_t> train_ids, eval_ids;
+  int epochs = 1;
+};
+
+struct TrainingOutcome {
+  double duration_hours = 0;
+  double alpha_eval = 0;
+  int64_t new_version = 0;
+  double mean_loss = 0;
+  int64_t steps = 0;
+};
+
+class DraftTrainerImpl;
+
+class DraftTrainer {
+ public:
+  DraftTrainer(const DraftShape& shape, const AdamWConfig& opt, uint64_t seed, int rank,
+               int world, const uint8_t* nccl_id, int device);
+  ~DraftTrainer();
+  StepResult step(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid);
+  StepResult eval(HiddenStateBuffer& buf, const int64_t* ids, int n);
+  TrainingOutcome train(HiddenStateBuffer& buf, const TrainJob& job);
+  DraftTrainerImpl& impl() { return *impl_; }
+  const DraftTrainerImpl& impl() const { return *impl_; }
+
+ private:
+  std::unique_ptr<DraftTrainerImpl> impl_;
+};
+
+}  // namespace specsim

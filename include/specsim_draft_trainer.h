@@ -249,6 +249,12 @@ int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_t N, int32_
                        const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb, void* C,
                        int64_t ldc, const uint16_t* R, int64_t ldr, int32_t iters,
                        float* mean_ms);
+/* Attention forward (+ backward when dout/dqkv are non-null) on host
+ * buffers: qkv [B*S, (nh+2*nkv)*hd] bf16 with RoPE already applied, o
+ * [B*S, nh*hd], lse [nh, B*S] (natural log), dqkv like qkv. */
+int specsim_debug_attention(int32_t B, int32_t S, int32_t nh, int32_t nkv, int32_t hd,
+                            const uint16_t* qkv, const uint16_t* dout, uint16_t* o, float* lse,
+                            uint16_t* dqkv);
 
 #ifdef __cplusplus
 }

@@ -111,6 +111,7 @@ SIGNATURES = {
     "specsim_trainer_phase_times": [P, PF64, PF64, PI32],
     "specsim_debug_gemm": [C.c_int, C.c_int, C.c_int, I32, I32, I32, P, I64, P, I64, P, I64, P,
                            I64, I32, PF32],
+    "specsim_debug_attention": [I32, I32, I32, I32, I32, P, P, P, P, P],
 }
 _RESTYPE = {"specsim_last_error": C.c_char_p, "specsim_version": C.c_char_p}
 

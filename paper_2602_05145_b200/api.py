@@ -1,0 +1,304 @@
+"""Python mirror of the reference-facing interface (thin ctypes wrappers).
+
+Names follow the reference's domain: SignalGeometry,
+extract_signals / record_sample, train(job) ->
+TrainingOutcome, the perf_model bookkeeping
+(perf_model.hpp:52-80) and the seeded Rng (rng.hpp:13-39).  Every call goes
+through the C ABI of libspecsim_draft.so; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import call, ptr
+
+# ------------------------------------------------------------- configs
+CONFIGS = {
+    # BASELINE.json configs; head / FFN dims from SURVEY §8 (public HF configs)
+    "C1": dict(hidden=256, vocab=4096, seq_len=128, n_heads=4, n_kv_heads=2, head_dim=64,
+               ffn=1024, micro_batch=8, rms_eps=1e-5, rope_theta=10000.0),
+    "C2": dict(hidden=4096, vocab=128256, seq_len=2048, n_heads=32, n_kv_heads=8, head_dim=128,
+               ffn=14336, micro_batch=4, rms_eps=1e-5, rope_theta=500000.0),
+    "C4": dict(hidden=5120, vocab=151936, seq_len=2048, n_heads=64, n_kv_heads=8, head_dim=128,
+               ffn=25600, micro_batch=4, rms_eps=1e-6, rope_theta=1000000.0),
+    "C5": dict(hidden=8192, vocab=128256, seq_len=4096, n_heads=64, n_kv_heads=8, head_dim=128,
+               ffn=28672, micro_batch=2, rms_eps=1e-5, rope_theta=500000.0),
+}
+
+
+def gemm_flops_per_token(c: dict) -> dict:
+    """Algorithmic FLOPs per processed token (SURVEY §8(d) convention)."""
+    H, V, S = c["hidden"], c["vocab"], c["seq_len"]
+    Q = c["n_heads"] * c["head_dim"]
+    KV = c["n_kv_heads"] * c["head_dim"]
+    I = c["ffn"]
+    L = c.get("layers_tapped", 3)
+    gemm_fwd = 2 * (L * H * H + 2 * H * (Q + 2 * KV) + Q * H + 3 * H * I + H * V)
+    attn_fwd = 2 * Q * (S + 1)
+    fwd = gemm_fwd + attn_fwd
+    bwd = 2 * gemm_fwd - 2 * (L * H * H) + 2 * attn_fwd
+    lm = 2 * H * V
+    return dict(total=fwd + bwd, gemm=3 * gemm_fwd - 2 * L * H * H, attn=3 * attn_fwd,
+                lm=3 * lm, decoder_gemm=3 * gemm_fwd - 2 * L * H * H - 3 * lm)
+
+
+# ------------------------------------------------------------ bookkeeping
+class Rng:
+    """The library's seeded Rng (bit-compatible with the reference)."""
+
+    def __init__(self, seed: int):
+        self.h = C.c_void_p()
+        call("specsim_rng_create", seed, C.byref(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.lib().specsim_rng_destroy(self.h)
+            self.h = None
+
+    def uniform(self) -> float:
+        o = C.c_double()
+        call("specsim_rng_uniform", self.h, C.byref(o))
+        return o.value
+
+    def normal(self, mean: float, sd: float) -> float:
+        o = C.c_double()
+        call("specsim_rng_normal", self.h, mean, sd, C.byref(o))
+        return o.value
+
+    def geometric(self, mean: float) -> int:
+        o = C.c_int64()
+        call("specsim_rng_geometric", self.h, mean, C.byref(o))
+        return o.value
+
+    def next_u64(self) -> int:
+        o = C.c_uint64()
+        call("specsim_rng_next_u64", self.h, C.byref(o))
+        return o.value
+
+    def sample_accept_length(self, alpha: float, gamma: int) -> int:
+        o = C.c_int32()
+        call("specsim_sample_accept_length", self.h, alpha, gamma, C.byref(o))
+        return o.value
+
+
+def expected_accept_length(alpha: float, gamma: int) -> float:
+    o = C.c_double()
+    call("specsim_expected_accept_length", alpha, gamma, C.byref(o))
+    return o.value
+
+
+def alpha_from_accept_length(ell: float, gamma: int) -> float:
+    o = C.c_double()
+    call("specsim_alpha_from_accept_length", ell, gamma, C.byref(o))
+    return o.value
+
+
+def split_train_eval(n: int):
+    a, b = C.c_int64(), C.c_int64()
+    call("specsim_split_train_eval", n, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+@dataclass
+class SignalGeometry:
+    hidden_dim: int
+    layers_tapped: int = 3
+    bytes_per_element: int = 2
+
+    def c(self):
+        return _lib.SignalGeometry(self.hidden_dim, self.layers_tapped, self.bytes_per_element)
+
+    def bytes_per_token(self) -> int:
+        o = C.c_int64()
+        g = self.c()
+        call("specsim_bytes_per_token", C.byref(g), C.byref(o))
+        return o.value
+
+
+def synth_capture(seed, index, length, vocab, hidden, layers=3, alpha=0.6, gamma=3,
+                  features=True):
+    ids = np.zeros(length, np.int32)
+    feats = np.zeros((length, layers * hidden), np.uint16) if features else None
+    acc = np.zeros(length, np.int32)
+    n = C.c_int32()
+    a_s = C.c_double()
+    call("specsim_synth_capture", seed, index, length, vocab, hidden, layers, alpha, gamma,
+         ptr(ids), ptr(feats), ptr(acc), C.byref(n), C.byref(a_s))
+    return dict(ids=ids, features=feats, accept_lengths=acc[: n.value].copy(), alpha_s=a_s.value)
+
+
+# --------------------------------------------------------- signal buffer
+class HiddenStateBuffer:
+    def __init__(self, geometry: SignalGeometry, capacity_tokens: int, flush_threshold: int = 0,
+                 device: int = 0):
+        self.geometry = geometry
+        self.h = C.c_void_p()
+        g = geometry.c()
+        call("specsim_hsbuf_create", C.byref(g), capacity_tokens, flush_threshold, device,
+             C.byref(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().specsim_hsbuf_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def extract_signals(self, sample_id, alpha, layers, token_ids, accepted_idx=None,
+                        on_device=False):
+        """One verify step: layers = list of [rows, H] uint16 (bf16) arrays."""
+        layers = [np.ascontiguousarray(l) for l in layers]
+        rows, ld = layers[0].shape
+        arr = (C.c_void_p * len(layers))(*[l.ctypes.data for l in layers])
+        ids = np.ascontiguousarray(token_ids, np.int32)
+        idx = None if accepted_idx is None else np.ascontiguousarray(accepted_idx, np.int32)
+        n = len(ids)
+        call("specsim_hsbuf_append", self.h, sample_id, alpha, C.cast(arr, C.POINTER(C.c_void_p)),
+             rows, ld, ptr(ids), ptr(idx), n, 1 if on_device else 0)
+
+    def append_packed(self, sample_id, alpha, features, token_ids):
+        f = np.ascontiguousarray(features, np.uint16)
+        ids = np.ascontiguousarray(token_ids, np.int32)
+        call("specsim_hsbuf_append_packed", self.h, sample_id, alpha, ptr(f), ptr(ids), len(ids), 0)
+
+    def stats(self) -> dict:
+        s = _lib.HsbufStats()
+        call("specsim_hsbuf_stats_get", self.h, C.byref(s))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def sample_info(self, sample_id):
+        n = C.c_int32()
+        a = C.c_double()
+        call("specsim_hsbuf_sample_info", self.h, sample_id, C.byref(n), C.byref(a))
+        return n.value, a.value
+
+    def read_sample(self, sample_id):
+        n, _ = self.sample_info(sample_id)
+        W = self.geometry.hidden_dim * self.geometry.layers_tapped
+        f = np.zeros((n, W), np.uint16)
+        ids = np.zeros(n, np.int32)
+        call("specsim_hsbuf_read_sample", self.h, sample_id, ptr(f), ptr(ids))
+        return f, ids
+
+
+# ---------------------------------------------------------------- trainer
+@dataclass
+class TrainingOutcome:
+    duration_hours: float
+    alpha_eval: float
+    new_version: int
+    mean_loss: float
+    steps: int
+
+
+class DraftTrainer:
+    PHASES = ("ingest", "gemm", "attention", "elementwise", "lm_head_ce", "adamw", "allreduce")
+
+    def __init__(self, shape: dict, lr=1e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0,
+                 seed=20260217, rank=0, world=1, nccl_id: bytes | None = None, device=0):
+        self.shape = dict(shape)
+        s = _lib.DraftShape(shape["hidden"], shape["vocab"], shape["seq_len"], shape["n_heads"],
+                            shape["n_kv_heads"], shape["head_dim"], shape["ffn"],
+                            shape.get("layers_tapped", 3), shape["micro_batch"],
+                            shape.get("rms_eps", 1e-5), shape.get("rope_theta", 10000.0))
+        a = _lib.AdamW(lr, betas[0], betas[1], eps, weight_decay)
+        self.h = C.c_void_p()
+        nid = None
+        if nccl_id is not None:
+            nid = C.create_string_buffer(bytes(nccl_id), 128)
+        call("specsim_trainer_create", C.byref(s), C.byref(a), seed, rank, world,
+             C.cast(nid, C.c_void_p) if nid is not None else None, device, C.byref(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().specsim_trainer_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        b = C.create_string_buffer(128)
+        call("specsim_nccl_unique_id", C.cast(b, C.c_void_p))
+        return b.raw
+
+    @staticmethod
+    def _res(r):
+        return dict(loss=r.loss, valid_tokens=r.valid_tokens, top1_correct=r.top1_correct,
+                    positions=r.positions, ms=r.ms)
+
+    def step(self, buf: HiddenStateBuffer, sample_ids, global_valid=0):
+        ids = np.ascontiguousarray(sample_ids, np.int64)
+        r = _lib.StepResult()
+        call("specsim_trainer_step", self.h, buf.h, ids.ctypes.data_as(_lib.PI64), len(ids),
+             global_valid, C.byref(r))
+        return self._res(r)
+
+    def eval(self, buf: HiddenStateBuffer, sample_ids):
+        ids = np.ascontiguousarray(sample_ids, np.int64)
+        r = _lib.StepResult()
+        call("specsim_trainer_eval", self.h, buf.h, ids.ctypes.data_as(_lib.PI64), len(ids),
+             C.byref(r))
+        return self._res(r)
+
+    def train(self, buf, train_ids, eval_ids, epochs=1) -> TrainingOutcome:
+        t = np.ascontiguousarray(train_ids, np.int64)
+        e = np.ascontiguousarray(eval_ids, np.int64)
+        o = _lib.TrainingOutcome()
+        call("specsim_trainer_train", self.h, buf.h, t.ctypes.data_as(_lib.PI64), len(t),
+             e.ctypes.data_as(_lib.PI64), len(e), epochs, C.byref(o))
+        return TrainingOutcome(o.duration_hours, o.alpha_eval, o.new_version, o.mean_loss, o.steps)
+
+    def params(self):
+        n = C.c_int32()
+        tot = C.c_int64()
+        call("specsim_trainer_num_params", self.h, C.byref(n), C.byref(tot))
+        out = []
+        for i in range(n.value):
+            nm = C.c_char_p()
+            r, c = C.c_int64(), C.c_int64()
+            call("specsim_trainer_param_info", self.h, i, C.byref(nm), C.byref(r), C.byref(c))
+            out.append((nm.value.decode(), r.value, c.value))
+        return out, tot.value
+
+    def get_param(self, name):
+        shp = {n: (r, c) for n, r, c in self.params()[0]}[name]
+        a = np.zeros(shp, np.float32)
+        call("specsim_trainer_get_param", self.h, name.encode(), ptr(a))
+        return a
+
+    def set_param(self, name, value):
+        a = np.ascontiguousarray(value, np.float32)
+        call("specsim_trainer_set_param", self.h, name.encode(), ptr(a))
+
+    def get_grad(self, name):
+        shp = {n: (r, c) for n, r, c in self.params()[0]}[name]
+        a = np.zeros(shp, np.float32)
+        call("specsim_trainer_get_grad", self.h, name.encode(), ptr(a))
+        return a
+
+    def set_embedding(self, e_bf16):
+        a = np.ascontiguousarray(e_bf16, np.uint16)
+        call("specsim_trainer_set_embedding", self.h, ptr(a))
+
+    def get_embedding(self):
+        a = np.zeros((self.shape["vocab"], self.shape["hidden"]), np.uint16)
+        call("specsim_trainer_get_embedding", self.h, ptr(a))
+        return a
+
+    def set_step_count(self, k):
+        call("specsim_trainer_set_step_count", self.h, k)
+
+    def set_timing(self, on: bool):
+        call("specsim_trainer_set_timing", self.h, 1 if on else 0)
+
+    def phase_times(self):
+        ms = (C.c_double * 7)()
+        fl = (C.c_double * 7)()
+        ln = (C.c_int32 * 7)()
+        call("specsim_trainer_phase_times", self.h, ms, fl, ln)
+        return {p: dict(ms=ms[i], flops=fl[i], launches=ln[i]) for i, p in enumerate(self.PHASES)}

@@ -1,9 +1,11 @@
 // Kernel test hooks: host-buffer wrappers around single device kernels so the
 // parity tests can exercise them through the C ABI (no framework types).
+#include <cmath>
 #include <cstring>
 #include <vector>
 
 #include "common.h"
+#include "attention.h"
 #include "gemm.h"
 
 namespace specsim {
@@ -76,5 +78,42 @@ extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_
       cudaEventDestroy(e1);
     }
     SPECSIM_CUDA(cudaStreamDestroy(s));
+  });
+}
+
+extern "C" int specsim_debug_attention(int32_t B, int32_t S, int32_t nh, int32_t nkv, int32_t hd,
+                                       const uint16_t* qkv, const uint16_t* dout, uint16_t* o,
+                                       float* lse, uint16_t* dqkv) {
+  using namespace specsim;
+  return guard([&] {
+    attn::Dims d;
+    d.B = B;
+    d.S = S;
+    d.nh = nh;
+    d.nkv = nkv;
+    d.Q = nh * hd;
+    d.KV = nkv * hd;
+    d.NQ = d.Q + 2 * d.KV;
+    d.scale = 1.0f / std::sqrt(static_cast<float>(hd));
+    attn::check_dims(d, hd);
+    if (!qkv || !o || !lse) throw std::invalid_argument("null argument");
+    const size_t T = static_cast<size_t>(B) * S;
+    DevBuf dq(T * d.NQ * 2), dO(T * d.Q * 2), dl(T * nh * 4), ddo(T * d.Q * 2),
+        ddq(T * d.NQ * 2), dD(T * nh * 4);
+    SPECSIM_CUDA(cudaMemcpy(dq.p, qkv, T * d.NQ * 2, cudaMemcpyHostToDevice));
+    attn::forward(static_cast<const __nv_bfloat16*>(dq.p), static_cast<__nv_bfloat16*>(dO.p),
+                  static_cast<float*>(dl.p), d, hd, 0);
+    SPECSIM_CHECK_LAUNCH();
+    if (dout && dqkv) {
+      SPECSIM_CUDA(cudaMemcpy(ddo.p, dout, T * d.Q * 2, cudaMemcpyHostToDevice));
+      attn::backward(static_cast<const __nv_bfloat16*>(dq.p), static_cast<const __nv_bfloat16*>(dO.p),
+                     static_cast<const __nv_bfloat16*>(ddo.p), static_cast<const float*>(dl.p),
+                     static_cast<float*>(dD.p), static_cast<__nv_bfloat16*>(ddq.p), d, hd, 0);
+      SPECSIM_CHECK_LAUNCH();
+    }
+    SPECSIM_CUDA(cudaDeviceSynchronize());
+    SPECSIM_CUDA(cudaMemcpy(o, dO.p, T * d.Q * 2, cudaMemcpyDeviceToHost));
+    SPECSIM_CUDA(cudaMemcpy(lse, dl.p, T * nh * 4, cudaMemcpyDeviceToHost));
+    if (dout && dqkv) SPECSIM_CUDA(cudaMemcpy(dqkv, ddq.p, T * d.NQ * 2, cudaMemcpyDeviceToHost));
   });
 }

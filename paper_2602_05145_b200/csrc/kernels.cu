@@ -1,0 +1,543 @@
+// HBM-bound kernels of the draft-training step.  See kernels.h.
+#include "common.h"
+#include "kernels.h"
+
+namespace specsim {
+namespace kern {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = __bfloat1622float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+  return q;
+}
+
+unsigned blocks_for(long long n, int per_block) {
+  return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+// ------------------------------------------------------------ batch gather
+__global__ void gather_batch_kernel(const uint4* __restrict__ ring_feat,
+                                    const int32_t* __restrict__ ring_ids, long long cap, int W8,
+                                    BatchSpec spec, int S, uint4* __restrict__ F,
+                                    int32_t* __restrict__ u, int32_t* __restrict__ y,
+                                    int32_t* __restrict__ m) {
+  const long long row = blockIdx.x;
+  const int b = static_cast<int>(row / S), t = static_cast<int>(row % S);
+  const int L = b < spec.n ? spec.len[b] : 0;
+  uint4* dst = F + row * W8;
+  if (t < L) {
+    const long long r = (spec.start[b] + t) % cap;
+    const uint4* src = ring_feat + r * W8;
+    for (int i = threadIdx.x; i < W8; i += blockDim.x) dst[i] = src[i];
+  } else {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < W8; i += blockDim.x) dst[i] = z;
+  }
+  if (threadIdx.x == 0) {
+    const long long base = b < spec.n ? spec.start[b] : 0;
+    u[row] = (t + 1 < L) ? ring_ids[(base + t + 1) % cap] : 0;
+    y[row] = (t + 2 < L) ? ring_ids[(base + t + 2) % cap] : 0;
+    m[row] = (t + 2 < L) ? 1 : 0;
+  }
+}
+
+__global__ void mask_count_kernel(const int32_t* __restrict__ m, long long T, long long* out) {
+  __shared__ long long part[32];
+  long long c = 0;
+  for (long long i = threadIdx.x; i < T; i += blockDim.x) c += m[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffff, c, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) s += part[i];
+    *out = s;
+  }
+}
+
+__global__ void ce_coef_kernel(const int32_t* __restrict__ m, const long long* __restrict__ n,
+                               float* __restrict__ coef, long long T) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  const long long N = *n > 0 ? *n : 1;
+  coef[i] = m[i] ? static_cast<float>(1.0 / static_cast<double>(N)) : 0.f;
+}
+
+// ------------------------------------------------------------ RMSNorm fwd
+constexpr int kNormThreads = 128;
+constexpr int kMaxChunks = 8;  // H <= 128 * 8 * 8 = 8192
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) s += red[i];
+  return s;
+}
+
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, long long ldx, const int32_t* __restrict__ gather,
+    const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ y, long long ldy,
+    float* __restrict__ rstd, int H) {
+  __shared__ float red[kNormThreads / 32];
+  const long long t = blockIdx.x;
+  const long long src_row = gather ? gather[t] : t;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + src_row * ldx);
+  const int H8 = H >> 3;
+  float v[kMaxChunks][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) {
+    const int c = threadIdx.x + k * kNormThreads;
+    if (c < H8) {
+      unpack8(xr[c], v[k]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
+    }
+  }
+  ss = block_sum(ss, red);
+  const float r = rsqrtf(ss / static_cast<float>(H) + eps);
+  if (threadIdx.x == 0) rstd[t] = r;
+  uint4* yr = reinterpret_cast<uint4*>(y + t * ldy);
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) {
+    const int c = threadIdx.x + k * kNormThreads;
+    if (c < H8) {
+      const float4 wa = w4[2 * c], wb = w4[2 * c + 1];
+      const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = v[k][j] * r * wv[j];
+      yr[c] = pack8(o);
+    }
+  }
+}
+
+// ------------------------------------------------------------ RMSNorm bwd
+constexpr int kBwdRows = 16;  // rows per CTA (dw partial granularity)
+
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
+    const float* __restrict__ dy, long long lddy, const __nv_bfloat16* __restrict__ x,
+    long long ldx, const int32_t* __restrict__ gather, const float* __restrict__ w,
+    const float* __restrict__ rstd, const float* __restrict__ resid, float* __restrict__ out32,
+    __nv_bfloat16* __restrict__ out16, long long ldo, float* __restrict__ dw_part, long long T,
+    int H) {
+  __shared__ float red[kNormThreads / 32];
+  const int H8 = H >> 3;
+  float dwacc[kMaxChunks][8];
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dwacc[k][j] = 0.f;
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+  const bool need_dx = out32 || out16;
+  const long long t0 = static_cast<long long>(blockIdx.x) * kBwdRows;
+  for (long long t = t0; t < t0 + kBwdRows && t < T; ++t) {
+    const long long src_row = gather ? gather[t] : t;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + src_row * ldx);
+    const float4* gr = reinterpret_cast<const float4*>(dy + t * lddy);
+    const float r = rstd[t];
+    float xv[kMaxChunks][8], gw[kMaxChunks][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxChunks; ++k) {
+      const int c = threadIdx.x + k * kNormThreads;
+      if (c < H8) {
+        unpack8(xr[c], xv[k]);
+        const float4 ga = gr[2 * c], gb = gr[2 * c + 1];
+        const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float4 wa = w4[2 * c], wb = w4[2 * c + 1];
+        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          dwacc[k][j] += gv[j] * xv[k][j] * r;
+          gw[k][j] = gv[j] * wv[j];
+          dot += gw[k][j] * xv[k][j];
+        }
+      }
+    }
+    if (!need_dx) continue;
+    dot = block_sum(dot, red);
+    const float c3 = dot / static_cast<float>(H) * r * r * r;
+#pragma unroll
+    for (int k = 0; k < kMaxChunks; ++k) {
+      const int c = threadIdx.x + k * kNormThreads;
+      if (c < H8) {
+        float o[8];
+        float rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (resid) {
+          const float4 ra = reinterpret_cast<const float4*>(resid + t * ldo)[2 * c];
+          const float4 rb = reinterpret_cast<const float4*>(resid + t * ldo)[2 * c + 1];
+          rv[0] = ra.x; rv[1] = ra.y; rv[2] = ra.z; rv[3] = ra.w;
+          rv[4] = rb.x; rv[5] = rb.y; rv[6] = rb.z; rv[7] = rb.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rv[j] + (r * gw[k][j] - xv[k][j] * c3);
+        if (out32) {
+          float4* op = reinterpret_cast<float4*>(out32 + t * ldo);
+          op[2 * c] = make_float4(o[0], o[1], o[2], o[3]);
+          op[2 * c + 1] = make_float4(o[4], o[5], o[6], o[7]);
+        }
+        if (out16) reinterpret_cast<uint4*>(out16 + t * ldo)[c] = pack8(o);
+      }
+    }
+  }
+  float4* dp = reinterpret_cast<float4*>(dw_part + static_cast<long long>(blockIdx.x) * H);
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) {
+    const int c = threadIdx.x + k * kNormThreads;
+    if (c < H8) {
+      dp[2 * c] = make_float4(dwacc[k][0], dwacc[k][1], dwacc[k][2], dwacc[k][3]);
+      dp[2 * c + 1] = make_float4(dwacc[k][4], dwacc[k][5], dwacc[k][6], dwacc[k][7]);
+    }
+  }
+}
+
+// dw[i] = sum over partial rows (fixed order)
+__global__ void colsum_kernel(const float* __restrict__ part, long long rows, int H,
+                              float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= H) return;
+  float s = 0.f;
+  for (long long r = 0; r < rows; ++r) s += part[r * H + i];
+  out[i] = s;
+}
+
+// ------------------------------------------------------------------ RoPE
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, long long T, int S, int NQ,
+                            int n_rot_heads, int hd, const float* __restrict__ cos_t,
+                            const float* __restrict__ sin_t, int inverse) {
+  const int half = hd >> 1;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long per_row = static_cast<long long>(n_rot_heads) * (half >> 1);  // pairs of i
+  if (idx >= T * per_row) return;
+  const long long t = idx / per_row;
+  const int rem = static_cast<int>(idx % per_row);
+  const int h = rem / (half >> 1);
+  const int i = (rem % (half >> 1)) * 2;  // two consecutive rotation indices
+  const int pos = static_cast<int>(t % S);
+  __nv_bfloat16* v = qkv + t * NQ + static_cast<long long>(h) * hd;
+  const float2 x1 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(v + i));
+  const float2 x2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(v + i + half));
+  const float c0 = cos_t[pos * half + i], c1 = cos_t[pos * half + i + 1];
+  const float s0 = sin_t[pos * half + i], s1 = sin_t[pos * half + i + 1];
+  float a0, a1, b0, b1;
+  if (!inverse) {
+    a0 = x1.x * c0 - x2.x * s0;
+    a1 = x1.y * c1 - x2.y * s1;
+    b0 = x2.x * c0 + x1.x * s0;
+    b1 = x2.y * c1 + x1.y * s1;
+  } else {
+    a0 = x1.x * c0 + x2.x * s0;
+    a1 = x1.y * c1 + x2.y * s1;
+    b0 = x2.x * c0 - x1.x * s0;
+    b1 = x2.y * c1 - x1.y * s1;
+  }
+  *reinterpret_cast<__nv_bfloat162*>(v + i) = __floats2bfloat162_rn(a0, a1);
+  *reinterpret_cast<__nv_bfloat162*>(v + i + half) = __floats2bfloat162_rn(b0, b1);
+}
+
+// ---------------------------------------------------------------- SwiGLU
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ act, long long T, int I) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int I8 = I >> 3;
+  if (idx >= T * I8) return;
+  const long long t = idx / I8;
+  const int c = static_cast<int>(idx % I8);
+  float g[8], u[8], o[8];
+  unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * I)[c], g);
+  unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * I + I)[c], u);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
+  reinterpret_cast<uint4*>(act + t * I)[c] = pack8(o);
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                  const __nv_bfloat16* __restrict__ dact,
+                                  __nv_bfloat16* __restrict__ dgu, long long T, int I) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int I8 = I >> 3;
+  if (idx >= T * I8) return;
+  const long long t = idx / I8;
+  const int c = static_cast<int>(idx % I8);
+  float g[8], u[8], d[8], dg[8], du[8];
+  unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * I)[c], g);
+  unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * I + I)[c], u);
+  unpack8(reinterpret_cast<const uint4*>(dact + t * I)[c], d);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float sg = 1.f / (1.f + __expf(-g[j]));
+    dg[j] = d[j] * u[j] * sg * (1.f + g[j] * (1.f - sg));
+    du[j] = d[j] * g[j] * sg;
+  }
+  reinterpret_cast<uint4*>(dgu + t * 2 * I)[c] = pack8(dg);
+  reinterpret_cast<uint4*>(dgu + t * 2 * I + I)[c] = pack8(du);
+}
+
+// ------------------------------------------------------------ CE reduce
+__global__ void ce_reduce_kernel(const gemm::CePartial* __restrict__ part, int num_nb, long long T,
+                                 const int32_t* __restrict__ y, const int32_t* __restrict__ m,
+                                 float* __restrict__ lse, float* __restrict__ row_loss,
+                                 int32_t* __restrict__ argmax) {
+  const long long t = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  float mx = -INFINITY, tg = -INFINITY;
+  int am = 0x7fffffff;
+  for (int nb = lane; nb < num_nb; nb += 32) {
+    const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
+    if (p.max > mx || (p.max == mx && p.argmax < am)) {
+      mx = p.max;
+      am = p.argmax;
+    }
+    tg = fmaxf(tg, p.target);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float omx = __shfl_xor_sync(0xffffffff, mx, o);
+    const int oam = __shfl_xor_sync(0xffffffff, am, o);
+    if (omx > mx || (omx == mx && oam < am)) {
+      mx = omx;
+      am = oam;
+    }
+    tg = fmaxf(tg, __shfl_xor_sync(0xffffffff, tg, o));
+  }
+  float s = 0.f;
+  for (int nb = lane; nb < num_nb; nb += 32) {
+    const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
+    if (p.sum > 0.f) s += p.sum * exp2f((p.max - mx) * 1.4426950408889634f);
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    const float l = mx + logf(s);
+    lse[t] = l;
+    argmax[t] = am;
+    row_loss[t] = m[t] ? (l - tg) : 0.f;
+  }
+}
+
+__global__ void ce_finalize_kernel(const float* __restrict__ row_loss,
+                                   const int32_t* __restrict__ argmax,
+                                   const int32_t* __restrict__ y, const int32_t* __restrict__ m,
+                                   const long long* __restrict__ n_global, long long T,
+                                   double* __restrict__ stats) {
+  __shared__ double sl[32], sv[32], sc[32];
+  double l = 0.0, v = 0.0, c = 0.0;
+  for (long long i = threadIdx.x; i < T; i += blockDim.x) {
+    l += row_loss[i];
+    if (m[i]) {
+      v += 1.0;
+      c += (argmax[i] == y[i]) ? 1.0 : 0.0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    l += __shfl_xor_sync(0xffffffff, l, o);
+    v += __shfl_xor_sync(0xffffffff, v, o);
+    c += __shfl_xor_sync(0xffffffff, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sl[threadIdx.x >> 5] = l;
+    sv[threadIdx.x >> 5] = v;
+    sc[threadIdx.x >> 5] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double L = 0, V = 0, Cc = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      L += sl[i];
+      V += sv[i];
+      Cc += sc[i];
+    }
+    const double N = *n_global > 0 ? static_cast<double>(*n_global) : (V > 0 ? V : 1.0);
+    stats[0] = L / N;
+    stats[1] = V;
+    stats[2] = Cc;
+  }
+}
+
+// ----------------------------------------------------------------- AdamW
+__global__ void adamw_kernel(long long n4, float4* __restrict__ p, float4* __restrict__ m,
+                             float4* __restrict__ v, const float4* __restrict__ g,
+                             uint2* __restrict__ p16, AdamHyper hp) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 pp = p[i], mm = m[i], vv = v[i];
+  const float4 gg = g[i];
+  float* pa = &pp.x;
+  float* ma = &mm.x;
+  float* va = &vv.x;
+  const float* ga = &gg.x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float pi = pa[j] * hp.decay;
+    const float mi = ma[j] + (ga[j] - ma[j]) * (1.f - hp.beta1);
+    const float vi = va[j] * hp.beta2 + (1.f - hp.beta2) * ga[j] * ga[j];
+    const float denom = sqrtf(vi) / hp.bc2_sqrt + hp.eps;
+    pi = pi - hp.step_size * (mi / denom);
+    pa[j] = pi;
+    ma[j] = mi;
+    va[j] = vi;
+  }
+  p[i] = pp;
+  m[i] = mm;
+  v[i] = vv;
+  __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
+  p16[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ y,
+                                   long long n4) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 a = x[i];
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+  y[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+// ------------------------------------------------------- signal packing
+__global__ void pack_signals_kernel(LayerPtrs layers, int n_layers, long long ld, int H8,
+                                    const int32_t* __restrict__ idx, int n,
+                                    uint4* __restrict__ ring, long long cap, long long pos) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const long long src_row = idx ? idx[i] : i;
+  uint4* dst = ring + ((pos + i) % cap) * static_cast<long long>(H8) * n_layers;
+  for (int l = 0; l < n_layers; ++l) {
+    const uint4* src = reinterpret_cast<const uint4*>(layers.p[l] + src_row * ld);
+    for (int c = threadIdx.x; c < H8; c += blockDim.x) dst[l * H8 + c] = src[c];
+  }
+}
+
+__global__ void pack_packed_kernel(const uint4* __restrict__ src, int W8, int n,
+                                   uint4* __restrict__ ring, long long cap, long long pos) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  uint4* dst = ring + ((pos + i) % cap) * W8;
+  const uint4* s = src + static_cast<long long>(i) * W8;
+  for (int c = threadIdx.x; c < W8; c += blockDim.x) dst[c] = s[c];
+}
+
+}  // namespace
+
+// ============================================================== launchers
+void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long long cap, int W,
+                  const BatchSpec& spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
+                  int32_t* m, cudaStream_t s) {
+  const long long T = static_cast<long long>(B) * S;
+  gather_batch_kernel<<<static_cast<unsigned>(T), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(ring_feat), ring_ids, cap, W / 8, spec, S,
+      reinterpret_cast<uint4*>(F), u, y, m);
+}
+
+void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s) {
+  mask_count_kernel<<<1, 1024, 0, s>>>(m, T, out);
+}
+
+void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T,
+             cudaStream_t s) {
+  ce_coef_kernel<<<blocks_for(T, 256), 256, 0, s>>>(m, n_global, coef, T);
+}
+
+void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, const float* w,
+                 float eps, __nv_bfloat16* y, long long ldy, float* rstd, long long T, int H,
+                 cudaStream_t s) {
+  rmsnorm_fwd_kernel<<<static_cast<unsigned>(T), kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y,
+                                                                       ldy, rstd, H);
+}
+
+long long rmsnorm_bwd_partial_rows(long long T) { return (T + kBwdRows - 1) / kBwdRows; }
+
+void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long long ldx,
+                 const int32_t* gather, const float* w, const float* rstd, const float* resid,
+                 float* out_f32, __nv_bfloat16* out_bf16, long long ldo, float* dw,
+                 float* dw_partial, long long T, int H, cudaStream_t s) {
+  const long long nb = rmsnorm_bwd_partial_rows(T);
+  rmsnorm_bwd_kernel<<<static_cast<unsigned>(nb), kNormThreads, 0, s>>>(
+      dy, lddy, x, ldx, gather, w, rstd, resid, out_f32, out_bf16, ldo, dw_partial, T, H);
+  colsum_kernel<<<blocks_for(H, 256), 256, 0, s>>>(dw_partial, nb, H, dw);
+}
+
+void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,
+          const float* cos_t, const float* sin_t, bool inverse, cudaStream_t s) {
+  const long long n = T * n_rot_heads * (hd / 4);
+  rope_kernel<<<blocks_for(n, 256), 256, 0, s>>>(qkv, T, S, NQ, n_rot_heads, hd, cos_t, sin_t,
+                                                 inverse ? 1 : 0);
+}
+
+void swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* act, long long T, int I, cudaStream_t s) {
+  swiglu_fwd_kernel<<<blocks_for(T * (I / 8), 256), 256, 0, s>>>(gu, act, T, I);
+}
+
+void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat16* dgu,
+                long long T, int I, cudaStream_t s) {
+  swiglu_bwd_kernel<<<blocks_for(T * (I / 8), 256), 256, 0, s>>>(gu, dact, dgu, T, I);
+}
+
+void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,
+               const int32_t* m, float* lse, float* row_loss, int32_t* argmax, cudaStream_t s) {
+  ce_reduce_kernel<<<blocks_for(T * 32, 256), 256, 0, s>>>(partials, num_nb, T, y, m, lse,
+                                                           row_loss, argmax);
+}
+
+void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,
+                 const long long* n_global, long long T, double* stats, cudaStream_t s) {
+  ce_finalize_kernel<<<1, 1024, 0, s>>>(row_loss, argmax, y, m, n_global, T, stats);
+}
+
+void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloat16* p16,
+           const AdamHyper& hp, cudaStream_t s) {
+  const long long n4 = n / 4;  // n is a multiple of 8 (checked at trainer creation)
+  adamw_kernel<<<blocks_for(n4, 256), 256, 0, s>>>(
+      n4, reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(m),
+      reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
+      reinterpret_cast<uint2*>(p16), hp);
+}
+
+void f32_to_bf16(const float* x, __nv_bfloat16* y, long long n, cudaStream_t s) {
+  f32_to_bf16_kernel<<<blocks_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                            reinterpret_cast<uint2*>(y), n / 4);
+}
+
+void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, const int32_t* idx,
+                  int n, __nv_bfloat16* ring_feat, long long cap, long long pos, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_signals_kernel<<<n, 128, 0, s>>>(layers, n_layers, ld, H / 8, idx,
+                                        n, reinterpret_cast<uint4*>(ring_feat), cap, pos);
+}
+
+void pack_packed(const __nv_bfloat16* src, int W, int n, __nv_bfloat16* ring_feat, long long cap,
+                 long long pos, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_packed_kernel<<<n, 128, 0, s>>>(reinterpret_cast<const uint4*>(src), W / 8, n,
+                                       reinterpret_cast<uint4*>(ring_feat), cap, pos);
+}
+
+}  // namespace kern
+}  // namespace specsim

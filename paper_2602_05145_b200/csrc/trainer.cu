@@ -1,0 +1,928 @@
+// DraftTrainer: the real body behind the reference's analytic train()
+// (SPEC.md:380-405).  One optimiser step = gather the micro-batch from the
+// signal ring, forward the EAGLE-3 style draft head, fused
+// vocabulary-chunked LM-head cross-entropy, backward, optional NCCL gradient
+// all-reduce across data-parallel ranks, fused AdamW.
+//
+// Every dense contraction runs on the tcgen05 GEMM (gemm.cuh); the plans
+// (tensor maps, shapes, epilogues) are built once here, so a step is a fixed
+// sequence of launches on one stream.
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "attention.h"
+#include "common.h"
+#include "gemm.h"
+#include "kernels.h"
+#include "nccl_dyn.h"
+#include "specsim/draft_trainer.hpp"
+
+namespace specsim {
+
+namespace {
+
+#define SPECSIM_NCCL(call)                                                              \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      throw NcclError(std::string(#call) + ": " + nccl::api().GetErrorString(_r));      \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    SPECSIM_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) SPECSIM_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// One cudaMalloc carved into 256-byte aligned buffers.
+class Arena {
+ public:
+  template <class T>
+  void reserve(T** slot, long long count) {
+    reqs_.push_back({reinterpret_cast<void**>(slot), static_cast<size_t>(count) * sizeof(T)});
+  }
+  void commit() {
+    size_t total = 0;
+    for (auto& r : reqs_) total += (r.bytes + 255) & ~size_t(255);
+    SPECSIM_CUDA(cudaMalloc(&base_, total));
+    size_t off = 0;
+    for (auto& r : reqs_) {
+      *r.slot = static_cast<uint8_t*>(base_) + off;
+      off += (r.bytes + 255) & ~size_t(255);
+    }
+    reqs_.clear();
+  }
+  ~Arena() {
+    if (base_) cudaFree(base_);
+  }
+ private:
+  struct Req {
+    void** slot;
+    size_t bytes;
+  };
+  std::vector<Req> reqs_;
+  void* base_ = nullptr;
+};
+
+enum Phase { PH_INGEST = 0, PH_GEMM, PH_ATTN, PH_ELEM, PH_LM, PH_ADAM, PH_COMM, PH_N };
+
+}  // namespace
+
+HiddenStateBuffer* hsbuf_unwrap(struct specsim_hsbuf* b);
+
+void DraftShape::validate() const {
+  Problems p("invalid draft shape");
+  p.check(hidden > 0 && hidden % 64 == 0, "hidden must be a positive multiple of 64");
+  p.check(hidden <= 8192, "hidden must be <= 8192");
+  p.check(vocab > 0 && vocab % 8 == 0, "vocab must be a positive multiple of 8");
+  p.check(seq_len > 0 && seq_len % 64 == 0, "seq_len must be a positive multiple of 64");
+  p.check(head_dim == 64 || head_dim == 128, "head_dim must be 64 or 128");
+  p.check(n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
+          "n_heads must be a positive multiple of n_kv_heads");
+  p.check(ffn > 0 && ffn % 64 == 0, "ffn must be a positive multiple of 64");
+  p.check(layers_tapped >= 1 && layers_tapped <= 8, "layers_tapped must be in [1, 8]");
+  p.check(micro_batch >= 1 && micro_batch <= kern::kMaxBatch, "micro_batch must be in [1, 64]");
+  p.check(rms_eps > 0.f, "rms_eps must be > 0");
+  p.check(rope_theta > 0.0, "rope_theta must be > 0");
+  p.throw_if_any();
+}
+
+class DraftTrainerImpl {
+ public:
+  struct Param {
+    std::string name;
+    long long rows, cols, off;
+    bool norm;
+  };
+
+  DraftShape sh;
+  AdamWConfig opt;
+  int rank, world, device;
+  long long T, H, Q, KV, NQ, I, V, W3, Vc;
+  int n_chunks;
+  std::vector<Param> params;
+  long long total = 0;
+  int64_t step_count = 0;
+  int64_t version = 0;
+  bool timing = false;
+  double phase_ms[PH_N] = {}, phase_flops[PH_N] = {};
+  int phase_launches[PH_N] = {};
+
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  Arena arena;
+
+  // parameters / optimiser state (flat, registry order)
+  float *P = nullptr, *Mst = nullptr, *Vst = nullptr, *G = nullptr;
+  __nv_bfloat16* P16 = nullptr;
+  __nv_bfloat16* E = nullptr;  // frozen embedding [V, H]
+  float *cos_t = nullptr, *sin_t = nullptr;
+  // activations
+  __nv_bfloat16 *F, *g, *U, *qkv, *o, *r, *z, *gu, *act, *h, *nrm;
+  int32_t *u, *y, *m, *argmax;
+  float *coef, *rstd_a, *rstd_b, *lse_attn, *rstd_post, *rstd_fin, *lse, *row_loss;
+  gemm::CePartial* partials;
+  long long* n_global;
+  double* stats;
+  // backward
+  __nv_bfloat16 *dlog, *dh_b, *dact, *dgu, *dr_b, *dO, *dqkv, *dg_b;
+  float *dn, *dh, *dz, *dr, *dU, *Dattn, *dw_part;
+  // pinned host scalars
+  long long* h_nglobal = nullptr;
+  double* h_stats = nullptr;
+
+  // GEMM plans
+  gemm::GemmPlan p_fc, p_qkv, p_o, p_gu, p_down, p_ce_fwd;
+  std::vector<gemm::GemmPlan> p_ce_bwd, p_lm_dx, p_lm_dw;
+  gemm::GemmPlan p_dact, p_dw_down, p_dz, p_dw_gu, p_dO, p_dw_o, p_dU, p_dw_qkv, p_dw_fc;
+
+  // timing
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+
+  const Param& param(const std::string& name) const {
+    for (const auto& p : params)
+      if (p.name == name) return p;
+    throw std::invalid_argument("unknown parameter '" + name + "'");
+  }
+  float* pf(const char* n) { return P + param(n).off; }
+  __nv_bfloat16* pb(const char* n) { return P16 + param(n).off; }
+  float* gf(const char* n) { return G + param(n).off; }
+
+  DraftTrainerImpl(const DraftShape& s, const AdamWConfig& a, uint64_t seed, int rk, int ws,
+                   const uint8_t* nccl_id, int dev)
+      : sh(s), opt(a), rank(rk), world(ws), device(dev) {
+    sh.validate();
+    Problems p("invalid trainer configuration");
+    p.check(world >= 1, "world must be >= 1");
+    p.check(rank >= 0 && rank < world, "rank must be in [0, world)");
+    p.check(world == 1 || nccl_id != nullptr, "nccl_id is required when world > 1");
+    p.check(opt.lr > 0.f, "lr must be > 0");
+    p.check(opt.beta1 >= 0.f && opt.beta1 < 1.f && opt.beta2 >= 0.f && opt.beta2 < 1.f,
+            "betas must be in [0, 1)");
+    p.check(opt.eps > 0.f, "eps must be > 0");
+    p.throw_if_any();
+    DeviceGuard dg(device);
+    int major = 0, minor = 0;
+    SPECSIM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    SPECSIM_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+      throw CudaError("this build targets sm_100a (B200); device has sm_" + std::to_string(major) +
+                      std::to_string(minor));
+    T = static_cast<long long>(sh.micro_batch) * sh.seq_len;
+    H = sh.hidden;
+    Q = static_cast<long long>(sh.n_heads) * sh.head_dim;
+    KV = static_cast<long long>(sh.n_kv_heads) * sh.head_dim;
+    NQ = Q + 2 * KV;
+    I = sh.ffn;
+    V = sh.vocab;
+    W3 = static_cast<long long>(sh.layers_tapped) * H;
+    // vocabulary chunk for the backward: multiple of the GEMM N tile, ~32k
+    Vc = std::min<long long>(V, 32768);
+    Vc = (Vc + gemm::BN - 1) / gemm::BN * gemm::BN;
+    if (Vc > V) Vc = V;
+    n_chunks = static_cast<int>((V + Vc - 1) / Vc);
+
+    // registry (same order / layout as the oracle)
+    auto add = [&](const char* n, long long r_, long long c_, bool norm) {
+      params.push_back({n, r_, c_, total, norm});
+      total += r_ * c_;
+    };
+    add("fc", H, W3, false);
+    add("w_in", 1, H, true);
+    add("w_hid", 1, H, true);
+    add("qkv", NQ, 2 * H, false);
+    add("o", H, Q, false);
+    add("w_post", 1, H, true);
+    add("gate_up", 2 * I, H, false);
+    add("down", H, I, false);
+    add("w_fin", 1, H, true);
+    add("lm_head", V, H, false);
+
+    SPECSIM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    const long long nb_ce = (V + gemm::BN - 1) / gemm::BN;
+    arena.reserve(&P, total);
+    arena.reserve(&Mst, total);
+    arena.reserve(&Vst, total);
+    arena.reserve(&G, total);
+    arena.reserve(&P16, total);
+    arena.reserve(&E, V * H);
+    arena.reserve(&cos_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
+    arena.reserve(&sin_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
+    arena.reserve(&F, T * W3);
+    arena.reserve(&g, T * H);
+    arena.reserve(&U, T * 2 * H);
+    arena.reserve(&qkv, T * NQ);
+    arena.reserve(&o, T * Q);
+    arena.reserve(&r, T * H);
+    arena.reserve(&z, T * H);
+    arena.reserve(&gu, T * 2 * I);
+    arena.reserve(&act, T * I);
+    arena.reserve(&h, T * H);
+    arena.reserve(&nrm, T * H);
+    arena.reserve(&u, T);
+    arena.reserve(&y, T);
+    arena.reserve(&m, T);
+    arena.reserve(&argmax, T);
+    arena.reserve(&coef, T);
+    arena.reserve(&rstd_a, T);
+    arena.reserve(&rstd_b, T);
+    arena.reserve(&lse_attn, T * sh.n_heads);
+    arena.reserve(&rstd_post, T);
+    arena.reserve(&rstd_fin, T);
+    arena.reserve(&lse, T);
+    arena.reserve(&row_loss, T);
+    arena.reserve(&partials, nb_ce * T);
+    arena.reserve(&n_global, 2);
+    arena.reserve(&stats, 4);
+    arena.reserve(&dlog, T * Vc);
+    arena.reserve(&dh_b, T * H);
+    arena.reserve(&dact, T * I);
+    arena.reserve(&dgu, T * 2 * I);
+    arena.reserve(&dr_b, T * H);
+    arena.reserve(&dO, T * Q);
+    arena.reserve(&dqkv, T * NQ);
+    arena.reserve(&dg_b, T * H);
+    arena.reserve(&dn, T * H);
+    arena.reserve(&dh, T * H);
+    arena.reserve(&dz, T * H);
+    arena.reserve(&dr, T * H);
+    arena.reserve(&dU, T * 2 * H);
+    arena.reserve(&Dattn, T * sh.n_heads);
+    arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(T) * H);
+    arena.commit();
+    SPECSIM_CUDA(cudaMallocHost(&h_nglobal, sizeof(long long)));
+    SPECSIM_CUDA(cudaMallocHost(&h_stats, 4 * sizeof(double)));
+    SPECSIM_CUDA(cudaMemsetAsync(Mst, 0, sizeof(float) * total, stream));
+    SPECSIM_CUDA(cudaMemsetAsync(Vst, 0, sizeof(float) * total, stream));
+    SPECSIM_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * total, stream));
+
+    init_params(seed);
+    init_rope();
+    build_plans();
+    SPECSIM_CUDA(cudaEventCreate(&ev_begin));
+    SPECSIM_CUDA(cudaEventCreate(&ev_end));
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      SPECSIM_NCCL(nccl::api().CommInitRank(&comm, world, id, rank));
+    }
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  ~DraftTrainerImpl() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (comm) nccl::api().CommDestroy(comm);
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (ev_begin) cudaEventDestroy(ev_begin);
+    if (ev_end) cudaEventDestroy(ev_end);
+    if (h_nglobal) cudaFreeHost(h_nglobal);
+    if (h_stats) cudaFreeHost(h_stats);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ------------------------------------------------------------ init
+  static void fill_normal_blocks(uint64_t seed_base, int pidx, long long n, float* out) {
+    // element e: Rng(seed_base + (p << 32) + (e >> 20)) in element order
+    const long long nblk = (n + (1 << 20) - 1) >> 20;
+    const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([=] {
+        for (long long j = w; j < nblk; j += nt) {
+          Rng rng(seed_base + (static_cast<uint64_t>(pidx) << 32) + static_cast<uint64_t>(j));
+          const long long e0 = j << 20, e1 = std::min(n, e0 + (1ll << 20));
+          for (long long e = e0; e < e1; ++e) out[e] = static_cast<float>(rng.normal(0.0, 0.02));
+        }
+      });
+    for (auto& t : th) t.join();
+  }
+
+  void init_params(uint64_t seed) {
+    const long long slab = 1ll << 26;  // 64M elements per host slab
+    std::vector<float> buf;
+    for (size_t pi = 0; pi < params.size(); ++pi) {
+      const Param& pr = params[pi];
+      const long long n = pr.rows * pr.cols;
+      if (pr.norm) {
+        buf.assign(n, 1.0f);
+        SPECSIM_CUDA(cudaMemcpy(P + pr.off, buf.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        continue;
+      }
+      buf.resize(n);
+      fill_normal_blocks(seed + 1, static_cast<int>(pi), n, buf.data());
+      for (long long e = 0; e < n; e += slab) {
+        const long long c = std::min(slab, n - e);
+        SPECSIM_CUDA(cudaMemcpy(P + pr.off + e, buf.data() + e, sizeof(float) * c,
+                                cudaMemcpyHostToDevice));
+      }
+    }
+    kern::f32_to_bf16(P, P16, total, stream);
+    // frozen embedding (parameter index 15, seed + 2), bf16
+    const long long ne = V * H;
+    buf.resize(ne);
+    fill_normal_blocks(seed + 2, 15, ne, buf.data());
+    std::vector<uint16_t> eb(ne);
+    for (long long i = 0; i < ne; ++i) {
+      uint32_t bits;
+      std::memcpy(&bits, &buf[i], 4);
+      bits += 0x7FFFu + ((bits >> 16) & 1u);
+      eb[i] = static_cast<uint16_t>(bits >> 16);
+    }
+    SPECSIM_CUDA(cudaMemcpy(E, eb.data(), 2 * ne, cudaMemcpyHostToDevice));
+    SPECSIM_CHECK_LAUNCH();
+  }
+
+  void init_rope() {
+    // NeoX rotate-half tables, angle = pos * theta^(-2i/hd) in double
+    const int half = sh.head_dim / 2;
+    std::vector<float> c(static_cast<size_t>(sh.seq_len) * half), s(c.size());
+    for (int pos = 0; pos < sh.seq_len; ++pos)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(sh.rope_theta, -2.0 * i / sh.head_dim);
+        const double ang = static_cast<double>(pos) * inv;
+        c[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::cos(ang));
+        s[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::sin(ang));
+      }
+    SPECSIM_CUDA(cudaMemcpy(cos_t, c.data(), sizeof(float) * c.size(), cudaMemcpyHostToDevice));
+    SPECSIM_CUDA(cudaMemcpy(sin_t, s.data(), sizeof(float) * s.size(), cudaMemcpyHostToDevice));
+  }
+
+  // ------------------------------------------------------------ plans
+  static gemm::Args out_args(void* C, long long ldc, const __nv_bfloat16* R = nullptr,
+                             long long ldr = 0) {
+    gemm::Args a{};
+    a.C = C;
+    a.ldc = ldc;
+    a.R = R;
+    a.ldr = ldr;
+    return a;
+  }
+
+  void build_plans() {
+    using gemm::Operand;
+    using namespace gemm;
+    // forward: Y = X W^T (both K-major)
+    p_fc = make_plan({F, W3, false}, {pb("fc"), W3, false}, T, H, W3, EPI_BF16, out_args(g, H));
+    p_qkv = make_plan({U, 2 * H, false}, {pb("qkv"), 2 * H, false}, T, NQ, 2 * H, EPI_BF16,
+                      out_args(qkv, NQ));
+    p_o = make_plan({o, Q, false}, {pb("o"), Q, false}, T, H, Q, EPI_BF16_RESID,
+                    out_args(r, H, g, H));
+    p_gu = make_plan({z, H, false}, {pb("gate_up"), H, false}, T, 2 * I, H, EPI_BF16,
+                     out_args(gu, 2 * I));
+    p_down = make_plan({act, I, false}, {pb("down"), I, false}, T, H, I, EPI_BF16_RESID,
+                       out_args(h, H, r, H));
+    Args ce{};
+    ce.targets = y;
+    ce.partials = partials;
+    p_ce_fwd = make_plan({nrm, H, false}, {pb("lm_head"), H, false}, T, V, H, EPI_CE_FWD, ce);
+    // LM head backward, vocabulary chunks
+    for (int c = 0; c < n_chunks; ++c) {
+      const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
+      Args cb = out_args(dlog, Vc);
+      cb.targets = y;
+      cb.lse = lse;
+      cb.coef = coef;
+      cb.vocab_offset = static_cast<int>(v0);
+      p_ce_bwd.push_back(make_plan({nrm, H, false}, {pb("lm_head") + v0 * H, H, false}, T, vn, H,
+                                   EPI_CE_BWD, cb));
+      // dn (+)= dlog_c . W_c     (B = W_c stored [vn, H] -> MN-major)
+      p_lm_dx.push_back(make_plan({dlog, Vc, false}, {pb("lm_head") + v0 * H, H, true}, T, H, vn,
+                                  c == 0 ? EPI_F32 : EPI_F32_ACC, out_args(dn, H)));
+      // dW_c = dlog_c^T . nrm    (A = dlog stored [T, vn] -> MN-major)
+      p_lm_dw.push_back(make_plan({dlog, Vc, true}, {nrm, H, true}, vn, H, T, EPI_F32,
+                                  out_args(gf("lm_head") + v0 * H, H)));
+    }
+    // MLP
+    p_dact = make_plan({dh_b, H, false}, {pb("down"), I, true}, T, I, H, EPI_BF16,
+                       out_args(dact, I));
+    p_dw_down = make_plan({dh_b, H, true}, {act, I, true}, H, I, T, EPI_F32,
+                          out_args(gf("down"), I));
+    p_dz = make_plan({dgu, 2 * I, false}, {pb("gate_up"), H, true}, T, H, 2 * I, EPI_F32,
+                     out_args(dz, H));
+    p_dw_gu = make_plan({dgu, 2 * I, true}, {z, H, true}, 2 * I, H, T, EPI_F32,
+                        out_args(gf("gate_up"), H));
+    // attention output projection
+    p_dO = make_plan({dr_b, H, false}, {pb("o"), Q, true}, T, Q, H, EPI_BF16, out_args(dO, Q));
+    p_dw_o = make_plan({dr_b, H, true}, {o, Q, true}, H, Q, T, EPI_F32, out_args(gf("o"), Q));
+    // qkv
+    p_dU = make_plan({dqkv, NQ, false}, {pb("qkv"), 2 * H, true}, T, 2 * H, NQ, EPI_F32,
+                     out_args(dU, 2 * H));
+    p_dw_qkv = make_plan({dqkv, NQ, true}, {U, 2 * H, true}, NQ, 2 * H, T, EPI_F32,
+                         out_args(gf("qkv"), 2 * H));
+    // fc (no dF: captured features are inputs)
+    p_dw_fc = make_plan({dg_b, H, true}, {F, W3, true}, H, W3, T, EPI_F32,
+                        out_args(gf("fc"), W3));
+  }
+
+  // ------------------------------------------------------------ timing
+  cudaEvent_t next_event() {
+    if (event_next == event_pool.size()) {
+      cudaEvent_t e;
+      SPECSIM_CUDA(cudaEventCreate(&e));
+      event_pool.push_back(e);
+    }
+    return event_pool[event_next++];
+  }
+  template <class Fn>
+  void timed(int phase, double flops, Fn&& fn) {
+    if (!timing) {
+      fn();
+      return;
+    }
+    cudaEvent_t a = next_event(), b = next_event();
+    SPECSIM_CUDA(cudaEventRecord(a, stream));
+    fn();
+    SPECSIM_CUDA(cudaEventRecord(b, stream));
+    marks.push_back({phase, {a, b}});
+    phase_flops[phase] += flops;
+    phase_launches[phase] += 1;
+  }
+  void run(const gemm::GemmPlan& p, int phase = PH_GEMM, double alg_flops = -1) {
+    timed(phase, alg_flops < 0 ? p.flops : alg_flops, [&] { p.launch(stream); });
+  }
+
+  // ------------------------------------------------------------ step
+  kern::BatchSpec batch_spec(HiddenStateBuffer& buf, const int64_t* ids, int n) {
+    if (n < 0 || n > sh.micro_batch)
+      throw std::invalid_argument("n must be in [0, micro_batch]");
+    if (buf.geometry().hidden_dim != sh.hidden || buf.geometry().layers_tapped != sh.layers_tapped)
+      throw std::invalid_argument("signal geometry does not match the draft shape");
+    if (buf.device() != device) throw std::invalid_argument("buffer lives on another device");
+    kern::BatchSpec spec{};
+    spec.n = n;
+    for (int b = 0; b < n; ++b) {
+      const auto& s = buf.sample(ids[b]);
+      spec.start[b] = s.start;
+      spec.len[b] = s.length;
+    }
+    return spec;
+  }
+
+  void forward(HiddenStateBuffer& buf, const kern::BatchSpec& spec, int64_t global_valid) {
+    const int S = sh.seq_len;
+    timed(PH_INGEST, 0, [&] {
+      kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
+                         buf.capacity(), static_cast<int>(W3), spec, sh.micro_batch, S, F, u, y,
+                         m, stream);
+      if (global_valid > 0) {
+        *h_nglobal = global_valid;
+        SPECSIM_CUDA(cudaMemcpyAsync(n_global, h_nglobal, sizeof(long long),
+                                     cudaMemcpyHostToDevice, stream));
+      } else {
+        kern::mask_count(m, T, n_global, stream);
+      }
+    });
+    if (global_valid <= 0 && world > 1)
+      timed(PH_COMM, 0, [&] {
+        SPECSIM_NCCL(nccl::api().AllReduce(n_global, n_global, 1, ncclInt64, ncclSum, comm, stream));
+      });
+    timed(PH_ELEM, 0, [&] { kern::ce_coef(m, n_global, coef, T, stream); });
+    run(p_fc);
+    timed(PH_ELEM, 0, [&] {
+      kern::rmsnorm_fwd(E, H, u, pf("w_in"), sh.rms_eps, U, 2 * H, rstd_a, T, sh.hidden, stream);
+      kern::rmsnorm_fwd(g, H, nullptr, pf("w_hid"), sh.rms_eps, U + H, 2 * H, rstd_b, T,
+                        sh.hidden, stream);
+    });
+    run(p_qkv);
+    timed(PH_ELEM, 0, [&] {
+      kern::rope(qkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim, cos_t,
+                 sin_t, false, stream);
+    });
+    const attn::Dims ad = attn_dims();
+    timed(PH_ATTN, 2.0 * Q * (S + 1) * T, [&] { attn::forward(qkv, o, lse_attn, ad, sh.head_dim, stream); });
+    run(p_o);
+    timed(PH_ELEM, 0, [&] {
+      kern::rmsnorm_fwd(r, H, nullptr, pf("w_post"), sh.rms_eps, z, H, rstd_post, T, sh.hidden,
+                        stream);
+    });
+    run(p_gu);
+    timed(PH_ELEM, 0, [&] { kern::swiglu_fwd(gu, act, T, sh.ffn, stream); });
+    run(p_down);
+    timed(PH_ELEM, 0, [&] {
+      kern::rmsnorm_fwd(h, H, nullptr, pf("w_fin"), sh.rms_eps, nrm, H, rstd_fin, T, sh.hidden,
+                        stream);
+    });
+    run(p_ce_fwd, PH_LM);
+    timed(PH_ELEM, 0, [&] {
+      kern::ce_reduce(partials, p_ce_fwd.args.num_n_blocks, T, y, m, lse, row_loss, argmax, stream);
+      kern::ce_finalize(row_loss, argmax, y, m, n_global, T, stats, stream);
+    });
+  }
+
+  attn::Dims attn_dims() const {
+    attn::Dims d;
+    d.B = sh.micro_batch;
+    d.S = sh.seq_len;
+    d.nh = sh.n_heads;
+    d.nkv = sh.n_kv_heads;
+    d.NQ = static_cast<int>(NQ);
+    d.Q = static_cast<int>(Q);
+    d.KV = static_cast<int>(KV);
+    d.scale = 1.0f / std::sqrt(static_cast<float>(sh.head_dim));
+    return d;
+  }
+
+  void backward() {
+    const int S = sh.seq_len;
+    for (int c = 0; c < n_chunks; ++c) {
+      run(p_ce_bwd[c], PH_LM, 0.0);  // logit recompute: not algorithmic work
+      run(p_lm_dx[c], PH_LM);
+      run(p_lm_dw[c], PH_LM);
+    }
+    timed(PH_ELEM, 0, [&] {
+      kern::rmsnorm_bwd(dn, H, h, H, nullptr, pf("w_fin"), rstd_fin, nullptr, dh, dh_b, H,
+                        gf("w_fin"), dw_part, T, sh.hidden, stream);
+    });
+    run(p_dact);
+    run(p_dw_down);
+    timed(PH_ELEM, 0, [&] { kern::swiglu_bwd(gu, dact, dgu, T, sh.ffn, stream); });
+    run(p_dz);
+    run(p_dw_gu);
+    timed(PH_ELEM, 0, [&] {
+      kern::rmsnorm_bwd(dz, H, r, H, nullptr, pf("w_post"), rstd_post, dh, dr, dr_b, H,
+                        gf("w_post"), dw_part, T, sh.hidden, stream);
+    });
+    run(p_dO);
+    run(p_dw_o);
+    const attn::Dims ad = attn_dims();
+    timed(PH_ATTN, 4.0 * Q * (S + 1) * T, [&] {
+      attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
+    });
+    timed(PH_ELEM, 0, [&] {
+      kern::rope(dqkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim, cos_t,
+                 sin_t, true, stream);
+    });
+    run(p_dU);
+    run(p_dw_qkv);
+    timed(PH_ELEM, 0, [&] {
+      // w_in: embedding is frozen, only the weight gradient is needed
+      kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
+                        gf("w_in"), dw_part, T, sh.hidden, stream);
+      // hidden norm: dg = dr + d/dg RMSNorm(g) ; bf16 copy feeds dW_fc
+      kern::rmsnorm_bwd(dU + H, 2 * H, g, H, nullptr, pf("w_hid"), rstd_b, dr, nullptr, dg_b, H,
+                        gf("w_hid"), dw_part, T, sh.hidden, stream);
+    });
+    run(p_dw_fc);
+  }
+
+  void optimizer_update() {
+    step_count += 1;
+    const double bc1 = 1.0 - std::pow(static_cast<double>(opt.beta1), static_cast<double>(step_count));
+    const double bc2 = 1.0 - std::pow(static_cast<double>(opt.beta2), static_cast<double>(step_count));
+    kern::AdamHyper hp;
+    hp.lr = opt.lr;
+    hp.beta1 = opt.beta1;
+    hp.beta2 = opt.beta2;
+    hp.eps = opt.eps;
+    hp.decay = 1.0f - opt.lr * opt.weight_decay;
+    hp.step_size = static_cast<float>(opt.lr / bc1);
+    hp.bc2_sqrt = static_cast<float>(std::sqrt(bc2));
+    timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, hp, stream); });
+  }
+
+  void begin_step() {
+    for (int i = 0; i < PH_N; ++i) {
+      phase_ms[i] = 0;
+      phase_flops[i] = 0;
+      phase_launches[i] = 0;
+    }
+    marks.clear();
+    event_next = 0;
+    SPECSIM_CUDA(cudaEventRecord(ev_begin, stream));
+  }
+
+  StepResult end_step() {
+    SPECSIM_CUDA(cudaEventRecord(ev_end, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(h_stats, stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    SPECSIM_CHECK_LAUNCH();
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    float ms = 0;
+    SPECSIM_CUDA(cudaEventElapsedTime(&ms, ev_begin, ev_end));
+    for (auto& mk : marks) {
+      float t = 0;
+      SPECSIM_CUDA(cudaEventElapsedTime(&t, mk.second.first, mk.second.second));
+      phase_ms[mk.first] += t;
+    }
+    StepResult res;
+    res.loss = h_stats[0];
+    res.valid_tokens = static_cast<int64_t>(h_stats[1]);
+    res.top1_correct = static_cast<int64_t>(h_stats[2]);
+    res.positions = T * world;
+    res.ms = ms;
+    return res;
+  }
+
+  void allreduce_stats() {
+    if (world == 1) return;
+    // loss is already normalised by the global count: sum over ranks
+    timed(PH_COMM, 0, [&] {
+      SPECSIM_NCCL(nccl::api().AllReduce(stats, stats, 3, ncclDouble, ncclSum, comm, stream));
+    });
+  }
+
+  StepResult step(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid) {
+    DeviceGuard dg(device);
+    const kern::BatchSpec spec = batch_spec(buf, ids, n);
+    begin_step();
+    forward(buf, spec, global_valid);
+    backward();
+    if (world > 1)
+      timed(PH_COMM, 0, [&] {
+        SPECSIM_NCCL(nccl::api().AllReduce(G, G, static_cast<size_t>(total), ncclFloat, ncclSum, comm,
+                                   stream));
+      });
+    optimizer_update();
+    allreduce_stats();
+    return end_step();
+  }
+
+  StepResult eval(HiddenStateBuffer& buf, const int64_t* ids, int n) {
+    DeviceGuard dg(device);
+    const kern::BatchSpec spec = batch_spec(buf, ids, n);
+    begin_step();
+    forward(buf, spec, 0);
+    allreduce_stats();
+    return end_step();
+  }
+
+  TrainingOutcome train(HiddenStateBuffer& buf, const TrainJob& job) {
+    Problems p("train job");
+    p.check(!job.train_ids.empty(), "D_train must be non-empty (SPEC.md:398 requires n > 0)");
+    p.check(job.epochs >= 1, "epochs must be >= 1");
+    p.throw_if_any();
+    const auto t0 = std::chrono::steady_clock::now();
+    const long long per_step = static_cast<long long>(sh.micro_batch) * world;
+    double loss_sum = 0;
+    int64_t steps = 0;
+    std::vector<int64_t> mine;
+    for (int ep = 0; ep < job.epochs; ++ep) {
+      const long long n = static_cast<long long>(job.train_ids.size());
+      for (long long s0 = 0; s0 < n; s0 += per_step) {
+        mine.clear();
+        // sample i of the step slice -> rank i mod world
+        for (long long i = s0 + rank; i < std::min(n, s0 + per_step); i += world)
+          mine.push_back(job.train_ids[i]);
+        const StepResult r = step(buf, mine.data(), static_cast<int>(mine.size()), 0);
+        loss_sum += r.loss;
+        ++steps;
+      }
+    }
+    // alpha_eval = top-1 accuracy of the new draft on D_eval
+    int64_t valid = 0, correct = 0;
+    const long long ne = static_cast<long long>(job.eval_ids.size());
+    for (long long s0 = 0; s0 < ne; s0 += per_step) {
+      mine.clear();
+      for (long long i = s0 + rank; i < std::min(ne, s0 + per_step); i += world)
+        mine.push_back(job.eval_ids[i]);
+      const StepResult r = eval(buf, mine.data(), static_cast<int>(mine.size()));
+      valid += r.valid_tokens;
+      correct += r.top1_correct;
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    TrainingOutcome out;
+    out.duration_hours = std::chrono::duration<double>(t1 - t0).count() / 3600.0;
+    out.alpha_eval = valid > 0 ? static_cast<double>(correct) / static_cast<double>(valid) : 0.0;
+    out.new_version = ++version;
+    out.steps = steps;
+    out.mean_loss = steps ? loss_sum / steps : 0.0;
+    return out;
+  }
+};
+
+DraftTrainer::DraftTrainer(const DraftShape& shape, const AdamWConfig& opt, uint64_t seed,
+                           int rank, int world, const uint8_t* nccl_id, int device)
+    : impl_(std::make_unique<DraftTrainerImpl>(shape, opt, seed, rank, world, nccl_id, device)) {}
+DraftTrainer::~DraftTrainer() = default;
+StepResult DraftTrainer::step(HiddenStateBuffer& buf, const int64_t* ids, int n,
+                              int64_t global_valid) {
+  return impl_->step(buf, ids, n, global_valid);
+}
+StepResult DraftTrainer::eval(HiddenStateBuffer& buf, const int64_t* ids, int n) {
+  return impl_->eval(buf, ids, n);
+}
+TrainingOutcome DraftTrainer::train(HiddenStateBuffer& buf, const TrainJob& job) {
+  return impl_->train(buf, job);
+}
+
+}  // namespace specsim
+
+// ================================================================== C ABI
+using namespace specsim;
+
+struct specsim_trainer {
+  DraftTrainer* t;
+};
+
+namespace {
+DraftTrainerImpl& impl_of(const specsim_trainer* t) {
+  if (!t || !t->t) throw std::invalid_argument("null trainer");
+  return const_cast<DraftTrainer*>(t->t)->impl();
+}
+void fill(specsim_step_result* out, const StepResult& r) {
+  if (!out) return;
+  out->loss = r.loss;
+  out->valid_tokens = r.valid_tokens;
+  out->top1_correct = r.top1_correct;
+  out->positions = r.positions;
+  out->ms = r.ms;
+}
+}  // namespace
+
+extern "C" {
+
+int specsim_nccl_unique_id(uint8_t* out128) {
+  return guard([&] {
+    if (!out128) throw std::invalid_argument("null output");
+    ncclUniqueId id;
+    SPECSIM_NCCL(nccl::api().GetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int specsim_trainer_create(const specsim_draft_shape* shape, const specsim_adamw* opt,
+                           uint64_t seed, int rank, int world, const uint8_t* nccl_id, int device,
+                           specsim_trainer** out) {
+  return guard([&] {
+    if (!shape || !out) throw std::invalid_argument("null argument");
+    DraftShape s;
+    s.hidden = shape->hidden;
+    s.vocab = shape->vocab;
+    s.seq_len = shape->seq_len;
+    s.n_heads = shape->n_heads;
+    s.n_kv_heads = shape->n_kv_heads;
+    s.head_dim = shape->head_dim;
+    s.ffn = shape->ffn;
+    s.layers_tapped = shape->layers_tapped;
+    s.micro_batch = shape->micro_batch;
+    s.rms_eps = shape->rms_eps;
+    s.rope_theta = shape->rope_theta;
+    AdamWConfig a;
+    if (opt) {
+      a.lr = opt->lr;
+      a.beta1 = opt->beta1;
+      a.beta2 = opt->beta2;
+      a.eps = opt->eps;
+      a.weight_decay = opt->weight_decay;
+    }
+    *out = new specsim_trainer{new DraftTrainer(s, a, seed, rank, world, nccl_id, device)};
+  });
+}
+
+int specsim_trainer_destroy(specsim_trainer* t) {
+  return guard([&] {
+    if (!t) return;
+    delete t->t;
+    delete t;
+  });
+}
+
+int specsim_trainer_step(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* ids, int32_t n,
+                         int64_t global_valid, specsim_step_result* out) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    if (n > 0 && !ids) throw std::invalid_argument("null sample ids");
+    fill(out, im.step(*hsbuf_unwrap(buf), ids, n, global_valid));
+  });
+}
+
+int specsim_trainer_eval(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* ids, int32_t n,
+                         specsim_step_result* out) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    if (n > 0 && !ids) throw std::invalid_argument("null sample ids");
+    fill(out, im.eval(*hsbuf_unwrap(buf), ids, n));
+  });
+}
+
+int specsim_trainer_train(specsim_trainer* t, specsim_hsbuf* buf, const int64_t* train_ids,
+                          int64_t n_train, const int64_t* eval_ids, int64_t n_eval,
+                          int32_t epochs, specsim_training_outcome* out) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    TrainJob job;
+    if (n_train > 0) job.train_ids.assign(train_ids, train_ids + n_train);
+    if (n_eval > 0) job.eval_ids.assign(eval_ids, eval_ids + n_eval);
+    job.epochs = epochs;
+    const TrainingOutcome o = im.train(*hsbuf_unwrap(buf), job);
+    if (out) {
+      out->duration_hours = o.duration_hours;
+      out->alpha_eval = o.alpha_eval;
+      out->new_version = o.new_version;
+      out->mean_loss = o.mean_loss;
+      out->steps = o.steps;
+    }
+  });
+}
+
+int specsim_trainer_num_params(const specsim_trainer* t, int32_t* count, int64_t* total_elems) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    if (count) *count = static_cast<int32_t>(im.params.size());
+    if (total_elems) *total_elems = im.total;
+  });
+}
+
+int specsim_trainer_param_info(const specsim_trainer* t, int32_t index, const char** name,
+                               int64_t* rows, int64_t* cols) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    if (index < 0 || index >= static_cast<int32_t>(im.params.size()))
+      throw std::invalid_argument("parameter index out of range");
+    const auto& p = im.params[index];
+    if (name) *name = p.name.c_str();
+    if (rows) *rows = p.rows;
+    if (cols) *cols = p.cols;
+  });
+}
+
+int specsim_trainer_get_param(const specsim_trainer* t, const char* name, float* host_out) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    const auto& p = im.param(name ? name : "");
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(host_out, im.P + p.off, sizeof(float) * p.rows * p.cols,
+                            cudaMemcpyDeviceToHost));
+  });
+}
+
+int specsim_trainer_set_param(specsim_trainer* t, const char* name, const float* host_in) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    const auto& p = im.param(name ? name : "");
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(im.P + p.off, host_in, sizeof(float) * p.rows * p.cols,
+                            cudaMemcpyHostToDevice));
+    kern::f32_to_bf16(im.P + p.off, im.P16 + p.off, p.rows * p.cols, im.stream);
+    SPECSIM_CHECK_LAUNCH();
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+  });
+}
+
+int specsim_trainer_get_grad(const specsim_trainer* t, const char* name, float* host_out) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    const auto& p = im.param(name ? name : "");
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(host_out, im.G + p.off, sizeof(float) * p.rows * p.cols,
+                            cudaMemcpyDeviceToHost));
+  });
+}
+
+int specsim_trainer_set_embedding(specsim_trainer* t, const uint16_t* host_bf16) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(im.E, host_bf16, 2 * im.V * im.H, cudaMemcpyHostToDevice));
+  });
+}
+
+int specsim_trainer_get_embedding(const specsim_trainer* t, uint16_t* host_bf16) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(host_bf16, im.E, 2 * im.V * im.H, cudaMemcpyDeviceToHost));
+  });
+}
+
+int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step) {
+  return guard([&] {
+    if (step < 0) throw std::invalid_argument("step must be >= 0");
+    impl_of(t).step_count = step;
+  });
+}
+
+int specsim_trainer_set_timing(specsim_trainer* t, int enabled) {
+  return guard([&] { impl_of(t).timing = enabled != 0; });
+}
+
+int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
+                                int32_t* launches7) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    for (int i = 0; i < PH_N; ++i) {
+      if (ms7) ms7[i] = im.phase_ms[i];
+      if (flops7) flops7[i] = im.phase_flops[i];
+      if (launches7) launches7[i] = im.phase_launches[i];
+    }
+  });
+}
+
+}  // extern "C"

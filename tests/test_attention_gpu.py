@@ -1,0 +1,76 @@
+"""Causal GQA attention kernels (forward + backward) vs a float64 numpy
+statement of the same maths on identical bf16 inputs."""
+import numpy as np
+import pytest
+
+from paper_2602_05145_b200 import _lib
+from _util import rand_bf16, bf16_bits_to_f32
+
+pytestmark = pytest.mark.gpu
+
+
+def ref(qkv, dO, B, S, nh, nkv, hd):
+    Q, KV = nh * hd, nkv * hd
+    x = qkv.astype(np.float64).reshape(B, S, -1)
+    q = x[..., :Q].reshape(B, S, nh, hd).transpose(0, 2, 1, 3)
+    k = x[..., Q:Q + KV].reshape(B, S, nkv, hd).transpose(0, 2, 1, 3)
+    v = x[..., Q + KV:].reshape(B, S, nkv, hd).transpose(0, 2, 1, 3)
+    rep = nh // nkv
+    k = np.repeat(k, rep, axis=1)
+    v = np.repeat(v, rep, axis=1)
+    sc = q @ k.transpose(0, 1, 3, 2) / np.sqrt(hd)
+    mask = np.triu(np.ones((S, S), bool), 1)
+    sc = np.where(mask, -np.inf, sc)
+    mx = sc.max(-1, keepdims=True)
+    e = np.exp(sc - mx)
+    l = e.sum(-1, keepdims=True)
+    p = e / l
+    o = p @ v
+    lse = (mx + np.log(l))[..., 0]  # [B, nh, S]
+    do = dO.astype(np.float64).reshape(B, S, nh, hd).transpose(0, 2, 1, 3)
+    dp = do @ v.transpose(0, 1, 3, 2)
+    D = (do * o).sum(-1, keepdims=True)
+    ds = p * (dp - D) / np.sqrt(hd)
+    dq = ds @ k
+    dk = (ds.transpose(0, 1, 3, 2) @ q).reshape(B, nkv, rep, S, hd).sum(2)
+    dv = (p.transpose(0, 1, 3, 2) @ do).reshape(B, nkv, rep, S, hd).sum(2)
+    O = o.transpose(0, 2, 1, 3).reshape(B * S, Q)
+    dQ = dq.transpose(0, 2, 1, 3).reshape(B * S, Q)
+    dK = dk.transpose(0, 2, 1, 3).reshape(B * S, KV)
+    dV = dv.transpose(0, 2, 1, 3).reshape(B * S, KV)
+    LSE = lse.transpose(1, 0, 2).reshape(nh, B * S)
+    return O, LSE, np.concatenate([dQ, dK, dV], axis=1)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("B,S,nh,nkv,hd", [(2, 128, 4, 2, 64), (1, 256, 8, 2, 128), (2, 192, 4, 4, 128),
+                                           (1, 64, 2, 1, 64)])
+def test_attention_fwd_bwd(B, S, nh, nkv, hd):
+    rng = np.random.default_rng(B * 1000 + S + nh)
+    NQ = (nh + 2 * nkv) * hd
+    qkv_bits, qkv = rand_bf16(rng, (B * S, NQ))
+    do_bits, do = rand_bf16(rng, (B * S, nh * hd))
+    o = np.zeros((B * S, nh * hd), np.uint16)
+    lse = np.zeros((nh, B * S), np.float32)
+    dqkv = np.zeros((B * S, NQ), np.uint16)
+    _lib.call("specsim_debug_attention", B, S, nh, nkv, hd, _lib.ptr(qkv_bits), _lib.ptr(do_bits),
+              _lib.ptr(o), _lib.ptr(lse), _lib.ptr(dqkv))
+    O, LSE, dQKV = ref(qkv, do, B, S, nh, nkv, hd)
+    assert rel(bf16_bits_to_f32(o), O) < 1e-2
+    np.testing.assert_allclose(lse, LSE, rtol=1e-4, atol=1e-3)
+    g = bf16_bits_to_f32(dqkv)
+    Q, KV = nh * hd, nkv * hd
+    assert rel(g[:, :Q], dQKV[:, :Q]) < 2e-2
+    assert rel(g[:, Q:Q + KV], dQKV[:, Q:Q + KV]) < 2e-2
+    assert rel(g[:, Q + KV:], dQKV[:, Q + KV:]) < 2e-2
+
+
+def test_attention_rejects_bad_shapes():
+    z = np.zeros(16, np.uint16)
+    f = np.zeros(16, np.float32)
+    with pytest.raises(_lib.DomainError):
+        _lib.call("specsim_debug_attention", 1, 100, 2, 1, 64, _lib.ptr(z), None, _lib.ptr(z),
+                  _lib.ptr(f), None)
