@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the TIDE draft-training hot path (BASELINE.json metric:
+"draft-train tokens/sec at 1/2/4/8 B200 + % bf16 tensor peak vs host-CPU ref").
+
+One step = one optimiser step of the EAGLE-3 style draft head over one
+micro-batch of synthetic captured hidden states per rank (config C2:
+Llama-3.1-8B shape, H 4096, V 128256, S 2048, B 4 -> 8192 positions per rank),
+forward + vocabulary-chunked LM-head CE + backward + (NCCL all-reduce) + AdamW.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints one JSON line (rank 0).  `value` is device-timed with inputs resident
+in the HBM signal ring; `e2e` is the same metric through the C ABI with the
+step's captured states copied from pinned host memory every step.  The
+reference arm (--impl reference) times the CPU restatement in oracle/ (the
+reference ships no trainer, SPEC.md:8 / SPEC.md:442) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOAD = "C2"
+SEED = 20260217
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=WORKLOAD)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-seq", type=int, default=256,
+                    help="positions in the bounded CPU sample (one sequence)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                    bf16_sustained=d.get("bf16_tflops_sustained", 1400.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_rank{index}.csv"
+
+    def start(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = [l.split(",") for l in self.path.read_text().splitlines() if l.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                s = float(r[1])
+                mx = max(mx, float(r[2]))
+                if float(r[3]) > 200:  # under load
+                    sm.append(s)
+                for i, n in enumerate(names):
+                    if r[5 + i].strip().lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            sm = [float(r[1]) for r in rows if len(r) > 1 and r[1].strip().replace(".", "").isdigit()]
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=mx or None,
+                    reasons=sorted(reasons), samples=len(rows))
+
+
+def ncu_traffic():
+    """dram bytes per GEMM launch from the committed ncu capture, if present."""
+    for p in sorted((ROOT / "profiles").glob("*gemm_ncu*.json")):
+        try:
+            d = json.loads(p.read_text())
+            if d.get("dram_bytes_per_launch"):
+                return d
+        except Exception:
+            pass
+    return None
+
+
+def cpu_sample(cfg, seq, threads_note=True):
+    """Time one oracle step (the CPU restatement) on a bounded sample: one
+    captured sequence of `seq` positions at the workload's model shape."""
+    import numpy as np
+    import oracle
+    shp = oracle.make_shape(cfg["hidden"], cfg["vocab"], seq, cfg["n_heads"], cfg["n_kv_heads"],
+                            cfg["head_dim"], cfg["ffn"], 1, eps=cfg["rms_eps"],
+                            theta=cfg["rope_theta"])
+    P = oracle.init_params(shp, SEED)
+    E = oracle.init_embedding(shp, SEED)
+    cap = oracle.synth_capture(SEED, 0, seq + 2, cfg["vocab"], cfg["hidden"])
+    F, u, y, m = oracle.gather_batch(shp, [(cap["ids"], cap["features"])])
+    Mst, Vst = np.zeros_like(P), np.zeros_like(P)
+    return shp, P, E, (F, u, y, m), Mst, Vst
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2602_05145_b200 import api
+    cfg = api.CONFIGS[args.config]
+    seq = args.cpu_sample_seq
+    shp, P, E, batch, Mst, Vst = cpu_sample(cfg, seq)
+    hp = [1e-4, 0.9, 0.95, 1e-8, 0.0]
+    steps = max(1, min(args.steps, 5))
+    warm = max(0, min(args.warmup, 1))
+    for k in range(warm):
+        oracle.train_step(shp, hp, k + 1, P, Mst, Vst, E, *batch)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        oracle.train_step(shp, hp, warm + k + 1, P, Mst, Vst, E, *batch)
+    dt = time.perf_counter() - t0
+    tps = steps * seq / dt
+    line = dict(impl="reference", metric="draft-train tokens/sec", value=round(tps, 3),
+                unit="tokens/s", n_gpus=args.gpus, steps=steps, warmup=warm,
+                ms_per_step=round(1e3 * dt / steps, 1), higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f32 (bf16-rounded operands)", data="synthetic",
+                config=config_block(args, cfg),
+                cpu_baseline=dict(value=round(tps, 3), unit="tokens/s", cores=oracle.num_threads(),
+                                  kind="port",
+                                  sample=f"{steps} oracle steps of 1 sequence x {seq} positions at "
+                                         f"the {args.config} model shape (full fwd+bwd+AdamW over "
+                                         "all trainable params)"),
+                e2e=dict(value=round(tps, 3), unit="tokens/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0),
+                note="the reference ships no trainer (SPEC.md:8, SPEC.md:442); this arm times the "
+                     "repo's C restatement (oracle/) of the same step on the host CPU")
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(args, cfg):
+    return dict(workload=f"{args.config}: EAGLE-3-style draft head, Llama-3.1-8B shape "
+                         f"(hidden {cfg['hidden']}, 3-layer feature concat, vocab {cfg['vocab']}, "
+                         f"seq {cfg['seq_len']}), bf16 GEMMs, synthetic captured hidden states",
+                hidden=cfg["hidden"], vocab=cfg["vocab"], seq_len=cfg["seq_len"],
+                micro_batch=cfg["micro_batch"], global_batch=cfg["micro_batch"] * args.gpus,
+                tokens_per_rank_step=cfg["micro_batch"] * cfg["seq_len"],
+                parallelism=f"dp{args.gpus}",
+                l2="inputs larger than L2 (multi-GB per-step working set; no flush needed)")
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2602_05145_b200 import _lib, api
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = api.CONFIGS[args.config]
+    B, S, H, V = cfg["micro_batch"], cfg["seq_len"], cfg["hidden"], cfg["vocab"]
+    T = B * S
+    nccl_id = None
+    if world > 1:
+        obj = [api.DraftTrainer.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    tr = api.DraftTrainer(cfg, seed=SEED, rank=rank, world=world, nccl_id=nccl_id, device=local)
+    geom = api.SignalGeometry(H)
+    pool_n = 2 * B
+    L = S + 2
+    W = 3 * H
+    buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + 2 * B) * L, device=local)
+    # synthetic captured requests; generated by the library in
+    # parallel threads (ctypes releases the GIL)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(pool_n, os.cpu_count() or 4)) as ex:
+        caps = list(ex.map(lambda i: api.synth_capture(SEED, rank * 100000 + i, L, V, H),
+                           range(pool_n)))
+    # pinned host copies of the pool for the end-to-end leg
+    pinned = []
+    for c in caps:
+        t = torch.empty((L, W), dtype=torch.int16, pin_memory=True)
+        t.numpy()[:] = c["features"].view(np.int16)
+        ids = torch.empty(L, dtype=torch.int32, pin_memory=True)
+        ids.numpy()[:] = c["ids"]
+        pinned.append((t, ids, c["alpha_s"]))
+    for i, (t, ids, a) in enumerate(pinned):
+        _lib.call("specsim_hsbuf_append_packed", buf.h, i, a, t.data_ptr(), ids.data_ptr(), L, 0)
+
+    def batch(k):
+        return [(k * B + j) % pool_n for j in range(B)]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ------------------------------------------------------------ device-timed leg
+    for k in range(args.warmup):
+        tr.step(buf, batch(k))
+    tr.set_timing(True)
+    phase_acc = {p: dict(ms=0.0, flops=0.0, launches=0) for p in api.DraftTrainer.PHASES}
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    launches0 = _lib.kernel_launches()
+    tr.region_begin()
+    losses = []
+    for k in range(args.steps):
+        r = tr.step(buf, batch(args.warmup + k))
+        losses.append(r["loss"])
+        for p, v in tr.phase_times().items():
+            for f in ("ms", "flops", "launches"):
+                phase_acc[p][f] += v[f]
+    region_ms = tr.region_end()
+    launches = _lib.kernel_launches() - launches0
+    clk = clocks.stop()
+    tr.set_timing(False)
+    barrier()
+    region_ms = max_over_ranks(region_ms)
+    value = world * T * args.steps / (region_ms / 1e3)
+
+    # ------------------------------------------------------------ end-to-end leg
+    e2e = None
+    if not args.no_e2e:
+        next_id = pool_n
+        h2d = B * L * (W * 2 + 4)
+        for k in range(max(1, args.warmup)):  # warm the staging path
+            ids = []
+            for j in range(B):
+                t, idt, a = pinned[(k * B + j) % pool_n]
+                _lib.call("specsim_hsbuf_append_packed", buf.h, next_id, a, t.data_ptr(),
+                          idt.data_ptr(), L, 0)
+                ids.append(next_id)
+                next_id += 1
+            tr.step(buf, ids)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            ids = []
+            for j in range(B):
+                t, idt, a = pinned[(k * B + j) % pool_n]
+                # H2D of this step's captured states (pinned -> HBM ring)
+                _lib.call("specsim_hsbuf_append_packed", buf.h, next_id, a, t.data_ptr(),
+                          idt.data_ptr(), L, 0)
+                ids.append(next_id)
+                next_id += 1
+            r = tr.step(buf, ids)  # returns loss / counters: D2H of the step result
+            losses.append(r["loss"])
+        barrier()
+        dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = dict(value=round(world * T * args.steps / dt, 1), unit="tokens/s",
+                   h2d_bytes_per_step=h2d, d2h_bytes_per_step=3 * 8,
+                   ms_per_step=round(1e3 * dt / args.steps, 2))
+
+    # ------------------------------------------------------------ roofline
+    pk = peaks()
+    fl = api.gemm_flops_per_token(cfg)
+    gemm_ms = phase_acc["gemm"]["ms"] + phase_acc["lm_head_ce"]["ms"]
+    gemm_alg = phase_acc["gemm"]["flops"] + phase_acc["lm_head_ce"]["flops"]
+    achieved = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    traffic = ncu_traffic()
+    roofline = dict(bound="tensor", kernel="gemm_kernel<tcgen05> (all GEMM launches of the step)",
+                    achieved=round(achieved, 1) if achieved else None,
+                    peak=pk["bf16_sustained"], unit="TFLOP/s",
+                    frac=round(achieved / pk["bf16_sustained"], 4) if achieved else None,
+                    peak_source=f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)",
+                    traffic=traffic.get("dram_bytes_per_launch") if traffic else None,
+                    traffic_kernel=traffic.get("kernel") if traffic else None,
+                    algorithmic="SURVEY §8(d): sum of GEMM FLOPs excluding the CE-backward logit "
+                                "recompute, over the summed device time of every GEMM launch "
+                                "(recompute time included)")
+    step_ms = region_ms / args.steps
+    phases = {p: dict(ms_per_step=round(v["ms"] / args.steps, 3),
+                      launches_per_step=v["launches"] // max(1, args.steps))
+              for p, v in phase_acc.items()}
+    whole_step_tflops = fl["total"] * T / (step_ms / 1e3) / 1e12
+
+    line = dict(metric="draft-train tokens/sec", value=round(value, 1), unit="tokens/s",
+                n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=round(step_ms, 3), higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="bf16", data="synthetic (seeded captured hidden states, "
+                "random-init draft weights)", config=config_block(args, cfg), e2e=e2e,
+                roofline=roofline, gpu_launches=int(launches),
+                whole_step=dict(tflops=round(whole_step_tflops, 1),
+                                frac_of_peak=round(whole_step_tflops / pk["bf16_sustained"], 4),
+                                gflop_per_token=round(fl["total"] / 1e9, 4)),
+                phases=phases, loss_first_last=[round(losses[0], 4), round(losses[-1], 4)],
+                clocks=clk)
+
+    # ------------------------------------------------------------ CPU baseline
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            seq = args.cpu_sample_seq
+            shp, P, E, batch_c, Mst, Vst = cpu_sample(cfg, seq)
+            t0 = time.perf_counter()
+            oracle.train_step(shp, [1e-4, 0.9, 0.95, 1e-8, 0.0], 1, P, Mst, Vst, E, *batch_c)
+            dtc = time.perf_counter() - t0
+            line["cpu_baseline"] = dict(
+                value=round(seq / dtc, 3), unit="tokens/s", cores=oracle.num_threads(),
+                kind="port",
+                sample=f"1 oracle step (fwd+bwd+AdamW, all {args.config} params) on 1 sequence x "
+                       f"{seq} positions; {dtc:.1f} s")
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = dict(value=None, unit="tokens/s", cores=os.cpu_count(),
+                                        kind="port", sample=f"failed: {e}")
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    tr.close()
+    buf.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

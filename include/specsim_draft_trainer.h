@@ -54,6 +54,8 @@ typedef enum specsim_status {
 /* Message of the last failing call on this thread ("" if none). */
 const char* specsim_last_error(void);
 const char* specsim_version(void);
+/* Device kernels launched by this library so far (all handles, all streams). */
+int specsim_kernel_launches(uint64_t* out);
 
 /* ------------------------------------------------- bookkeeping (host only) */
 /* Seeded mt19937_64 with the reference's hand-rolled conversions
@@ -237,6 +239,10 @@ int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step);
  * 2 attention, 3 norms/elementwise, 4 LM-head+CE GEMMs, 5 AdamW,
  * 6 all-reduce.  flops[i] = algorithmic FLOPs of the phase (GEMM phases). */
 int specsim_trainer_set_timing(specsim_trainer* t, int enabled);
+/* Device-timed region on the trainer's stream: end == 0 records the start
+ * event, end != 0 records the stop event, waits, and returns the elapsed ms
+ * (idle gaps between steps included). */
+int specsim_trainer_region(specsim_trainer* t, int end, double* ms);
 int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
                                 int32_t* launches7);
 

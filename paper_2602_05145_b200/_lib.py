@@ -73,6 +73,7 @@ PF32, PF64, PU16 = C.POINTER(C.c_float), C.POINTER(C.c_double), C.POINTER(C.c_ui
 SIGNATURES = {
     "specsim_last_error": [],
     "specsim_version": [],
+    "specsim_kernel_launches": [PU64],
     "specsim_rng_create": [U64, C.POINTER(P)],
     "specsim_rng_destroy": [P],
     "specsim_rng_uniform": [P, PF64],
@@ -108,6 +109,7 @@ SIGNATURES = {
     "specsim_trainer_get_embedding": [P, P],
     "specsim_trainer_set_step_count": [P, I64],
     "specsim_trainer_set_timing": [P, C.c_int],
+    "specsim_trainer_region": [P, C.c_int, PF64],
     "specsim_trainer_phase_times": [P, PF64, PF64, PI32],
     "specsim_debug_gemm": [C.c_int, C.c_int, C.c_int, I32, I32, I32, P, I64, P, I64, P, I64, P,
                            I64, I32, PF32],
@@ -135,6 +137,12 @@ def lib() -> C.CDLL:
             fn.restype = _RESTYPE.get(name, C.c_int)
         _lib = L
     return _lib
+
+
+def kernel_launches() -> int:
+    o = C.c_uint64()
+    check(lib().specsim_kernel_launches(C.byref(o)))
+    return o.value
 
 
 def exported_symbols() -> list[str]:

@@ -293,6 +293,14 @@ class DraftTrainer:
     def set_step_count(self, k):
         call("specsim_trainer_set_step_count", self.h, k)
 
+    def region_begin(self):
+        call("specsim_trainer_region", self.h, 0, None)
+
+    def region_end(self) -> float:
+        ms = C.c_double()
+        call("specsim_trainer_region", self.h, 1, C.byref(ms))
+        return ms.value
+
     def set_timing(self, on: bool):
         call("specsim_trainer_set_timing", self.h, 1 if on else 0)
 

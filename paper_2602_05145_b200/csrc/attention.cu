@@ -555,6 +555,7 @@ void fwd_t(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d
     init = true;
   }
   dim3 grid(d.S / 64, d.nh, d.B);
+  count_launches();
   attn_fwd_kernel<HD><<<grid, 128, smem, s>>>(qkv, o, lse, d);
 }
 
@@ -563,6 +564,7 @@ void bwd_t(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16
            const float* lse, float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, cudaStream_t s) {
   const long long T = static_cast<long long>(d.B) * d.S;
   const long long warps = T * d.nh;
+  count_launches();
   attn_bwd_dot_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(dout, o,
                                                                                       Dbuf, d, HD);
   const int smem_kv = (2 * 64 + 4 * 32) * HD * 2 + 4 * 32 * 4;
@@ -575,8 +577,10 @@ void bwd_t(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
     init = true;
   }
+  count_launches();
   attn_bwd_dkdv_kernel<HD><<<dim3(d.S / 64, d.nkv, d.B), 128, smem_kv, s>>>(qkv, dout, lse, Dbuf,
                                                                            dqkv, d);
+  count_launches();
   attn_bwd_dq_kernel<HD><<<dim3(d.S / 64, d.nh, d.B), 128, smem_q, s>>>(qkv, dout, lse, Dbuf, dqkv,
                                                                        d);
 }

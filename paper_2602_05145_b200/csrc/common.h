@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -65,6 +67,11 @@ class Problems {
 };
 
 void set_last_error(const std::string& msg);
+
+// Number of device kernels this library has launched (all streams); read by
+// the benchmark as its gpu_launches evidence.
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void count_launches(unsigned n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // Runs f, mapping exceptions onto specsim_status codes.
 template <class F>

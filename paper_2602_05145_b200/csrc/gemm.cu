@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "common.h"
 #include "gemm.cuh"
 
 namespace specsim {
@@ -72,6 +73,7 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr_set = true;
   }
+  count_launches();
   k<<<p.grid, NUM_THREADS, SMEM_BYTES, s>>>(p.map_a, p.map_b, p.args);
 }
 

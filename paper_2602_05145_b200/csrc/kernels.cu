@@ -451,23 +451,27 @@ void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long 
                   const BatchSpec& spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
                   int32_t* m, cudaStream_t s) {
   const long long T = static_cast<long long>(B) * S;
+  count_launches();
   gather_batch_kernel<<<static_cast<unsigned>(T), 256, 0, s>>>(
       reinterpret_cast<const uint4*>(ring_feat), ring_ids, cap, W / 8, spec, S,
       reinterpret_cast<uint4*>(F), u, y, m);
 }
 
 void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s) {
+  count_launches();
   mask_count_kernel<<<1, 1024, 0, s>>>(m, T, out);
 }
 
 void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T,
              cudaStream_t s) {
+  count_launches();
   ce_coef_kernel<<<blocks_for(T, 256), 256, 0, s>>>(m, n_global, coef, T);
 }
 
 void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, const float* w,
                  float eps, __nv_bfloat16* y, long long ldy, float* rstd, long long T, int H,
                  cudaStream_t s) {
+  count_launches();
   rmsnorm_fwd_kernel<<<static_cast<unsigned>(T), kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y,
                                                                        ldy, rstd, H);
 }
@@ -479,41 +483,49 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
                  float* out_f32, __nv_bfloat16* out_bf16, long long ldo, float* dw,
                  float* dw_partial, long long T, int H, cudaStream_t s) {
   const long long nb = rmsnorm_bwd_partial_rows(T);
+  count_launches();
   rmsnorm_bwd_kernel<<<static_cast<unsigned>(nb), kNormThreads, 0, s>>>(
       dy, lddy, x, ldx, gather, w, rstd, resid, out_f32, out_bf16, ldo, dw_partial, T, H);
+  count_launches();
   colsum_kernel<<<blocks_for(H, 256), 256, 0, s>>>(dw_partial, nb, H, dw);
 }
 
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,
           const float* cos_t, const float* sin_t, bool inverse, cudaStream_t s) {
   const long long n = T * n_rot_heads * (hd / 4);
+  count_launches();
   rope_kernel<<<blocks_for(n, 256), 256, 0, s>>>(qkv, T, S, NQ, n_rot_heads, hd, cos_t, sin_t,
                                                  inverse ? 1 : 0);
 }
 
 void swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* act, long long T, int I, cudaStream_t s) {
+  count_launches();
   swiglu_fwd_kernel<<<blocks_for(T * (I / 8), 256), 256, 0, s>>>(gu, act, T, I);
 }
 
 void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat16* dgu,
                 long long T, int I, cudaStream_t s) {
+  count_launches();
   swiglu_bwd_kernel<<<blocks_for(T * (I / 8), 256), 256, 0, s>>>(gu, dact, dgu, T, I);
 }
 
 void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,
                const int32_t* m, float* lse, float* row_loss, int32_t* argmax, cudaStream_t s) {
+  count_launches();
   ce_reduce_kernel<<<blocks_for(T * 32, 256), 256, 0, s>>>(partials, num_nb, T, y, m, lse,
                                                            row_loss, argmax);
 }
 
 void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,
                  const long long* n_global, long long T, double* stats, cudaStream_t s) {
+  count_launches();
   ce_finalize_kernel<<<1, 1024, 0, s>>>(row_loss, argmax, y, m, n_global, T, stats);
 }
 
 void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloat16* p16,
            const AdamHyper& hp, cudaStream_t s) {
   const long long n4 = n / 4;  // n is a multiple of 8 (checked at trainer creation)
+  count_launches();
   adamw_kernel<<<blocks_for(n4, 256), 256, 0, s>>>(
       n4, reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(m),
       reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
@@ -521,6 +533,7 @@ void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloa
 }
 
 void f32_to_bf16(const float* x, __nv_bfloat16* y, long long n, cudaStream_t s) {
+  count_launches();
   f32_to_bf16_kernel<<<blocks_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
                                                             reinterpret_cast<uint2*>(y), n / 4);
 }
@@ -528,6 +541,7 @@ void f32_to_bf16(const float* x, __nv_bfloat16* y, long long n, cudaStream_t s) 
 void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, const int32_t* idx,
                   int n, __nv_bfloat16* ring_feat, long long cap, long long pos, cudaStream_t s) {
   if (n <= 0) return;
+  count_launches();
   pack_signals_kernel<<<n, 128, 0, s>>>(layers, n_layers, ld, H / 8, idx,
                                         n, reinterpret_cast<uint4*>(ring_feat), cap, pos);
 }
@@ -535,6 +549,7 @@ void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, co
 void pack_packed(const __nv_bfloat16* src, int W, int n, __nv_bfloat16* ring_feat, long long cap,
                  long long pos, cudaStream_t s) {
   if (n <= 0) return;
+  count_launches();
   pack_packed_kernel<<<n, 128, 0, s>>>(reinterpret_cast<const uint4*>(src), W / 8, n,
                                        reinterpret_cast<uint4*>(ring_feat), cap, pos);
 }

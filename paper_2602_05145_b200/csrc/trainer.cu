@@ -149,6 +149,7 @@ class DraftTrainerImpl {
   std::vector<cudaEvent_t> event_pool;
   size_t event_next = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_region[2] = {nullptr, nullptr};
 
   const Param& param(const std::string& name) const {
     for (const auto& p : params)
@@ -272,6 +273,8 @@ class DraftTrainerImpl {
     build_plans();
     SPECSIM_CUDA(cudaEventCreate(&ev_begin));
     SPECSIM_CUDA(cudaEventCreate(&ev_end));
+    SPECSIM_CUDA(cudaEventCreate(&ev_region[0]));
+    SPECSIM_CUDA(cudaEventCreate(&ev_region[1]));
     if (world > 1) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
@@ -287,6 +290,8 @@ class DraftTrainerImpl {
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
+    for (auto e : ev_region)
+      if (e) cudaEventDestroy(e);
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
     if (stream) cudaStreamDestroy(stream);
@@ -906,6 +911,20 @@ int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step) {
   return guard([&] {
     if (step < 0) throw std::invalid_argument("step must be >= 0");
     impl_of(t).step_count = step;
+  });
+}
+
+int specsim_trainer_region(specsim_trainer* t, int end, double* ms) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaEventRecord(im.ev_region[end ? 1 : 0], im.stream));
+    if (end) {
+      SPECSIM_CUDA(cudaEventSynchronize(im.ev_region[1]));
+      float v = 0;
+      SPECSIM_CUDA(cudaEventElapsedTime(&v, im.ev_region[0], im.ev_region[1]));
+      if (ms) *ms = v;
+    }
   });
 }
 
