@@ -78,6 +78,12 @@ int specsim_alpha_from_accept_length(double ell, int32_t gamma, double* out);
 /* SPEC.md:348 chronological 9:1 split: the oldest floor(9n/10) samples train. */
 int specsim_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
 
+/* Data-parallel sharding of a job: optimiser step `step` takes
+ * items [step*per_rank*world, (step+1)*per_rank*world); item i of that slice
+ * goes to rank i mod world.  Writes this rank's item indices (<= per_rank). */
+int specsim_dp_shard(int64_t n_items, int32_t per_rank, int32_t world, int32_t rank,
+                     int64_t step, int64_t* out_idx, int32_t* out_n);
+
 /* ------------------------------------------------------ signal geometry */
 /* bytes per token = layers_tapped * hidden_dim * bytes_per_element */
 typedef struct specsim_signal_geometry {

@@ -103,6 +103,13 @@ def split_train_eval(n: int):
     return a.value, b.value
 
 
+def dp_shard(n_items: int, per_rank: int, world: int, rank: int, step: int):
+    idx = np.zeros(max(1, per_rank), np.int64)
+    n = C.c_int32()
+    call("specsim_dp_shard", n_items, per_rank, world, rank, step, ptr(idx), C.byref(n))
+    return idx[: n.value].tolist()
+
+
 @dataclass
 class SignalGeometry:
     hidden_dim: int

@@ -5,6 +5,7 @@
 // SPEC.md:294) and are checked bit-exact against the compiled
 // reference by tests/test_bookkeeping_capi.py.  Compiled without FP
 // contraction (see Makefile) so every double rounds like the reference.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <numbers>
@@ -183,6 +184,29 @@ int specsim_bytes_per_token(const specsim_signal_geometry* g, int64_t* out) {
     *out = geo.bytes_per_token();
   });
 }
+int specsim_dp_shard(int64_t n_items, int32_t per_rank, int32_t world, int32_t rank,
+                     int64_t step, int64_t* out_idx, int32_t* out_n) {
+  return guard([&] {
+    Problems p("dp_shard");
+    p.check(n_items >= 0, "n_items must be >= 0");
+    p.check(per_rank >= 1, "per_rank must be >= 1");
+    p.check(world >= 1 && rank >= 0 && rank < world, "rank must be in [0, world)");
+    p.check(step >= 0, "step must be >= 0");
+    p.check(out_n != nullptr, "out_n is null");
+    p.throw_if_any();
+    // step k covers items [k*per_rank*world, (k+1)*per_rank*world); item i of
+    // that slice goes to rank i mod world
+    const int64_t s0 = step * per_rank * static_cast<int64_t>(world);
+    int32_t n = 0;
+    for (int64_t i = s0 + rank; i < std::min<int64_t>(n_items, s0 + per_rank * static_cast<int64_t>(world));
+         i += world) {
+      if (out_idx) out_idx[n] = i;
+      ++n;
+    }
+    *out_n = n;
+  });
+}
+
 int specsim_synth_capture(uint64_t seed, int64_t index, int32_t length, int32_t vocab,
                           int32_t hidden, int32_t layers, double alpha, int32_t gamma,
                           int32_t* ids, uint16_t* features, int32_t* accept_lengths,

@@ -662,6 +662,17 @@ class DraftTrainerImpl {
     return end_step();
   }
 
+  // sample i of step k's slice -> rank i mod world (same rule as specsim_dp_shard)
+  void shard(long long n, long long k, std::vector<int64_t>& mine,
+             const std::vector<int64_t>& ids) const {
+    mine.clear();
+    int64_t idx[kern::kMaxBatch];
+    int32_t cnt = 0;
+    if (specsim_dp_shard(n, sh.micro_batch, world, rank, k, idx, &cnt) != SPECSIM_OK)
+      throw std::invalid_argument(specsim_last_error());
+    for (int i = 0; i < cnt; ++i) mine.push_back(ids[idx[i]]);
+  }
+
   TrainingOutcome train(HiddenStateBuffer& buf, const TrainJob& job) {
     Problems p("train job");
     p.check(!job.train_ids.empty(), "D_train must be non-empty (SPEC.md:398 requires n > 0)");
@@ -674,11 +685,8 @@ class DraftTrainerImpl {
     std::vector<int64_t> mine;
     for (int ep = 0; ep < job.epochs; ++ep) {
       const long long n = static_cast<long long>(job.train_ids.size());
-      for (long long s0 = 0; s0 < n; s0 += per_step) {
-        mine.clear();
-        // sample i of the step slice -> rank i mod world
-        for (long long i = s0 + rank; i < std::min(n, s0 + per_step); i += world)
-          mine.push_back(job.train_ids[i]);
+      for (long long s0 = 0, k = 0; s0 < n; s0 += per_step, ++k) {
+        shard(n, k, mine, job.train_ids);
         const StepResult r = step(buf, mine.data(), static_cast<int>(mine.size()), 0);
         loss_sum += r.loss;
         ++steps;
@@ -687,10 +695,8 @@ class DraftTrainerImpl {
     // alpha_eval = top-1 accuracy of the new draft on D_eval
     int64_t valid = 0, correct = 0;
     const long long ne = static_cast<long long>(job.eval_ids.size());
-    for (long long s0 = 0; s0 < ne; s0 += per_step) {
-      mine.clear();
-      for (long long i = s0 + rank; i < std::min(ne, s0 + per_step); i += world)
-        mine.push_back(job.eval_ids[i]);
+    for (long long s0 = 0, k = 0; s0 < ne; s0 += per_step, ++k) {
+      shard(ne, k, mine, job.eval_ids);
       const StepResult r = eval(buf, mine.data(), static_cast<int>(mine.size()));
       valid += r.valid_tokens;
       correct += r.top1_correct;

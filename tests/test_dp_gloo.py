@@ -1,0 +1,102 @@
+"""Data-parallel path on CPU with world_size 2 (gloo): each rank takes its
+shard by the library's sharding rule (specsim_dp_shard, the same rule
+DraftTrainer::train uses), runs the oracle step with the globally all-reduced
+valid-token count, all-reduces (sums) the gradients and applies AdamW.  The
+result must equal the single-process step on the whole global batch — the
+property the NCCL path in trainer.cu relies on (loss normalised by the global
+sum of masks, gradients summed)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2602_05145_b200 import api
+
+SH = dict(H=64, V=512, S=32, nh=4, nkv=2, hd=16, I=128)
+HP = [1e-3, 0.9, 0.95, 1e-8, 0.01]
+LENS = [34, 20, 34, 9, 34, 30]  # 6 samples, some short (masked tails)
+WORLD, PER_RANK = 2, 2
+
+
+def samples():
+    out = []
+    for i, L in enumerate(LENS):
+        c = oracle.synth_capture(5, i, L, SH["V"], SH["H"])
+        out.append((c["ids"], c["features"]))
+    return out
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    shp = oracle.make_shape(**SH, B=PER_RANK)
+    P = oracle.init_params(shp, 3)
+    E = oracle.init_embedding(shp, 3)
+    smp = samples()
+    Mst, Vst = np.zeros_like(P), np.zeros_like(P)
+    results = []
+    for step in range(2):  # 6 samples, 4 per global step -> second step is partial
+        mine = api.dp_shard(len(LENS), PER_RANK, WORLD, rank, step)
+        F, u, y, m = oracle.gather_batch(shp, [smp[i] for i in mine])
+        n = torch.tensor([int(m.sum())], dtype=torch.int64)
+        dist.all_reduce(n)
+        out, g = oracle.train_step(shp, HP, step + 1, P, Mst, Vst, E, F, u, y, m,
+                                   global_valid=int(n.item()), update=False)
+        gt = torch.from_numpy(g)
+        dist.all_reduce(gt)
+        loss = torch.tensor([out.loss], dtype=torch.float64)
+        dist.all_reduce(loss)
+        oracle.adamw(P, Mst, Vst, gt.numpy(), HP, step + 1)
+        results.append((float(loss.item()), gt.numpy().copy(), P.copy(), mine))
+    if rank == 0:
+        q.put(results)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharding_rule():
+    got = [api.dp_shard(6, 2, 2, r, s) for s in range(2) for r in range(2)]
+    assert got == [[0, 2], [1, 3], [4], [5]]
+    assert api.dp_shard(3, 4, 1, 0, 0) == [0, 1, 2]
+    assert api.dp_shard(10, 2, 4, 3, 1) == [] and api.dp_shard(10, 2, 4, 1, 1) == [9]
+
+
+def test_world2_equals_single_process_global_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single process, whole global batch of each step
+    shp = oracle.make_shape(**SH, B=PER_RANK * WORLD)
+    P = oracle.init_params(shp, 3)
+    E = oracle.init_embedding(shp, 3)
+    smp = samples()
+    Mst, Vst = np.zeros_like(P), np.zeros_like(P)
+    for step in range(2):
+        batch = smp[step * 4:(step + 1) * 4]
+        F, u, y, m = oracle.gather_batch(shp, batch)
+        out, g = oracle.train_step(shp, HP, step + 1, P, Mst, Vst, E, F, u, y, m)
+        loss_dp, g_dp, P_dp, _ = res[step]
+        assert abs(loss_dp - out.loss) < 1e-6 * abs(out.loss)
+        assert np.linalg.norm(g_dp - g) / np.linalg.norm(g) < 1e-5
+        assert np.abs(P_dp - P).max() < 1e-3 * HP[0] + 1e-7

@@ -22,6 +22,10 @@ SHAPES = {
     "C1": api.CONFIGS["C1"],
     "gqa128": dict(hidden=256, vocab=2048, seq_len=128, n_heads=4, n_kv_heads=1, head_dim=128,
                    ffn=512, micro_batch=3, rms_eps=1e-6, rope_theta=500000.0),
+    # vocabulary > one 32k backward chunk and not a multiple of the 256-wide N tile
+    # (exercises the chunk loop, the fp32-accumulate dX epilogue and N tails, as C2/C4 do)
+    "bigvocab": dict(hidden=256, vocab=40000, seq_len=128, n_heads=4, n_kv_heads=2, head_dim=64,
+                     ffn=512, micro_batch=4, rms_eps=1e-5, rope_theta=10000.0),
 }
 
 
