@@ -81,8 +81,12 @@ class HiddenStateBuffer {
   void append(int64_t sample_id, double alpha, const void* const* layer_ptrs, int64_t rows,
               int64_t ld, const int32_t* token_ids, const int32_t* accepted_idx, int n,
               bool on_device);
+  // mode 0: host (copied before return); 1: device; 2: page-locked host,
+  // asynchronous (the buffer must stay unmodified until the next step / eval
+  // on this buffer returns or sync() is called).
   void append_packed(int64_t sample_id, double alpha, const uint16_t* features,
-                     const int32_t* token_ids, int n, bool on_device);
+                     const int32_t* token_ids, int n, int mode);
+  void sync() const;
 
   Stats stats() const { return stats_; }
   const Sample& sample(int64_t id) const;  // throws std::out_of_range if evicted/unknown
@@ -94,6 +98,7 @@ class HiddenStateBuffer {
   const int32_t* ring_ids() const { return ring_ids_; }
   int device() const { return device_; }
   void* stream() const { return stream_; }
+  void* ready_event() const { return ready_; }
 
  private:
   void open_sample(int64_t sample_id, double alpha);
@@ -104,6 +109,7 @@ class HiddenStateBuffer {
   int64_t cap_, flush_threshold_;
   int device_;
   void* stream_ = nullptr;
+  void* ready_ = nullptr;  // cudaEvent_t recorded after the latest append
   void* ring_feat_ = nullptr;
   int32_t* ring_ids_ = nullptr;
   void* staging_dev_ = nullptr;   // device staging for host appends

@@ -144,10 +144,17 @@ int specsim_hsbuf_append(specsim_hsbuf* buf, int64_t sample_id, double alpha,
                          const int32_t* token_ids, const int32_t* accepted_idx, int32_t n,
                          int on_device);
 
-/* Same, with records already packed [n, layers*hidden] (host or device). */
+/* Same, with records already packed [n, layers*hidden].  mode 0: host memory,
+ * copied before return; 1: device memory; 2: page-locked host memory, copied
+ * ASYNCHRONOUSLY on the buffer's stream so the DMA overlaps a running step —
+ * the caller keeps the buffers unmodified until the next trainer step / eval
+ * on this buffer returns or specsim_hsbuf_sync() is called.  Trainer steps
+ * are ordered after every append by an event (no host synchronisation). */
 int specsim_hsbuf_append_packed(specsim_hsbuf* buf, int64_t sample_id, double alpha,
                                 const uint16_t* features, const int32_t* token_ids, int32_t n,
-                                int on_device);
+                                int mode);
+/* Waits for every append issued on the buffer. */
+int specsim_hsbuf_sync(specsim_hsbuf* buf);
 
 int specsim_hsbuf_stats_get(const specsim_hsbuf* buf, specsim_hsbuf_stats* out);
 int specsim_hsbuf_sample_info(const specsim_hsbuf* buf, int64_t sample_id, int32_t* length,
@@ -255,9 +262,10 @@ int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* f
 /* ------------------------------------------------------ kernel test hooks */
 /* Host-buffer wrappers around single kernels, used by the parity tests.
  * GEMM: epi 0 bf16 out, 1 f32 out, 2 f32 accumulate (C in/out), 3 bf16 out
- * plus residual R.  A is [M, lda] (K-major) or [K, lda] (MN-major); B is
+ * plus residual R; bits 8..15 of epi select the CTA group (0 = default pair
+ * kernel cta_group::2, 1 = single-CTA cta_group::1).  A is [M, lda] (K-major) or [K, lda] (MN-major); B is
  * [N, ldb] or [K, ldb].  iters > 1 re-launches and reports mean kernel ms. */
-int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_t N, int32_t K,
+int specsim_debug_gemm(int a_mn, int b_mn, int epi_cg, int32_t M, int32_t N, int32_t K,
                        const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb, void* C,
                        int64_t ldc, const uint16_t* R, int64_t ldr, int32_t iters,
                        float* mean_ms);

@@ -91,6 +91,7 @@ SIGNATURES = {
     "specsim_hsbuf_destroy": [P],
     "specsim_hsbuf_append": [P, I64, F64, C.POINTER(P), I64, I64, P, P, I32, C.c_int],
     "specsim_hsbuf_append_packed": [P, I64, F64, P, P, I32, C.c_int],
+    "specsim_hsbuf_sync": [P],
     "specsim_hsbuf_stats_get": [P, C.POINTER(HsbufStats)],
     "specsim_hsbuf_sample_info": [P, I64, PI32, PF64],
     "specsim_hsbuf_read_sample": [P, I64, P, P],

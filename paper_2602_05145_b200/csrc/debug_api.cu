@@ -26,12 +26,14 @@ struct DevBuf {
 }  // namespace
 }  // namespace specsim
 
-extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_t N, int32_t K,
+extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi_cg, int32_t M, int32_t N, int32_t K,
                                   const uint16_t* A, int64_t lda, const uint16_t* B, int64_t ldb,
                                   void* C, int64_t ldc, const uint16_t* R, int64_t ldr,
                                   int32_t iters, float* mean_ms) {
   using namespace specsim;
   return guard([&] {
+    const int epi = epi_cg & 0xff;
+    const int cg = (epi_cg >> 8) ? (epi_cg >> 8) : 2;
     Problems pr("specsim_debug_gemm");
     pr.check(M > 0 && N > 0 && K > 0, "M, N, K must be > 0");
     pr.check(A && B && C, "A, B, C must be non-null");
@@ -53,7 +55,7 @@ extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi, int32_t M, int32_
     args.R = static_cast<const __nv_bfloat16*>(dR.p);
     args.ldr = ldr;
     gemm::GemmPlan plan = gemm::make_plan({dA.p, lda, a_mn != 0}, {dB.p, ldb, b_mn != 0}, M, N,
-                                          K, epi, args);
+                                          K, epi, args, cg);
     cudaStream_t s;
     SPECSIM_CUDA(cudaStreamCreate(&s));
     plan.launch(s);

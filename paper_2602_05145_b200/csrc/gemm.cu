@@ -65,51 +65,93 @@ int num_sms() {
   return n;
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int CG>
 void launch_t(const GemmPlan& p, cudaStream_t s) {
-  auto k = gemm_kernel<A_MN, B_MN, EPI>;
+  auto k = gemm_kernel<A_MN, B_MN, EPI, CG>;
+  constexpr int smem = Cfg<CG>::SMEM;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    SPECSIM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   count_launches();
-  k<<<p.grid, NUM_THREADS, SMEM_BYTES, s>>>(p.map_a, p.map_b, p.args);
+  if constexpr (CG == 1) {
+    k<<<p.grid, NUM_THREADS, smem, s>>>(p.map_a, p.map_b, p.args);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pair on one TPC
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SPECSIM_CUDA(cudaLaunchKernelEx(&cfg, k, p.map_a, p.map_b, p.args));
+  }
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int CG>
 void dispatch_epi(const GemmPlan& p, cudaStream_t s) {
   switch (p.epi) {
-    case EPI_BF16: launch_t<A_MN, B_MN, EPI_BF16>(p, s); break;
-    case EPI_F32: launch_t<A_MN, B_MN, EPI_F32>(p, s); break;
-    case EPI_F32_ACC: launch_t<A_MN, B_MN, EPI_F32_ACC>(p, s); break;
-    case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID>(p, s); break;
-    case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD>(p, s); break;
-    case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD>(p, s); break;
+    case EPI_BF16: launch_t<A_MN, B_MN, EPI_BF16, CG>(p, s); break;
+    case EPI_F32: launch_t<A_MN, B_MN, EPI_F32, CG>(p, s); break;
+    case EPI_F32_ACC: launch_t<A_MN, B_MN, EPI_F32_ACC, CG>(p, s); break;
+    case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID, CG>(p, s); break;
+    case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD, CG>(p, s); break;
+    case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
+}
+
+template <int CG>
+void dispatch_major(const GemmPlan& p, cudaStream_t s) {
+  if (!p.a_mn && !p.b_mn)
+    dispatch_epi<false, false, CG>(p, s);
+  else if (!p.a_mn && p.b_mn)
+    dispatch_epi<false, true, CG>(p, s);
+  else if (p.a_mn && p.b_mn)
+    dispatch_epi<true, true, CG>(p, s);
+  else
+    dispatch_epi<true, false, CG>(p, s);
 }
 
 }  // namespace
 
 GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
-                   const Args& extra) {
+                   const Args& extra, int cg) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: empty shape");
+  if (cg != 1 && cg != 2) throw std::invalid_argument("gemm: cg must be 1 or 2");
   GemmPlan p;
   p.a_mn = A.mn_major;
   p.b_mn = B.mn_major;
   p.epi = epi;
-  // A: K-major = [M, K] rows; MN-major = [K, M] rows.
+  p.cg = cg;
+  const int bn_cta = BN / cg;
+  // A: K-major = [M, K] rows; MN-major = [K, M] rows.  Boxes are per CTA.
   p.map_a = A.mn_major ? make_map(A.ptr, K, M, A.ld, 64, 64) : make_map(A.ptr, M, K, A.ld, 64, BM);
-  p.map_b = B.mn_major ? make_map(B.ptr, K, N, B.ld, 64, 64) : make_map(B.ptr, N, K, B.ld, 64, BN);
+  p.map_b =
+      B.mn_major ? make_map(B.ptr, K, N, B.ld, 64, 64) : make_map(B.ptr, N, K, B.ld, 64, bn_cta);
   p.args = extra;
   p.args.M = M;
   p.args.N = N;
   p.args.K = K;
-  p.args.num_m_blocks = (M + BM - 1) / BM;
+  const int tile_m = BM * cg;
+  p.args.num_m_blocks = (M + tile_m - 1) / tile_m;
   p.args.num_n_blocks = (N + BN - 1) / BN;
   p.args.num_tiles = p.args.num_m_blocks * p.args.num_n_blocks;
-  p.grid = p.args.num_tiles < num_sms() ? p.args.num_tiles : num_sms();
+  // Row group: keep the group's A panel (tile_m x K bf16 per row block) within
+  // ~64 MB of the 126 MB L2 so B panels stream from DRAM about once.
+  const long long panel = static_cast<long long>(tile_m) * K * 2;
+  long long gm = (64ll << 20) / (panel > 0 ? panel : 1);
+  if (gm < 1) gm = 1;
+  if (gm > p.args.num_m_blocks) gm = p.args.num_m_blocks;
+  p.args.group_m = static_cast<int>(gm);
+  const int units = num_sms() / cg;  // CTA pairs (or CTAs) resident at once
+  p.grid = (p.args.num_tiles < units ? p.args.num_tiles : units) * cg;
   p.flops = 2.0 * M * static_cast<double>(N) * K;
   if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
       epi == EPI_F32_ACC) {
@@ -121,14 +163,10 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
 }
 
 void GemmPlan::launch(cudaStream_t s) const {
-  if (!a_mn && !b_mn)
-    dispatch_epi<false, false>(*this, s);
-  else if (!a_mn && b_mn)
-    dispatch_epi<false, true>(*this, s);
-  else if (a_mn && b_mn)
-    dispatch_epi<true, true>(*this, s);
+  if (cg == 2)
+    dispatch_major<2>(*this, s);
   else
-    dispatch_epi<true, false>(*this, s);
+    dispatch_major<1>(*this, s);
 }
 
 }  // namespace gemm

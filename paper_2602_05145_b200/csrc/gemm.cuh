@@ -29,31 +29,47 @@
 namespace specsim {
 namespace gemm {
 
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+// Per-CTA-group configuration.  CG = 1: one CTA computes a 128 x 256 tile
+// (tcgen05.mma.cta_group::1, M = 128).  CG = 2: a cluster of two CTAs on one
+// TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256): each
+// CTA stages 128 rows of A and 128 of the 256 B rows, so per-SM shared-memory
+// and L2 operand traffic drop by a third.
+template <int CG>
+struct Cfg {
+  static constexpr int BN_CTA = BN / CG;                 // B rows staged per CTA
+  static constexpr int A_STAGE = BM * BK * 2;            // 16 KB
+  static constexpr int B_STAGE = BN_CTA * BK * 2;        // 32 KB (CG1) / 16 KB (CG2)
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int TILE_M = BM * CG;                 // rows per (pair) tile
+};
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
-constexpr int GROUP_M = 8;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 
 __device__ __forceinline__ void tile_coords(int tile, const Args& a, int& mb, int& nb) {
-  // Grouped rasterisation: consecutive tiles walk GROUP_M row blocks first so
-  // the concurrently resident CTAs share A rows and B columns in L2.
-  const int group_size = GROUP_M * a.num_n_blocks;
+  // Grouped rasterisation: consecutive tiles walk group_m row blocks first so
+  // the concurrently resident CTAs share B column panels in L2; group_m is
+  // chosen on the host so the A panel of a group stays L2-resident and B
+  // streams through DRAM about once.
+  const int group_size = a.group_m * a.num_n_blocks;
   const int group = tile / group_size;
-  const int first_m = group * GROUP_M;
-  const int gm = min(a.num_m_blocks - first_m, GROUP_M);
+  const int first_m = group * a.group_m;
+  const int gm = min(a.num_m_blocks - first_m, a.group_m);
   const int in_group = tile - group * group_size;
   mb = first_m + in_group % gm;
   nb = in_group / gm;
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const Args args) {
+  using C_ = Cfg<CG>;
+  constexpr int STAGES = C_::STAGES;
+  constexpr int A_STAGE_BYTES = C_::A_STAGE;
+  constexpr int B_STAGE_BYTES = C_::B_STAGE;
+  constexpr int STAGE_BYTES = C_::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -67,6 +83,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // CTA within the pair
+  const int unit = CG == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int num_units = CG == 2 ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -77,13 +96,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull_bar[s], 1);
-      ptx::mbar_init(&tempty_bar[s], 4);
+      ptx::mbar_init(&tempty_bar[s], 4 * CG);  // every epilogue warp of the group
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS, CG>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    ptx::cluster_sync();  // peer barriers initialised before any remote arrive
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -94,29 +116,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+      auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+        if constexpr (CG == 2)
+          ptx::tma_load_2d_pair(m, bar, dst, c0, c1);
+        else
+          ptx::tma_load_2d(m, bar, dst, c0, c1);
+      };
+      for (int tile = unit; tile < args.num_tiles; tile += num_units) {
         int mb, nb;
         tile_coords(tile, args, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * C_::TILE_M + static_cast<int>(rank) * BM;    // this CTA's A rows
+        const int n0 = nb * BN + static_cast<int>(rank) * C_::BN_CTA;     // this CTA's B rows
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          // the leader's barrier counts both CTAs' bytes; the peer only issues TMA
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES * CG);
           uint8_t* a_dst = smA + stage * A_STAGE_BYTES;
           uint8_t* b_dst = smB + stage * B_STAGE_BYTES;
           const int k0 = kb * BK;
           if constexpr (!A_MN) {
-            ptx::tma_load_2d(&tmA, &full_bar[stage], a_dst, k0, m0);
+            load(&tmA, &full_bar[stage], a_dst, k0, m0);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              ptx::tma_load_2d(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, k0);
+              load(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, k0);
           }
           if constexpr (!B_MN) {
-            ptx::tma_load_2d(&tmB, &full_bar[stage], b_dst, k0, n0);
+            load(&tmB, &full_bar[stage], b_dst, k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              ptx::tma_load_2d(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, k0);
+            for (int j = 0; j < C_::BN_CTA / 64; ++j)
+              load(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -127,13 +157,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < args.num_tiles; tile += num_units) {
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -152,15 +182,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                         : ptx::make_sw128_desc(a_base + k * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? ptx::make_sw128_desc(b_base + k * 2048, 8192, 1024)
                                         : ptx::make_sw128_desc(b_base + k * 32, 16, 1024);
-            ptx::umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            if constexpr (CG == 2)
+              ptx::umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            else
+              ptx::umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          ptx::umma_commit(&empty_bar[stage]);
+          if constexpr (CG == 2)
+            ptx::umma_commit_pair(&empty_bar[stage], 0x3);  // free the slot in both CTAs
+          else
+            ptx::umma_commit(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 2)
+          ptx::umma_commit_pair(&tfull_bar[acc], 0x3);
+        else
+          ptx::umma_commit(&tfull_bar[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -170,10 +209,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32)
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < args.num_tiles; tile += num_units) {
       int mb, nb;
       tile_coords(tile, args, mb, nb);
-      const int m0 = mb * BM, n0 = nb * BN;
+      const int m0 = mb * C_::TILE_M + static_cast<int>(rank) * BM, n0 = nb * BN;
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const int row = m0 + quad * 32 + lane;
@@ -316,17 +355,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          ptx::mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA waits on it
+        else
+          ptx::mbar_arrive(&tempty_bar[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    ptx::cluster_sync();  // no CTA frees TMEM / smem the peer's MMA may still touch
+  else
+    __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+    ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
   }
 }
 

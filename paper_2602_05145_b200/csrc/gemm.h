@@ -44,6 +44,7 @@ struct Args {
   CePartial* partials;     // [num_n_blocks, M] (fwd)
   int vocab_offset;        // vocabulary index of output column 0
   int num_m_blocks, num_n_blocks, num_tiles;
+  int group_m;  // rasterisation group (row blocks)
 };
 
 // A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).
@@ -59,6 +60,7 @@ struct GemmPlan {
   Args args;
   int epi = 0;
   bool a_mn = false, b_mn = false;
+  int cg = 2;  // CTAs per MMA tile (1 or 2)
   int grid = 0;
   double flops = 0;
   void launch(cudaStream_t s) const;
@@ -66,7 +68,7 @@ struct GemmPlan {
 
 // Throws std::invalid_argument on bad shapes / alignment.
 GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
-                   const Args& extra);
+                   const Args& extra, int cg = 2);
 
 }  // namespace gemm
 }  // namespace specsim

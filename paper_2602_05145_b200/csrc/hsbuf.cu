@@ -50,6 +50,9 @@ HiddenStateBuffer::HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_t
   const size_t row = static_cast<size_t>(geom_.bytes_per_token());
   SPECSIM_CUDA(cudaMalloc(&ring_feat_, row * cap_));
   SPECSIM_CUDA(cudaMalloc(&ring_ids_, sizeof(int32_t) * cap_));
+  cudaEvent_t ev;
+  SPECSIM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  ready_ = ev;
 }
 
 HiddenStateBuffer::~HiddenStateBuffer() {
@@ -59,7 +62,12 @@ HiddenStateBuffer::~HiddenStateBuffer() {
   cudaFree(ring_ids_);
   cudaFree(staging_dev_);
   cudaFreeHost(staging_host_);
+  if (ready_) cudaEventDestroy(static_cast<cudaEvent_t>(ready_));
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+void HiddenStateBuffer::sync() const {
+  SPECSIM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
 }
 
 const HiddenStateBuffer::Sample& HiddenStateBuffer::sample(int64_t id) const {
@@ -186,7 +194,8 @@ void HiddenStateBuffer::append(int64_t sample_id, double alpha, const void* cons
   if (first < n)
     SPECSIM_CUDA(cudaMemcpyAsync(ring_ids_, d_ids + first, sizeof(int32_t) * (n - first),
                                  cudaMemcpyDeviceToDevice, s));
-  SPECSIM_CUDA(cudaStreamSynchronize(s));  // staging reuse + visibility to the trainer
+  SPECSIM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ready_), s));
+  SPECSIM_CUDA(cudaStreamSynchronize(s));  // staging reuse
   head_ += n;
   samples_.at(open_id_).length += n;
   stats_.resident_tokens = head_ - tail_;
@@ -194,13 +203,24 @@ void HiddenStateBuffer::append(int64_t sample_id, double alpha, const void* cons
 }
 
 void HiddenStateBuffer::append_packed(int64_t sample_id, double alpha, const uint16_t* features,
-                                      const int32_t* token_ids, int n, bool on_device) {
+                                      const int32_t* token_ids, int n, int mode) {
+  const bool on_device = mode == 1;
+  const bool async_pinned = mode == 2;
   Problems p("hsbuf_append_packed");
   p.check(n >= 0, "n must be >= 0");
   p.check(features != nullptr || n == 0, "features is null");
   p.check(token_ids != nullptr || n == 0, "token_ids is null");
   p.check(alpha >= 0.0 && alpha <= 1.0, "alpha must be in [0,1]");
+  p.check(mode >= 0 && mode <= 2, "mode must be 0 (host), 1 (device) or 2 (pinned host, async)");
   p.throw_if_any();
+  if (async_pinned) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, features) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+        cudaPointerGetAttributes(&a, token_ids) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      throw std::invalid_argument("mode 2 needs page-locked (pinned) host buffers");
+    }
+  }
   open_sample(sample_id, alpha);
   if (n == 0) return;
   reserve(n);
@@ -221,7 +241,11 @@ void HiddenStateBuffer::append_packed(int64_t sample_id, double alpha, const uin
   if (first < n)
     SPECSIM_CUDA(cudaMemcpyAsync(ring_ids_, token_ids + first, sizeof(int32_t) * (n - first),
                                  kind, s));
-  SPECSIM_CUDA(cudaStreamSynchronize(s));
+  // consumers (trainer steps) order themselves after this event instead of a
+  // host sync; pinned-host appends return immediately so the DMA overlaps
+  // the step that is running
+  SPECSIM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ready_), s));
+  if (!async_pinned) SPECSIM_CUDA(cudaStreamSynchronize(s));
   head_ += n;
   samples_.at(open_id_).length += n;
   stats_.resident_tokens = head_ - tail_;
@@ -231,6 +255,7 @@ void HiddenStateBuffer::append_packed(int64_t sample_id, double alpha, const uin
 void HiddenStateBuffer::read_sample(int64_t id, uint16_t* features, int32_t* ids) const {
   const Sample& sm = sample(id);
   DeviceGuard dg(device_);
+  sync();  // async appends land on the buffer's own stream
   const int W = geom_.hidden_dim * geom_.layers_tapped;
   const size_t row = static_cast<size_t>(W) * 2;
   const int64_t pos = sm.start % cap_;
@@ -292,10 +317,17 @@ int specsim_hsbuf_append(specsim_hsbuf* b, int64_t sample_id, double alpha,
 
 int specsim_hsbuf_append_packed(specsim_hsbuf* b, int64_t sample_id, double alpha,
                                 const uint16_t* features, const int32_t* token_ids, int32_t n,
-                                int on_device) {
+                                int mode) {
   return guard([&] {
     if (!b) throw std::invalid_argument("null buffer");
-    b->b->append_packed(sample_id, alpha, features, token_ids, n, on_device != 0);
+    b->b->append_packed(sample_id, alpha, features, token_ids, n, mode);
+  });
+}
+
+int specsim_hsbuf_sync(specsim_hsbuf* b) {
+  return guard([&] {
+    if (!b) throw std::invalid_argument("null buffer");
+    b->b->sync();
   });
 }
 

@@ -477,6 +477,8 @@ class DraftTrainerImpl {
 
   void forward(HiddenStateBuffer& buf, const kern::BatchSpec& spec, int64_t global_valid) {
     const int S = sh.seq_len;
+    // order after every append issued on the buffer's stream (async ingest)
+    SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(buf.ready_event()), 0));
     timed(PH_INGEST, 0, [&] {
       kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
                          buf.capacity(), static_cast<int>(W3), spec, sh.micro_batch, S, F, u, y,

@@ -11,7 +11,7 @@ from _util import rand_bf16, bf16_bits_to_f32
 pytestmark = pytest.mark.gpu
 
 
-def run_gemm(a_mn, b_mn, epi, M, N, K, seed=0, iters=0):
+def run_gemm(a_mn, b_mn, epi, M, N, K, seed=0, iters=0, cg=2):
     rng = np.random.default_rng(seed)
     # logical A [M,K], B [N,K]; stored per major-ness
     A_bits, A = rand_bf16(rng, (M, K))
@@ -32,31 +32,37 @@ def run_gemm(a_mn, b_mn, epi, M, N, K, seed=0, iters=0):
         R_bits, R = rand_bf16(rng, (M, N))
         ref = ref + R.astype(np.float64)
     ms = C.c_float(0)
-    _lib.call("specsim_debug_gemm", a_mn, b_mn, epi, M, N, K, _lib.ptr(A_st), lda, _lib.ptr(B_st),
+    _lib.call("specsim_debug_gemm", a_mn, b_mn, epi | (cg << 8), M, N, K, _lib.ptr(A_st), lda, _lib.ptr(B_st),
               ldb, _lib.ptr(Cbuf), N, _lib.ptr(R_bits), N, iters, C.byref(ms))
     out = Cbuf if epi in (1, 2) else bf16_bits_to_f32(Cbuf)
     return out, ref, ms.value
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 320), (384, 768, 1024), (200, 328, 136)])
-def test_gemm_forms_f32(a_mn, b_mn, M, N, K):
-    out, ref, _ = run_gemm(a_mn, b_mn, 1, M, N, K)
+def test_gemm_forms_f32(a_mn, b_mn, M, N, K, cg):
+    out, ref, _ = run_gemm(a_mn, b_mn, 1, M, N, K, cg=cg)
     err = np.abs(out - ref).max()
     assert err <= 1e-3 * np.sqrt(K), (err, out[:2, :4], ref[:2, :4])
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("epi", [0, 2, 3])
-def test_gemm_epilogues(epi):
+def test_gemm_epilogues(epi, cg):
     M, N, K = 256, 512, 256
-    out, ref, _ = run_gemm(0, 0, epi, M, N, K, seed=3)
+    out, ref, _ = run_gemm(0, 0, epi, M, N, K, seed=3, cg=cg)
     if epi == 2:
         np.testing.assert_allclose(out, ref, atol=2e-3 * np.sqrt(K))
     else:  # bf16 output: one rounding of the fp32 result
         np.testing.assert_allclose(out, ref, rtol=1.0 / 128, atol=1e-2)
 
 
-def test_gemm_many_tiles_persistent():
-    # more tiles than SMs -> exercises the persistent loop and both TMEM stages
-    out, ref, _ = run_gemm(0, 0, 1, 2048, 4096, 256, seed=5)
+@pytest.mark.parametrize("cg", [1, 2])
+def test_gemm_many_tiles_persistent(cg):
+    # more tiles than SMs -> exercises the persistent loop, both TMEM stages and
+    # the grouped rasterisation (several row groups)
+    out, ref, _ = run_gemm(0, 0, 1, 2048, 4096, 256, seed=5, cg=cg)
     assert np.abs(out - ref).max() <= 1e-3 * 16
+    out, ref, _ = run_gemm(1, 1, 1, 4096, 512, 2048, seed=6, cg=cg)
+    assert np.abs(out - ref).max() <= 1e-3 * 46

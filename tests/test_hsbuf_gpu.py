@@ -99,3 +99,34 @@ def test_validation_errors():
     with pytest.raises(_lib.DomainError):
         buf.extract_signals(1, 0.5, [np.zeros((4, H), np.uint16)] * 3, [1, 2], accepted_idx=[0, 9])
     buf.close()
+
+
+def test_async_pinned_append_feeds_the_step():
+    """mode 2 (pinned host, asynchronous DMA) must be ordered before the step
+    that consumes it: a step on asynchronously appended samples equals a step on
+    synchronously appended copies."""
+    import torch
+    cfg = dict(api.CONFIGS["C1"], micro_batch=2)
+    buf = api.HiddenStateBuffer(api.SignalGeometry(cfg["hidden"]), 8192)
+    pins = []
+    for i in range(2):
+        cap = oracle.synth_capture(11, i, cfg["seq_len"] + 2, cfg["vocab"], cfg["hidden"])
+        buf.append_packed(i, 0.5, cap["features"], cap["ids"])  # mode 0
+        f = torch.from_numpy(cap["features"].view(np.int16)).pin_memory()
+        ids = torch.from_numpy(cap["ids"]).pin_memory()
+        pins.append((f, ids))
+        _lib.call("specsim_hsbuf_append_packed", buf.h, 10 + i, 0.5, f.data_ptr(), ids.data_ptr(),
+                  len(cap["ids"]), 2)
+    t1 = api.DraftTrainer(cfg, seed=1)
+    t2 = api.DraftTrainer(cfg, seed=1)
+    r1 = t1.step(buf, [0, 1])
+    r2 = t2.step(buf, [10, 11])
+    assert r1["loss"] == r2["loss"]
+    assert np.array_equal(t1.get_grad("fc"), t2.get_grad("fc"))
+    f, ids = buf.read_sample(11)
+    assert np.array_equal(f.view(np.int16), pins[1][0].numpy())
+    with pytest.raises(_lib.DomainError):  # pageable memory is rejected for mode 2
+        z = np.zeros((4, 3 * cfg["hidden"]), np.uint16)
+        zi = np.zeros(4, np.int32)
+        _lib.call("specsim_hsbuf_append_packed", buf.h, 99, 0.5, z.ctypes.data, zi.ctypes.data, 4, 2)
+    t1.close(); t2.close(); buf.close()
