@@ -10,7 +10,7 @@ timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_ou
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
      --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_run.txt 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 3 -c 3 \
-     -o gpurun_out/gemm_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_run.txt 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-gemm_kernel} -s ${NCU_SKIP:-3} -c ${NCU_COUNT:-3} \
+     -o gpurun_out/prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_run.txt 2>&1
 fi
 tail -3 gpurun_out/pytest_gpu.txt; cat gpurun_out/smoke.txt | tail -2; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
