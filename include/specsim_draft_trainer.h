@@ -241,8 +241,13 @@ int specsim_trainer_param_info(const specsim_trainer* t, int32_t index, const ch
                                int64_t* rows, int64_t* cols);
 int specsim_trainer_get_param(const specsim_trainer* t, const char* name, float* host_out);
 int specsim_trainer_set_param(specsim_trainer* t, const char* name, const float* host_in);
-/* Gradient of the last step (after the DP all-reduce). */
+/* Gradient of the last step (after the DP all-reduce).  On a single replica the
+ * GEMM-weight gradients are consumed by the AdamW update fused into the
+ * weight-gradient GEMM epilogue and are only materialised after
+ * specsim_trainer_keep_grads(t, 1) (an extra 4 B/param store); otherwise
+ * get_grad fails with SPECSIM_EDOMAIN for them. */
 int specsim_trainer_get_grad(const specsim_trainer* t, const char* name, float* host_out);
+int specsim_trainer_keep_grads(specsim_trainer* t, int enabled);
 int specsim_trainer_set_embedding(specsim_trainer* t, const uint16_t* host_bf16);
 int specsim_trainer_get_embedding(const specsim_trainer* t, uint16_t* host_bf16);
 int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "specsim_trainer_get_param": [P, C.c_char_p, P],
     "specsim_trainer_set_param": [P, C.c_char_p, P],
     "specsim_trainer_get_grad": [P, C.c_char_p, P],
+    "specsim_trainer_keep_grads": [P, C.c_int],
     "specsim_trainer_set_embedding": [P, P],
     "specsim_trainer_get_embedding": [P, P],
     "specsim_trainer_set_step_count": [P, I64],

@@ -288,6 +288,9 @@ class DraftTrainer:
         call("specsim_trainer_get_grad", self.h, name.encode(), ptr(a))
         return a
 
+    def keep_grads(self, on: bool = True):
+        call("specsim_trainer_keep_grads", self.h, 1 if on else 0)
+
     def set_embedding(self, e_bf16):
         a = np.ascontiguousarray(e_bf16, np.uint16)
         call("specsim_trainer_set_embedding", self.h, ptr(a))

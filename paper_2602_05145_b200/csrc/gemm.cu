@@ -69,6 +69,7 @@ template <bool A_MN, bool B_MN, int EPI, int CG>
 void launch_t(const GemmPlan& p, cudaStream_t s) {
   auto k = gemm_kernel<A_MN, B_MN, EPI, CG>;
   constexpr int smem = Cfg<CG>::SMEM;
+  static_assert(smem <= 232448, "shared memory budget");
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     SPECSIM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -103,6 +104,7 @@ void dispatch_epi(const GemmPlan& p, cudaStream_t s) {
     case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID, CG>(p, s); break;
     case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD, CG>(p, s); break;
     case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s); break;
+    case EPI_ADAMW: launch_t<A_MN, B_MN, EPI_ADAMW, CG>(p, s); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
 }
@@ -124,6 +126,7 @@ void dispatch_major(const GemmPlan& p, cudaStream_t s) {
 GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
                    const Args& extra, int cg) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: empty shape");
+  if (N % 4 != 0) throw std::invalid_argument("gemm: N must be a multiple of 4");
   if (cg != 1 && cg != 2) throw std::invalid_argument("gemm: cg must be 1 or 2");
   GemmPlan p;
   p.a_mn = A.mn_major;
@@ -153,6 +156,11 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   const int units = num_sms() / cg;  // CTA pairs (or CTAs) resident at once
   p.grid = (p.args.num_tiles < units ? p.args.num_tiles : units) * cg;
   p.flops = 2.0 * M * static_cast<double>(N) * K;
+  if (epi == EPI_ADAMW) {
+    if (!p.args.opt_p || !p.args.opt_m || !p.args.opt_v || !p.args.opt_p16 || !p.args.opt_hp)
+      throw std::invalid_argument("gemm: AdamW epilogue needs p/m/v/p16/hp");
+    if ((p.args.ldc * 4) % 16 != 0) throw std::invalid_argument("gemm: ldc not 16B aligned");
+  }
   if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
       epi == EPI_F32_ACC) {
     if (!p.args.C) throw std::invalid_argument("gemm: missing output");

@@ -41,7 +41,8 @@ struct Cfg {
   static constexpr int B_STAGE = BN_CTA * BK * 2;        // 32 KB (CG1) / 16 KB (CG2)
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int EPI_STAGE = 4 * 32 * 36 * 4;     // per-warp 32x32 fp32 (+pad) staging
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + EPI_STAGE;
   static constexpr int TILE_M = BM * CG;                 // rows per (pair) tile
 };
 constexpr int NUM_THREADS = 192;
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -206,7 +208,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // TMEM gives one accumulator row per thread (32x32b loads).  Row-wise
+    // reductions (CE forward) consume it directly; every other epilogue stages
+    // each 32x32 chunk through shared memory (row stride 36 floats: conflict-
+    // free float4 writes and reads) and then walks it row-contiguously, 4 rows
+    // x 8 lanes x float4 per warp instruction, so global loads / stores are
+    // coalesced 128-byte row segments.
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32)
+    float* stg = epi_stage + quad * (32 * 36);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < args.num_tiles; tile += num_units) {
@@ -215,107 +224,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m0 = mb * C_::TILE_M + static_cast<int>(rank) * BM, n0 = nb * BN;
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = m0 + quad * 32 + lane;
+      const int row_base = m0 + quad * 32;
+      const int row = row_base + lane;  // the row this thread owns in TMEM
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
 
-      // per-row state for the cross-entropy epilogues
-      float run_max = -INFINITY, run_sum = 0.f, tgt_logit = -INFINITY;
-      int run_arg = 0;
-      int tgt = -1;
-      float lse_r = 0.f, coef_r = 0.f;
-      if constexpr (EPI == EPI_CE_FWD || EPI == EPI_CE_BWD) {
-        if (row_ok) tgt = args.targets[row] - args.vocab_offset;
-      }
-      if constexpr (EPI == EPI_CE_BWD) {
-        if (row_ok) {
-          lse_r = args.lse[row];
-          coef_r = args.coef[row];
-        }
-      }
-
+      if constexpr (EPI == EPI_CE_FWD) {
+        float run_max = -INFINITY, run_sum = 0.f, tgt_logit = -INFINITY;
+        int run_arg = 0;
+        const int tgt = row_ok ? args.targets[row] - args.vocab_offset : -1;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after masked lanes
-        ptx::tmem_ld_32x32b_x32(t_row + c, r);
-        ptx::tmem_ld_wait();
-        const int col0 = n0 + c;
-        if (!row_ok || col0 >= args.N) continue;
-        const bool full_chunk = col0 + 32 <= args.N;
-        const int ncol = full_chunk ? 32 : args.N - col0;
-        if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if constexpr (EPI == EPI_BF16_RESID) {
-            const __nv_bfloat16* rp = args.R + static_cast<long long>(row) * args.ldr + col0;
-            if (full_chunk) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 8) {
-                uint4 q = *reinterpret_cast<const uint4*>(rp + i);
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  float2 f = __bfloat1622float2(h[j]);
-                  v[i + 2 * j] += f.x;
-                  v[i + 2 * j + 1] += f.y;
-                }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < ncol) v[i] += __bfloat162float(rp[i]);
-            }
-          }
-          if constexpr (EPI == EPI_CE_BWD) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float p = exp2f((v[i] - lse_r) * 1.4426950408889634f);
-              v[i] = (p - ((c + i) == tgt - n0 ? 1.f : 0.f)) * coef_r;
-            }
-          }
-          __nv_bfloat16* cp =
-              static_cast<__nv_bfloat16*>(args.C) + static_cast<long long>(row) * args.ldc + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 8)
-              ptx::st_global_v4(cp + i, ptx::pack_bf16x2(v[i], v[i + 1]),
-                                ptx::pack_bf16x2(v[i + 2], v[i + 3]),
-                                ptx::pack_bf16x2(v[i + 4], v[i + 5]),
-                                ptx::pack_bf16x2(v[i + 6], v[i + 7]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < ncol) cp[i] = __float2bfloat16_rn(v[i]);
-          }
-        } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
-          float* cp = static_cast<float*>(args.C) + static_cast<long long>(row) * args.ldc + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 o = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                                     __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-              if constexpr (EPI == EPI_F32_ACC) {
-                const float4 prev = *reinterpret_cast<const float4*>(cp + i);
-                o.x += prev.x;
-                o.y += prev.y;
-                o.z += prev.z;
-                o.w += prev.w;
-              }
-              *reinterpret_cast<float4*>(cp + i) = o;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < ncol) {
-                float o = __uint_as_float(r[i]);
-                if constexpr (EPI == EPI_F32_ACC) o += cp[i];
-                cp[i] = o;
-              }
-            }
-          }
-        } else if constexpr (EPI == EPI_CE_FWD) {
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(t_row + c, r);
+          ptx::tmem_ld_wait();
+          const int col0 = n0 + c;
+          if (!row_ok || col0 >= args.N) continue;
+          const int ncol = min(32, args.N - col0);
           float cmax = -INFINITY;
           int carg = 0;
 #pragma unroll
@@ -342,8 +268,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (i == t_local) tgt_logit = __uint_as_float(r[i]);
           }
         }
-      }
-      if constexpr (EPI == EPI_CE_FWD) {
         if (row_ok) {
           CePartial p;
           p.max = run_max;
@@ -351,6 +275,130 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           p.target = tgt_logit;
           p.argmax = run_arg + args.vocab_offset;
           args.partials[static_cast<long long>(nb) * args.M + row] = p;
+        }
+      } else {
+        // per-row constants, owned by lane (row - row_base); shuffled below
+        float lse_r = 0.f, coef_r = 0.f;
+        int tgt_r = -1;
+        if constexpr (EPI == EPI_CE_BWD) {
+          if (row_ok) {
+            lse_r = args.lse[row];
+            coef_r = args.coef[row];
+            tgt_r = args.targets[row] - args.vocab_offset;
+          }
+        }
+        AdamDev hp{};
+        if constexpr (EPI == EPI_ADAMW) hp = *args.opt_hp;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(t_row + c, r);
+          ptx::tmem_ld_wait();
+          const int col0 = n0 + c;
+          if (col0 >= args.N) continue;  // warp-uniform
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(stg + lane * 36 + i) =
+                make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                            __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          __syncwarp();
+          const int cl = (lane & 7) * 4;  // this lane's 4 columns
+          const int col = col0 + cl;
+          const bool col_ok = col < args.N;  // N % 4 == 0: all 4 valid
+          // phase 1: every global load of the chunk is issued before any store
+          // (loads and stores may alias as far as the compiler knows), so the
+          // 8 row groups' DRAM latencies overlap
+          float4 v[8], x1[8], x2[8], x3[8];
+          bool ok[8];
+          long long e[8];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + (lane >> 3);
+            const int rr = row_base + rl;
+            ok[it] = col_ok && rr < args.M;
+            e[it] = static_cast<long long>(rr) * args.ldc + col;
+            v[it] = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
+            if constexpr (EPI == EPI_BF16_RESID) {
+              if (ok[it]) {
+                const uint2 q = *reinterpret_cast<const uint2*>(
+                    args.R + static_cast<long long>(rr) * args.ldr + col);
+                x1[it].x = __uint_as_float(q.x);
+                x1[it].y = __uint_as_float(q.y);
+              }
+            } else if constexpr (EPI == EPI_F32_ACC) {
+              if (ok[it])
+                x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e[it]);
+            } else if constexpr (EPI == EPI_ADAMW) {
+              if (ok[it]) {
+                x1[it] = *reinterpret_cast<const float4*>(args.opt_p + e[it]);
+                x2[it] = *reinterpret_cast<const float4*>(args.opt_m + e[it]);
+                x3[it] = *reinterpret_cast<const float4*>(args.opt_v + e[it]);
+              }
+            } else if constexpr (EPI == EPI_CE_BWD) {
+              // row constants: x1 = {lse, coef, target (bits)}
+              x1[it].x = __shfl_sync(0xffffffffu, lse_r, rl);
+              x1[it].y = __shfl_sync(0xffffffffu, coef_r, rl);
+              x1[it].z = __int_as_float(__shfl_sync(0xffffffffu, tgt_r, rl));
+            }
+          }
+          // phase 2: compute and store
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            if (!ok[it]) continue;
+            float4 w = v[it];
+            float* wa = &w.x;
+            if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
+              if constexpr (EPI == EPI_BF16_RESID) {
+                uint32_t q0 = __float_as_uint(x1[it].x), q1 = __float_as_uint(x1[it].y);
+                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q0));
+                const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q1));
+                w.x += a.x;
+                w.y += a.y;
+                w.z += b.x;
+                w.w += b.y;
+              }
+              if constexpr (EPI == EPI_CE_BWD) {
+                const float lse_x = x1[it].x, coef_x = x1[it].y;
+                const int tgt_x = __float_as_int(x1[it].z);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float p = exp2f((wa[j] - lse_x) * 1.4426950408889634f);
+                  wa[j] = (p - ((c + cl + j) == tgt_x - n0 ? 1.f : 0.f)) * coef_x;
+                }
+              }
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(args.C) + e[it]) =
+                  make_uint2(ptx::pack_bf16x2(w.x, w.y), ptx::pack_bf16x2(w.z, w.w));
+            } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+              if constexpr (EPI == EPI_F32_ACC) {
+                w.x += x1[it].x;
+                w.y += x1[it].y;
+                w.z += x1[it].z;
+                w.w += x1[it].w;
+              }
+              *reinterpret_cast<float4*>(static_cast<float*>(args.C) + e[it]) = w;
+            } else if constexpr (EPI == EPI_ADAMW) {
+              float4 p = x1[it], m = x2[it], s2 = x3[it];
+              float* pa = &p.x;
+              float* ma = &m.x;
+              float* sa = &s2.x;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float g = wa[j];
+                const float pi = pa[j] * hp.decay;
+                ma[j] = ma[j] + (g - ma[j]) * (1.f - hp.beta1);
+                sa[j] = sa[j] * hp.beta2 + (1.f - hp.beta2) * g * g;
+                const float denom = sqrtf(sa[j]) / hp.bc2_sqrt + hp.eps;
+                pa[j] = pi - hp.step_size * (ma[j] / denom);
+              }
+              *reinterpret_cast<float4*>(args.opt_p + e[it]) = p;
+              *reinterpret_cast<float4*>(args.opt_m + e[it]) = m;
+              *reinterpret_cast<float4*>(args.opt_v + e[it]) = s2;
+              *reinterpret_cast<uint2*>(args.opt_p16 + e[it]) =
+                  make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w));
+              if (args.opt_g) *reinterpret_cast<float4*>(args.opt_g + e[it]) = w;
+            }
+          }
         }
       }
       ptx::tc_fence_before();

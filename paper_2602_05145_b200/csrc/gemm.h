@@ -21,6 +21,14 @@ enum Epi : int {
   EPI_BF16_RESID = 3,  // C(bf16) = acc + R(bf16)
   EPI_CE_FWD = 4,      // per-row partial (max, sum exp, target logit, argmax) per N tile
   EPI_CE_BWD = 5,      // C(bf16) = (exp(acc - lse[row]) - [col == y[row]]) * coef[row]
+  EPI_ADAMW = 6,       // acc is a weight gradient: fused PyTorch-AdamW update of p/m/v (+ bf16 p)
+};
+
+// Device-resident AdamW hyper-parameters of the current step (updated per step
+// by a tiny copy so GEMM plans stay fixed).
+struct AdamDev {
+  float lr, beta1, beta2, eps, decay /* 1 - lr*wd */, step_size /* lr / bc1 */, bc2_sqrt;
+  float pad;
 };
 
 // Per-(row, N-tile) partial softmax statistics written by EPI_CE_FWD.
@@ -45,6 +53,11 @@ struct Args {
   int vocab_offset;        // vocabulary index of output column 0
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;  // rasterisation group (row blocks)
+  // fused AdamW epilogue: parameter tensors laid out like C (ldc)
+  float *opt_p, *opt_m, *opt_v;
+  __nv_bfloat16* opt_p16;
+  float* opt_g;  // optional gradient store (nullable)
+  const AdamDev* opt_hp;
 };
 
 // A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).

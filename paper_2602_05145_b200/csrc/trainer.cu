@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -118,6 +119,11 @@ class DraftTrainerImpl {
 
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  bool use_nccl = false;              // world > 1, or SPECSIM_FORCE_NCCL=1 (1-rank comm, tests)
+  cudaStream_t comm_stream = nullptr;  // gradient buckets all-reduced behind the backward
+  std::vector<cudaEvent_t> bucket_events;
+  size_t bucket_next = 0;
+  cudaEvent_t ev_comm_done = nullptr;
   Arena arena;
 
   // parameters / optimiser state (flat, registry order)
@@ -138,11 +144,18 @@ class DraftTrainerImpl {
   // pinned host scalars
   long long* h_nglobal = nullptr;
   double* h_stats = nullptr;
+  gemm::AdamDev* adam_dev = nullptr;  // this step's AdamW constants (device)
+  gemm::AdamDev* h_adam = nullptr;    // pinned staging
+  bool keep_grads = false;            // materialise fp32 grads in the fused-AdamW path
 
   // GEMM plans
   gemm::GemmPlan p_fc, p_qkv, p_o, p_gu, p_down, p_ce_fwd;
   std::vector<gemm::GemmPlan> p_ce_bwd, p_lm_dx, p_lm_dw;
   gemm::GemmPlan p_dact, p_dw_down, p_dz, p_dw_gu, p_dO, p_dw_o, p_dU, p_dw_qkv, p_dw_fc;
+  // weight-gradient GEMMs with the AdamW update fused into the epilogue
+  // (single-replica path: no all-reduce between gradient and update)
+  std::vector<gemm::GemmPlan> f_lm_dw;
+  gemm::GemmPlan f_dw_down, f_dw_gu, f_dw_o, f_dw_qkv, f_dw_fc;
 
   // timing
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
@@ -261,7 +274,9 @@ class DraftTrainerImpl {
     arena.reserve(&dU, T * 2 * H);
     arena.reserve(&Dattn, T * sh.n_heads);
     arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(T) * H);
+    arena.reserve(&adam_dev, 1);
     arena.commit();
+    SPECSIM_CUDA(cudaMallocHost(&h_adam, sizeof(gemm::AdamDev)));
     SPECSIM_CUDA(cudaMallocHost(&h_nglobal, sizeof(long long)));
     SPECSIM_CUDA(cudaMallocHost(&h_stats, 4 * sizeof(double)));
     SPECSIM_CUDA(cudaMemsetAsync(Mst, 0, sizeof(float) * total, stream));
@@ -275,10 +290,17 @@ class DraftTrainerImpl {
     SPECSIM_CUDA(cudaEventCreate(&ev_end));
     SPECSIM_CUDA(cudaEventCreate(&ev_region[0]));
     SPECSIM_CUDA(cudaEventCreate(&ev_region[1]));
-    if (world > 1) {
+    const char* force = std::getenv("SPECSIM_FORCE_NCCL");
+    use_nccl = world > 1 || (force && force[0] == '1');
+    if (use_nccl) {
       ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
+      if (world > 1)
+        std::memcpy(&id, nccl_id, sizeof(id));
+      else
+        SPECSIM_NCCL(nccl::api().GetUniqueId(&id));
       SPECSIM_NCCL(nccl::api().CommInitRank(&comm, world, id, rank));
+      SPECSIM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+      SPECSIM_CUDA(cudaEventCreateWithFlags(&ev_comm_done, cudaEventDisableTiming));
     }
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
   }
@@ -286,7 +308,11 @@ class DraftTrainerImpl {
   ~DraftTrainerImpl() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (comm_stream) cudaStreamSynchronize(comm_stream);
     if (comm) nccl::api().CommDestroy(comm);
+    for (auto e : bucket_events) cudaEventDestroy(e);
+    if (ev_comm_done) cudaEventDestroy(ev_comm_done);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
@@ -294,6 +320,7 @@ class DraftTrainerImpl {
       if (e) cudaEventDestroy(e);
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
+    if (h_adam) cudaFreeHost(h_adam);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -429,6 +456,37 @@ class DraftTrainerImpl {
     // fc (no dF: captured features are inputs)
     p_dw_fc = make_plan({dg_b, H, true}, {F, W3, true}, H, W3, T, EPI_F32,
                         out_args(gf("fc"), W3));
+    // fused-AdamW twins of every weight-gradient GEMM
+    auto fused = [&](const GemmPlan& src, const char* name, long long row0) {
+      GemmPlan f = src;
+      const long long off = param(name).off + row0 * param(name).cols;
+      f.epi = EPI_ADAMW;
+      f.args.opt_p = P + off;
+      f.args.opt_m = Mst + off;
+      f.args.opt_v = Vst + off;
+      f.args.opt_p16 = P16 + off;
+      f.args.opt_g = G + off;  // cleared per launch unless keep_grads
+      f.args.opt_hp = adam_dev;
+      return f;
+    };
+    for (int c = 0; c < n_chunks; ++c) f_lm_dw.push_back(fused(p_lm_dw[c], "lm_head", c * Vc));
+    f_dw_down = fused(p_dw_down, "down", 0);
+    f_dw_gu = fused(p_dw_gu, "gate_up", 0);
+    f_dw_o = fused(p_dw_o, "o", 0);
+    f_dw_qkv = fused(p_dw_qkv, "qkv", 0);
+    f_dw_fc = fused(p_dw_fc, "fc", 0);
+  }
+
+  // weight-gradient GEMM: fused AdamW on a single replica, plain fp32 grads
+  // (then bucketed all-reduce) when data-parallel
+  void run_dw(const gemm::GemmPlan& plain, const gemm::GemmPlan& fusedp, int phase = PH_GEMM) {
+    if (use_nccl) {
+      run(plain, phase);
+      return;
+    }
+    gemm::GemmPlan f = fusedp;
+    if (!keep_grads) f.args.opt_g = nullptr;
+    run(f, phase, plain.flops);
   }
 
   // ------------------------------------------------------------ timing
@@ -491,7 +549,7 @@ class DraftTrainerImpl {
         kern::mask_count(m, T, n_global, stream);
       }
     });
-    if (global_valid <= 0 && world > 1)
+    if (global_valid <= 0 && use_nccl)
       timed(PH_COMM, 0, [&] {
         SPECSIM_NCCL(nccl::api().AllReduce(n_global, n_global, 1, ncclInt64, ncclSum, comm, stream));
       });
@@ -541,28 +599,55 @@ class DraftTrainerImpl {
     return d;
   }
 
+  // Data-parallel exchange: a contiguous range of the flat gradient vector is
+  // final -> all-reduce it on the comm stream while the backward continues.
+  void bucket_ready(const char* first, const char* last, long long elems_override = -1,
+                    long long off_override = -1) {
+    if (!use_nccl) return;
+    const long long off = off_override >= 0 ? off_override : param(first).off;
+    const long long end = param(last).off + param(last).rows * param(last).cols;
+    const long long n = elems_override >= 0 ? elems_override : end - off;
+    if (bucket_next == bucket_events.size()) {
+      cudaEvent_t e;
+      SPECSIM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      bucket_events.push_back(e);
+    }
+    cudaEvent_t e = bucket_events[bucket_next++];
+    SPECSIM_CUDA(cudaEventRecord(e, stream));
+    SPECSIM_CUDA(cudaStreamWaitEvent(comm_stream, e, 0));
+    SPECSIM_NCCL(nccl::api().AllReduce(G + off, G + off, static_cast<size_t>(n), ncclFloat, ncclSum,
+                                       comm, comm_stream));
+  }
+
   void backward() {
     const int S = sh.seq_len;
+    bucket_next = 0;
     for (int c = 0; c < n_chunks; ++c) {
       run(p_ce_bwd[c], PH_LM, 0.0);  // logit recompute: not algorithmic work
       run(p_lm_dx[c], PH_LM);
-      run(p_lm_dw[c], PH_LM);
+      run_dw(p_lm_dw[c], f_lm_dw[c], PH_LM);
+      // LM-head rows of this chunk are final: their all-reduce overlaps the rest
+      const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
+      bucket_ready("lm_head", "lm_head", vn * H, param("lm_head").off + v0 * H);
     }
     timed(PH_ELEM, 0, [&] {
       kern::rmsnorm_bwd(dn, H, h, H, nullptr, pf("w_fin"), rstd_fin, nullptr, dh, dh_b, H,
                         gf("w_fin"), dw_part, T, sh.hidden, stream);
     });
     run(p_dact);
-    run(p_dw_down);
+    run_dw(p_dw_down, f_dw_down);
+    bucket_ready("down", "w_fin");
     timed(PH_ELEM, 0, [&] { kern::swiglu_bwd(gu, dact, dgu, T, sh.ffn, stream); });
     run(p_dz);
-    run(p_dw_gu);
+    run_dw(p_dw_gu, f_dw_gu);
+    bucket_ready("gate_up", "gate_up");
     timed(PH_ELEM, 0, [&] {
       kern::rmsnorm_bwd(dz, H, r, H, nullptr, pf("w_post"), rstd_post, dh, dr, dr_b, H,
                         gf("w_post"), dw_part, T, sh.hidden, stream);
     });
     run(p_dO);
-    run(p_dw_o);
+    run_dw(p_dw_o, f_dw_o);
+    bucket_ready("o", "w_post");
     const attn::Dims ad = attn_dims();
     timed(PH_ATTN, 4.0 * Q * (S + 1) * T, [&] {
       attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
@@ -572,7 +657,8 @@ class DraftTrainerImpl {
                  sin_t, true, stream);
     });
     run(p_dU);
-    run(p_dw_qkv);
+    run_dw(p_dw_qkv, f_dw_qkv);
+    bucket_ready("qkv", "qkv");
     timed(PH_ELEM, 0, [&] {
       // w_in: embedding is frozen, only the weight gradient is needed
       kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
@@ -581,13 +667,21 @@ class DraftTrainerImpl {
       kern::rmsnorm_bwd(dU + H, 2 * H, g, H, nullptr, pf("w_hid"), rstd_b, dr, nullptr, dg_b, H,
                         gf("w_hid"), dw_part, T, sh.hidden, stream);
     });
-    run(p_dw_fc);
+    run_dw(p_dw_fc, f_dw_fc);
+    bucket_ready("fc", "w_hid");
+    if (use_nccl) {
+      // join: AdamW waits for every bucket
+      timed(PH_COMM, 0, [&] {
+        SPECSIM_CUDA(cudaEventRecord(ev_comm_done, comm_stream));
+        SPECSIM_CUDA(cudaStreamWaitEvent(stream, ev_comm_done, 0));
+      });
+    }
   }
 
-  void optimizer_update() {
-    step_count += 1;
-    const double bc1 = 1.0 - std::pow(static_cast<double>(opt.beta1), static_cast<double>(step_count));
-    const double bc2 = 1.0 - std::pow(static_cast<double>(opt.beta2), static_cast<double>(step_count));
+  kern::AdamHyper next_hyper() const {
+    const int64_t k = step_count + 1;
+    const double bc1 = 1.0 - std::pow(static_cast<double>(opt.beta1), static_cast<double>(k));
+    const double bc2 = 1.0 - std::pow(static_cast<double>(opt.beta2), static_cast<double>(k));
     kern::AdamHyper hp;
     hp.lr = opt.lr;
     hp.beta1 = opt.beta1;
@@ -596,7 +690,34 @@ class DraftTrainerImpl {
     hp.decay = 1.0f - opt.lr * opt.weight_decay;
     hp.step_size = static_cast<float>(opt.lr / bc1);
     hp.bc2_sqrt = static_cast<float>(std::sqrt(bc2));
-    timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, hp, stream); });
+    return hp;
+  }
+
+  // before the backward: this step's AdamW constants for the fused epilogues
+  void stage_hyper() {
+    const kern::AdamHyper hp = next_hyper();
+    *h_adam = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
+                            hp.bc2_sqrt, 0.f};
+    SPECSIM_CUDA(cudaMemcpyAsync(adam_dev, h_adam, sizeof(gemm::AdamDev), cudaMemcpyHostToDevice,
+                                 stream));
+  }
+
+  void optimizer_update() {
+    const kern::AdamHyper hp = next_hyper();
+    step_count += 1;
+    if (use_nccl) {
+      timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, hp, stream); });
+      return;
+    }
+    // GEMM weights were updated in their dW epilogues; the norm weights remain
+    timed(PH_ADAM, 0, [&] {
+      const auto& a = param("w_in");   // w_in, w_hid contiguous
+      const auto& b = param("w_post");
+      const auto& c = param("w_fin");
+      kern::adamw(2 * H, P + a.off, Mst + a.off, Vst + a.off, G + a.off, P16 + a.off, hp, stream);
+      kern::adamw(H, P + b.off, Mst + b.off, Vst + b.off, G + b.off, P16 + b.off, hp, stream);
+      kern::adamw(H, P + c.off, Mst + c.off, Vst + c.off, G + c.off, P16 + c.off, hp, stream);
+    });
   }
 
   void begin_step() {
@@ -632,7 +753,7 @@ class DraftTrainerImpl {
   }
 
   void allreduce_stats() {
-    if (world == 1) return;
+    if (!use_nccl) return;
     // loss is already normalised by the global count: sum over ranks
     timed(PH_COMM, 0, [&] {
       SPECSIM_NCCL(nccl::api().AllReduce(stats, stats, 3, ncclDouble, ncclSum, comm, stream));
@@ -644,12 +765,8 @@ class DraftTrainerImpl {
     const kern::BatchSpec spec = batch_spec(buf, ids, n);
     begin_step();
     forward(buf, spec, global_valid);
-    backward();
-    if (world > 1)
-      timed(PH_COMM, 0, [&] {
-        SPECSIM_NCCL(nccl::api().AllReduce(G, G, static_cast<size_t>(total), ncclFloat, ncclSum, comm,
-                                   stream));
-      });
+    stage_hyper();
+    backward();  // includes the bucketed gradient all-reduce when data-parallel
     optimizer_update();
     allreduce_stats();
     return end_step();
@@ -890,6 +1007,10 @@ int specsim_trainer_get_grad(const specsim_trainer* t, const char* name, float* 
   return guard([&] {
     auto& im = impl_of(t);
     const auto& p = im.param(name ? name : "");
+    if (!im.use_nccl && !im.keep_grads && !p.norm)
+      throw std::invalid_argument(
+          "gradients of GEMM weights are consumed by the fused AdamW epilogue; enable "
+          "specsim_trainer_keep_grads before the step to materialise them");
     DeviceGuard dg(im.device);
     SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
     SPECSIM_CUDA(cudaMemcpy(host_out, im.G + p.off, sizeof(float) * p.rows * p.cols,
@@ -934,6 +1055,10 @@ int specsim_trainer_region(specsim_trainer* t, int end, double* ms) {
       if (ms) *ms = v;
     }
   });
+}
+
+int specsim_trainer_keep_grads(specsim_trainer* t, int enabled) {
+  return guard([&] { impl_of(t).keep_grads = enabled != 0; });
 }
 
 int specsim_trainer_set_timing(specsim_trainer* t, int enabled) {

@@ -119,6 +119,8 @@ def test_async_pinned_append_feeds_the_step():
                   len(cap["ids"]), 2)
     t1 = api.DraftTrainer(cfg, seed=1)
     t2 = api.DraftTrainer(cfg, seed=1)
+    t1.keep_grads(True)
+    t2.keep_grads(True)
     r1 = t1.step(buf, [0, 1])
     r2 = t2.step(buf, [10, 11])
     assert r1["loss"] == r2["loss"]
