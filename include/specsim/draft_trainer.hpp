@@ -69,6 +69,7 @@ class HiddenStateBuffer {
     int64_t start = 0;  // ring row of token 0
     int32_t length = 0;
     double alpha = 0;
+    int64_t last_seq = 0;  // append sequence number of the sample's last records
   };
 
   HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_tokens, int64_t flush_threshold,
@@ -97,19 +98,26 @@ class HiddenStateBuffer {
   const void* ring_features() const { return ring_feat_; }
   const int32_t* ring_ids() const { return ring_ids_; }
   int device() const { return device_; }
+  uint64_t serial() const { return serial_; }  // unique per buffer in the process
   void* stream() const { return stream_; }
-  void* ready_event() const { return ready_; }
+  // Event recorded after append number `seq` (or a later one, when the event
+  // ring has wrapped — waiting on it is then conservative but still correct).
+  void* event_for(int64_t seq) const;
 
  private:
   void open_sample(int64_t sample_id, double alpha);
   void reserve(int n);  // evict oldest samples so n more tokens fit
   void account(int n);  // extract_signals byte accounting
+  void record_append(void* stream);  // event + sequence number of this append
 
   SignalGeometry geom_;
+  uint64_t serial_ = 0;
   int64_t cap_, flush_threshold_;
   int device_;
   void* stream_ = nullptr;
-  void* ready_ = nullptr;  // cudaEvent_t recorded after the latest append
+  static constexpr int kEventRing = 256;
+  std::vector<void*> events_;  // cudaEvent_t ring, one record per append
+  int64_t append_seq_ = 0;
   void* ring_feat_ = nullptr;
   int32_t* ring_ids_ = nullptr;
   void* staging_dev_ = nullptr;   // device staging for host appends

@@ -546,14 +546,31 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
 }
 
 template <int HD>
+constexpr int fwd_smem() {
+  return (64 + 4 * 64) * HD * 2;
+}
+template <int HD>
+constexpr int bwd_kv_smem() {
+  return (2 * 64 + 4 * 32) * HD * 2 + 4 * 32 * 4;
+}
+template <int HD>
+constexpr int bwd_q_smem() {
+  return (2 * 64 + 4 * 64) * HD * 2;
+}
+
+template <int HD>
+void prepare_t() {
+  SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<HD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<HD>()));
+  SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel<HD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_kv_smem<HD>()));
+  SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_q_smem<HD>()));
+}
+
+template <int HD>
 void fwd_t(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, cudaStream_t s) {
-  const int smem = (64 + 4 * 64) * HD * 2;
-  static bool init = false;
-  if (!init) {
-    SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<HD>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    init = true;
-  }
+  const int smem = fwd_smem<HD>();
   dim3 grid(d.S / 64, d.nh, d.B);
   count_launches();
   attn_fwd_kernel<HD><<<grid, 128, smem, s>>>(qkv, o, lse, d);
@@ -567,16 +584,8 @@ void bwd_t(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16
   count_launches();
   attn_bwd_dot_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(dout, o,
                                                                                       Dbuf, d, HD);
-  const int smem_kv = (2 * 64 + 4 * 32) * HD * 2 + 4 * 32 * 4;
-  const int smem_q = (2 * 64 + 4 * 64) * HD * 2;
-  static bool init = false;
-  if (!init) {
-    SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel<HD>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
-    SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
-    init = true;
-  }
+  const int smem_kv = bwd_kv_smem<HD>();
+  const int smem_q = bwd_q_smem<HD>();
   count_launches();
   attn_bwd_dkdv_kernel<HD><<<dim3(d.S / 64, d.nkv, d.B), 128, smem_kv, s>>>(qkv, dout, lse, Dbuf,
                                                                            dqkv, d);
@@ -593,6 +602,13 @@ void check_dims(const Dims& d, int hd) {
   p.check(d.S % 64 == 0, "seq_len must be a multiple of 64");
   p.check(d.nkv > 0 && d.nh % d.nkv == 0, "n_heads must be a multiple of n_kv_heads");
   p.throw_if_any();
+}
+
+void prepare(int hd) {
+  if (hd == 128)
+    prepare_t<128>();
+  else
+    prepare_t<64>();
 }
 
 void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,

@@ -15,6 +15,7 @@ struct Dims {
 };
 
 void check_dims(const Dims& d, int hd);  // throws std::invalid_argument
+void prepare(int hd);                    // one-time kernel attributes
 void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,
              cudaStream_t s);
 // Dbuf: [nh, T] fp32 scratch.  Writes every element of dqkv.

@@ -98,6 +98,7 @@ extern "C" int specsim_debug_attention(int32_t B, int32_t S, int32_t nh, int32_t
     d.NQ = d.Q + 2 * d.KV;
     d.scale = 1.0f / std::sqrt(static_cast<float>(hd));
     attn::check_dims(d, hd);
+    attn::prepare(hd);
     if (!qkv || !o || !lse) throw std::invalid_argument("null argument");
     const size_t T = static_cast<size_t>(B) * S;
     DevBuf dq(T * d.NQ * 2), dO(T * d.Q * 2), dl(T * nh * 4), ddo(T * d.Q * 2),

@@ -66,15 +66,16 @@ int num_sms() {
 }
 
 template <bool A_MN, bool B_MN, int EPI, int CG>
-void launch_t(const GemmPlan& p, cudaStream_t s) {
+void launch_t(const GemmPlan& p, cudaStream_t s, bool attr_only = false) {
   auto k = gemm_kernel<A_MN, B_MN, EPI, CG>;
   constexpr int smem = Cfg<CG>::SMEM;
   static_assert(smem <= 232448, "shared memory budget");
-  static bool attr_set = false;  // per instantiation
+  static bool attr_set = false;  // per instantiation; set at plan time (never mid-capture)
   if (!attr_set) {
     SPECSIM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
+  if (attr_only) return;
   count_launches();
   if constexpr (CG == 1) {
     k<<<p.grid, NUM_THREADS, smem, s>>>(p.map_a, p.map_b, p.args);
@@ -96,29 +97,29 @@ void launch_t(const GemmPlan& p, cudaStream_t s) {
 }
 
 template <bool A_MN, bool B_MN, int CG>
-void dispatch_epi(const GemmPlan& p, cudaStream_t s) {
+void dispatch_epi(const GemmPlan& p, cudaStream_t s, bool a = false) {
   switch (p.epi) {
-    case EPI_BF16: launch_t<A_MN, B_MN, EPI_BF16, CG>(p, s); break;
-    case EPI_F32: launch_t<A_MN, B_MN, EPI_F32, CG>(p, s); break;
-    case EPI_F32_ACC: launch_t<A_MN, B_MN, EPI_F32_ACC, CG>(p, s); break;
-    case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID, CG>(p, s); break;
-    case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD, CG>(p, s); break;
-    case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s); break;
-    case EPI_ADAMW: launch_t<A_MN, B_MN, EPI_ADAMW, CG>(p, s); break;
+    case EPI_BF16: launch_t<A_MN, B_MN, EPI_BF16, CG>(p, s, a); break;
+    case EPI_F32: launch_t<A_MN, B_MN, EPI_F32, CG>(p, s, a); break;
+    case EPI_F32_ACC: launch_t<A_MN, B_MN, EPI_F32_ACC, CG>(p, s, a); break;
+    case EPI_BF16_RESID: launch_t<A_MN, B_MN, EPI_BF16_RESID, CG>(p, s, a); break;
+    case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD, CG>(p, s, a); break;
+    case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s, a); break;
+    case EPI_ADAMW: launch_t<A_MN, B_MN, EPI_ADAMW, CG>(p, s, a); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
 }
 
 template <int CG>
-void dispatch_major(const GemmPlan& p, cudaStream_t s) {
+void dispatch_major(const GemmPlan& p, cudaStream_t s, bool a = false) {
   if (!p.a_mn && !p.b_mn)
-    dispatch_epi<false, false, CG>(p, s);
+    dispatch_epi<false, false, CG>(p, s, a);
   else if (!p.a_mn && p.b_mn)
-    dispatch_epi<false, true, CG>(p, s);
+    dispatch_epi<false, true, CG>(p, s, a);
   else if (p.a_mn && p.b_mn)
-    dispatch_epi<true, true, CG>(p, s);
+    dispatch_epi<true, true, CG>(p, s, a);
   else
-    dispatch_epi<true, false, CG>(p, s);
+    dispatch_epi<true, false, CG>(p, s, a);
 }
 
 }  // namespace
@@ -156,6 +157,7 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   const int units = num_sms() / cg;  // CTA pairs (or CTAs) resident at once
   p.grid = (p.args.num_tiles < units ? p.args.num_tiles : units) * cg;
   p.flops = 2.0 * M * static_cast<double>(N) * K;
+  p.prepare();
   if (epi == EPI_ADAMW) {
     if (!p.args.opt_p || !p.args.opt_m || !p.args.opt_v || !p.args.opt_p16 || !p.args.opt_hp)
       throw std::invalid_argument("gemm: AdamW epilogue needs p/m/v/p16/hp");
@@ -175,6 +177,13 @@ void GemmPlan::launch(cudaStream_t s) const {
     dispatch_major<2>(*this, s);
   else
     dispatch_major<1>(*this, s);
+}
+
+void GemmPlan::prepare() const {
+  if (cg == 2)
+    dispatch_major<2>(*this, nullptr, true);
+  else
+    dispatch_major<1>(*this, nullptr, true);
 }
 
 }  // namespace gemm

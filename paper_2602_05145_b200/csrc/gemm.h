@@ -77,6 +77,7 @@ struct GemmPlan {
   int grid = 0;
   double flops = 0;
   void launch(cudaStream_t s) const;
+  void prepare() const;  // one-time kernel attributes (never inside a graph capture)
 };
 
 // Throws std::invalid_argument on bad shapes / alignment.

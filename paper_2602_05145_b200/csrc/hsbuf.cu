@@ -9,6 +9,7 @@
 // interleaves the tapped layers into [n, layers*H] rows; device appends
 // (capture on the same GPU) pack straight from the layer tensors.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "common.h"
@@ -37,6 +38,8 @@ HiddenStateBuffer::HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_t
       cap_(capacity_tokens),
       flush_threshold_(flush_threshold > 0 ? flush_threshold : kDefaultFlush),
       device_(device) {
+  static std::atomic<uint64_t> next_serial{1};
+  serial_ = next_serial.fetch_add(1);
   geom_.validate();
   Problems p("invalid hidden-state buffer");
   p.check(capacity_tokens > 0, "capacity_tokens must be > 0");
@@ -50,9 +53,26 @@ HiddenStateBuffer::HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_t
   const size_t row = static_cast<size_t>(geom_.bytes_per_token());
   SPECSIM_CUDA(cudaMalloc(&ring_feat_, row * cap_));
   SPECSIM_CUDA(cudaMalloc(&ring_ids_, sizeof(int32_t) * cap_));
-  cudaEvent_t ev;
-  SPECSIM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  ready_ = ev;
+  for (int i = 0; i < kEventRing; ++i) {
+    cudaEvent_t ev;
+    SPECSIM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    events_.push_back(ev);
+  }
+}
+
+void HiddenStateBuffer::record_append(void* stream) {
+  const int64_t seq = ++append_seq_;
+  cudaEvent_t ev = static_cast<cudaEvent_t>(events_[seq % kEventRing]);
+  // the slot last held append seq - kEventRing: make sure it has landed so
+  // event_for() can report anything that old as complete
+  if (seq > kEventRing) SPECSIM_CUDA(cudaEventSynchronize(ev));
+  SPECSIM_CUDA(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)));
+  samples_.at(open_id_).last_seq = seq;
+}
+
+void* HiddenStateBuffer::event_for(int64_t seq) const {
+  if (seq <= 0 || append_seq_ - seq >= kEventRing) return nullptr;  // known complete
+  return events_[static_cast<size_t>(seq % kEventRing)];
 }
 
 HiddenStateBuffer::~HiddenStateBuffer() {
@@ -62,7 +82,7 @@ HiddenStateBuffer::~HiddenStateBuffer() {
   cudaFree(ring_ids_);
   cudaFree(staging_dev_);
   cudaFreeHost(staging_host_);
-  if (ready_) cudaEventDestroy(static_cast<cudaEvent_t>(ready_));
+  for (void* e : events_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -194,7 +214,7 @@ void HiddenStateBuffer::append(int64_t sample_id, double alpha, const void* cons
   if (first < n)
     SPECSIM_CUDA(cudaMemcpyAsync(ring_ids_, d_ids + first, sizeof(int32_t) * (n - first),
                                  cudaMemcpyDeviceToDevice, s));
-  SPECSIM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ready_), s));
+  record_append(s);
   SPECSIM_CUDA(cudaStreamSynchronize(s));  // staging reuse
   head_ += n;
   samples_.at(open_id_).length += n;
@@ -244,7 +264,7 @@ void HiddenStateBuffer::append_packed(int64_t sample_id, double alpha, const uin
   // consumers (trainer steps) order themselves after this event instead of a
   // host sync; pinned-host appends return immediately so the DMA overlaps
   // the step that is running
-  SPECSIM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ready_), s));
+  record_append(s);
   if (!async_pinned) SPECSIM_CUDA(cudaStreamSynchronize(s));
   head_ += n;
   samples_.at(open_id_).length += n;

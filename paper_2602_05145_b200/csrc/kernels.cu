@@ -37,11 +37,12 @@ unsigned blocks_for(long long n, int per_block) {
 // ------------------------------------------------------------ batch gather
 __global__ void gather_batch_kernel(const uint4* __restrict__ ring_feat,
                                     const int32_t* __restrict__ ring_ids, long long cap, int W8,
-                                    BatchSpec spec, int S, uint4* __restrict__ F,
-                                    int32_t* __restrict__ u, int32_t* __restrict__ y,
-                                    int32_t* __restrict__ m) {
+                                    const BatchSpec* __restrict__ specp, int S,
+                                    uint4* __restrict__ F, int32_t* __restrict__ u,
+                                    int32_t* __restrict__ y, int32_t* __restrict__ m) {
   const long long row = blockIdx.x;
   const int b = static_cast<int>(row / S), t = static_cast<int>(row % S);
+  const BatchSpec& spec = *specp;
   const int L = b < spec.n ? spec.len[b] : 0;
   uint4* dst = F + row * W8;
   if (t < L) {
@@ -73,6 +74,11 @@ __global__ void mask_count_kernel(const int32_t* __restrict__ m, long long T, lo
     for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) s += part[i];
     *out = s;
   }
+}
+
+__global__ void select_count_kernel(const long long* __restrict__ o, const long long* __restrict__ c,
+                                    long long* __restrict__ n) {
+  *n = *o > 0 ? *o : *c;
 }
 
 __global__ void ce_coef_kernel(const int32_t* __restrict__ m, const long long* __restrict__ n,
@@ -385,9 +391,10 @@ __global__ void ce_finalize_kernel(const float* __restrict__ row_loss,
 // ----------------------------------------------------------------- AdamW
 __global__ void adamw_kernel(long long n4, float4* __restrict__ p, float4* __restrict__ m,
                              float4* __restrict__ v, const float4* __restrict__ g,
-                             uint2* __restrict__ p16, AdamHyper hp) {
+                             uint2* __restrict__ p16, const gemm::AdamDev* __restrict__ hpp) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n4) return;
+  const gemm::AdamDev hp = *hpp;
   float4 pp = p[i], mm = m[i], vv = v[i];
   const float4 gg = g[i];
   float* pa = &pp.x;
@@ -448,7 +455,7 @@ __global__ void pack_packed_kernel(const uint4* __restrict__ src, int W8, int n,
 
 // ============================================================== launchers
 void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long long cap, int W,
-                  const BatchSpec& spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
+                  const BatchSpec* spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
                   int32_t* m, cudaStream_t s) {
   const long long T = static_cast<long long>(B) * S;
   count_launches();
@@ -460,6 +467,12 @@ void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long 
 void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s) {
   count_launches();
   mask_count_kernel<<<1, 1024, 0, s>>>(m, T, out);
+}
+
+void select_count(const long long* override_n, const long long* counted, long long* n_global,
+                  cudaStream_t s) {
+  count_launches();
+  select_count_kernel<<<1, 1, 0, s>>>(override_n, counted, n_global);
 }
 
 void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T,
@@ -523,7 +536,7 @@ void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y,
 }
 
 void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloat16* p16,
-           const AdamHyper& hp, cudaStream_t s) {
+           const gemm::AdamDev* hp, cudaStream_t s) {
   const long long n4 = n / 4;  // n is a multiple of 8 (checked at trainer creation)
   count_launches();
   adamw_kernel<<<blocks_for(n4, 256), 256, 0, s>>>(

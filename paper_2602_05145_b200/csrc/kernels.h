@@ -24,14 +24,18 @@ struct BatchSpec {
 };
 
 // F[T, W] bf16, u/y int32, mask int32 (SURVEY A.2 alignment).
+// spec lives in device memory (so the launch can sit in a CUDA graph)
 void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long long cap, int W,
-                  const BatchSpec& spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
+                  const BatchSpec* spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
                   int32_t* m, cudaStream_t s);
 
 // coef[t] = m[t] / n_global ; n_global read from device scalar (int64)
 void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T, cudaStream_t s);
 // count of mask (int64 device scalar)
 void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s);
+// n_global = override > 0 ? override : counted
+void select_count(const long long* override_n, const long long* counted, long long* n_global,
+                  cudaStream_t s);
 
 // y[t, :H] = bf16(x_row * rstd * w); x_row = x[t] or x[gather[t]] (embedding).
 void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, const float* w,
@@ -72,7 +76,7 @@ struct AdamHyper {
       bc2_sqrt;
 };
 void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloat16* p16,
-           const AdamHyper& hp, cudaStream_t s);
+           const gemm::AdamDev* hp, cudaStream_t s);
 
 void f32_to_bf16(const float* x, __nv_bfloat16* y, long long n, cudaStream_t s);
 

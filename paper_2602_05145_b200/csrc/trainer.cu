@@ -14,6 +14,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <map>
+#include <memory>
+#include <tuple>
 #include <vector>
 
 #include "attention.h"
@@ -157,11 +160,36 @@ class DraftTrainerImpl {
   std::vector<gemm::GemmPlan> f_lm_dw;
   gemm::GemmPlan f_dw_down, f_dw_gu, f_dw_o, f_dw_qkv, f_dw_fc;
 
-  // timing
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
-  std::vector<cudaEvent_t> event_pool;
-  size_t event_next = 0;
+  // One recorded launch sequence (eager step, or a captured CUDA graph): the
+  // phase-timing events it contains and the algorithmic work per phase.
+  struct Recording {
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    std::vector<cudaEvent_t> events;
+    size_t next = 0;
+    unsigned long long kernels = 0;  // device kernels one replay launches
+    double flops[PH_N] = {};
+    int launches[PH_N] = {};
+    cudaGraphExec_t exec = nullptr;
+    void reset() {
+      marks.clear();
+      next = 0;
+      for (int i = 0; i < PH_N; ++i) flops[i] = 0, launches[i] = 0;
+    }
+    ~Recording() {
+      for (auto e : events) cudaEventDestroy(e);
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+  };
+  Recording eager_rec;
+  Recording* rec = &eager_rec;
+  std::map<std::tuple<bool, bool, bool, uint64_t>, std::unique_ptr<Recording>> graphs;
+  bool use_graphs = true;
+  bool capturing = false;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  // per-step inputs, staged in pinned memory and copied by the step itself
+  kern::BatchSpec* d_spec = nullptr;
+  kern::BatchSpec* h_spec = nullptr;
+  long long* n_counted = nullptr;
   cudaEvent_t ev_region[2] = {nullptr, nullptr};
 
   const Param& param(const std::string& name) const {
@@ -275,8 +303,13 @@ class DraftTrainerImpl {
     arena.reserve(&Dattn, T * sh.n_heads);
     arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(T) * H);
     arena.reserve(&adam_dev, 1);
+    arena.reserve(&d_spec, 1);
+    arena.reserve(&n_counted, 1);
     arena.commit();
     SPECSIM_CUDA(cudaMallocHost(&h_adam, sizeof(gemm::AdamDev)));
+    SPECSIM_CUDA(cudaMallocHost(&h_spec, sizeof(kern::BatchSpec)));
+    const char* ng = std::getenv("SPECSIM_NO_GRAPH");
+    use_graphs = !(ng && ng[0] == '1');
     SPECSIM_CUDA(cudaMallocHost(&h_nglobal, sizeof(long long)));
     SPECSIM_CUDA(cudaMallocHost(&h_stats, 4 * sizeof(double)));
     SPECSIM_CUDA(cudaMemsetAsync(Mst, 0, sizeof(float) * total, stream));
@@ -286,6 +319,7 @@ class DraftTrainerImpl {
     init_params(seed);
     init_rope();
     build_plans();
+    attn::prepare(sh.head_dim);
     SPECSIM_CUDA(cudaEventCreate(&ev_begin));
     SPECSIM_CUDA(cudaEventCreate(&ev_end));
     SPECSIM_CUDA(cudaEventCreate(&ev_region[0]));
@@ -313,7 +347,6 @@ class DraftTrainerImpl {
     for (auto e : bucket_events) cudaEventDestroy(e);
     if (ev_comm_done) cudaEventDestroy(ev_comm_done);
     if (comm_stream) cudaStreamDestroy(comm_stream);
-    for (auto e : event_pool) cudaEventDestroy(e);
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
     for (auto e : ev_region)
@@ -321,6 +354,8 @@ class DraftTrainerImpl {
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
     if (h_adam) cudaFreeHost(h_adam);
+    if (h_spec) cudaFreeHost(h_spec);
+    graphs.clear();
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -491,26 +526,29 @@ class DraftTrainerImpl {
 
   // ------------------------------------------------------------ timing
   cudaEvent_t next_event() {
-    if (event_next == event_pool.size()) {
+    if (rec->next == rec->events.size()) {
       cudaEvent_t e;
       SPECSIM_CUDA(cudaEventCreate(&e));
-      event_pool.push_back(e);
+      rec->events.push_back(e);
     }
-    return event_pool[event_next++];
+    return rec->events[rec->next++];
   }
   template <class Fn>
   void timed(int phase, double flops, Fn&& fn) {
+    rec->flops[phase] += flops;
+    rec->launches[phase] += 1;
     if (!timing) {
       fn();
       return;
     }
     cudaEvent_t a = next_event(), b = next_event();
-    SPECSIM_CUDA(cudaEventRecord(a, stream));
+    // inside a capture, External makes these real timestamp nodes (a plain
+    // record would only express a dependency)
+    const unsigned flags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    SPECSIM_CUDA(cudaEventRecordWithFlags(a, stream, flags));
     fn();
-    SPECSIM_CUDA(cudaEventRecord(b, stream));
-    marks.push_back({phase, {a, b}});
-    phase_flops[phase] += flops;
-    phase_launches[phase] += 1;
+    SPECSIM_CUDA(cudaEventRecordWithFlags(b, stream, flags));
+    rec->marks.push_back({phase, {a, b}});
   }
   void run(const gemm::GemmPlan& p, int phase = PH_GEMM, double alg_flops = -1) {
     timed(phase, alg_flops < 0 ? p.flops : alg_flops, [&] { p.launch(stream); });
@@ -525,35 +563,41 @@ class DraftTrainerImpl {
     if (buf.device() != device) throw std::invalid_argument("buffer lives on another device");
     kern::BatchSpec spec{};
     spec.n = n;
+    wait_seq = 0;
     for (int b = 0; b < n; ++b) {
       const auto& s = buf.sample(ids[b]);
       spec.start[b] = s.start;
       spec.len[b] = s.length;
+      wait_seq = std::max<int64_t>(wait_seq, s.last_seq);
     }
     return spec;
   }
+  int64_t wait_seq = 0;  // latest append the current batch depends on
 
-  void forward(HiddenStateBuffer& buf, const kern::BatchSpec& spec, int64_t global_valid) {
+  // Device work of the forward.  Everything that varies per step comes from
+  // pinned staging (h_spec, h_nglobal) through copies issued here, so the
+  // whole step can be captured once into a CUDA graph and replayed.
+  void forward(HiddenStateBuffer& buf) {
     const int S = sh.seq_len;
-    // order after every append issued on the buffer's stream (async ingest)
-    SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(buf.ready_event()), 0));
     timed(PH_INGEST, 0, [&] {
+      SPECSIM_CUDA(cudaMemcpyAsync(d_spec, h_spec, sizeof(kern::BatchSpec), cudaMemcpyHostToDevice,
+                                   stream));
+      SPECSIM_CUDA(cudaMemcpyAsync(n_global + 1, h_nglobal, sizeof(long long),
+                                   cudaMemcpyHostToDevice, stream));
       kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
-                         buf.capacity(), static_cast<int>(W3), spec, sh.micro_batch, S, F, u, y,
+                         buf.capacity(), static_cast<int>(W3), d_spec, sh.micro_batch, S, F, u, y,
                          m, stream);
-      if (global_valid > 0) {
-        *h_nglobal = global_valid;
-        SPECSIM_CUDA(cudaMemcpyAsync(n_global, h_nglobal, sizeof(long long),
-                                     cudaMemcpyHostToDevice, stream));
-      } else {
-        kern::mask_count(m, T, n_global, stream);
-      }
+      kern::mask_count(m, T, n_counted, stream);
     });
-    if (global_valid <= 0 && use_nccl)
+    if (use_nccl)
       timed(PH_COMM, 0, [&] {
-        SPECSIM_NCCL(nccl::api().AllReduce(n_global, n_global, 1, ncclInt64, ncclSum, comm, stream));
+        SPECSIM_NCCL(nccl::api().AllReduce(n_counted, n_counted, 1, ncclInt64, ncclSum, comm, stream));
       });
-    timed(PH_ELEM, 0, [&] { kern::ce_coef(m, n_global, coef, T, stream); });
+    timed(PH_ELEM, 0, [&] {
+      // caller-provided global count (n_global[1]) wins over the counted one
+      kern::select_count(n_global + 1, n_counted, n_global, stream);
+      kern::ce_coef(m, n_global, coef, T, stream);
+    });
     run(p_fc);
     timed(PH_ELEM, 0, [&] {
       kern::rmsnorm_fwd(E, H, u, pf("w_in"), sh.rms_eps, U, 2 * H, rstd_a, T, sh.hidden, stream);
@@ -693,42 +737,34 @@ class DraftTrainerImpl {
     return hp;
   }
 
-  // before the backward: this step's AdamW constants for the fused epilogues
+  // host: this step's AdamW constants into pinned staging (before launch)
   void stage_hyper() {
     const kern::AdamHyper hp = next_hyper();
     *h_adam = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
                             hp.bc2_sqrt, 0.f};
+  }
+
+  // device: copy the constants (read by the fused epilogues and AdamW kernels)
+  void upload_hyper() {
     SPECSIM_CUDA(cudaMemcpyAsync(adam_dev, h_adam, sizeof(gemm::AdamDev), cudaMemcpyHostToDevice,
                                  stream));
   }
 
   void optimizer_update() {
-    const kern::AdamHyper hp = next_hyper();
-    step_count += 1;
     if (use_nccl) {
-      timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, hp, stream); });
+      timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, adam_dev, stream); });
       return;
     }
     // GEMM weights were updated in their dW epilogues; the norm weights remain
     timed(PH_ADAM, 0, [&] {
-      const auto& a = param("w_in");   // w_in, w_hid contiguous
+      const auto& a = param("w_in");  // w_in, w_hid contiguous
       const auto& b = param("w_post");
       const auto& c = param("w_fin");
-      kern::adamw(2 * H, P + a.off, Mst + a.off, Vst + a.off, G + a.off, P16 + a.off, hp, stream);
-      kern::adamw(H, P + b.off, Mst + b.off, Vst + b.off, G + b.off, P16 + b.off, hp, stream);
-      kern::adamw(H, P + c.off, Mst + c.off, Vst + c.off, G + c.off, P16 + c.off, hp, stream);
+      kern::adamw(2 * H, P + a.off, Mst + a.off, Vst + a.off, G + a.off, P16 + a.off, adam_dev,
+                  stream);
+      kern::adamw(H, P + b.off, Mst + b.off, Vst + b.off, G + b.off, P16 + b.off, adam_dev, stream);
+      kern::adamw(H, P + c.off, Mst + c.off, Vst + c.off, G + c.off, P16 + c.off, adam_dev, stream);
     });
-  }
-
-  void begin_step() {
-    for (int i = 0; i < PH_N; ++i) {
-      phase_ms[i] = 0;
-      phase_flops[i] = 0;
-      phase_launches[i] = 0;
-    }
-    marks.clear();
-    event_next = 0;
-    SPECSIM_CUDA(cudaEventRecord(ev_begin, stream));
   }
 
   StepResult end_step() {
@@ -738,11 +774,17 @@ class DraftTrainerImpl {
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
     float ms = 0;
     SPECSIM_CUDA(cudaEventElapsedTime(&ms, ev_begin, ev_end));
-    for (auto& mk : marks) {
-      float t = 0;
-      SPECSIM_CUDA(cudaEventElapsedTime(&t, mk.second.first, mk.second.second));
-      phase_ms[mk.first] += t;
+    for (int i = 0; i < PH_N; ++i) {
+      phase_ms[i] = 0;
+      phase_flops[i] = rec->flops[i];
+      phase_launches[i] = rec->launches[i];
     }
+    if (timing)
+      for (auto& mk : rec->marks) {
+        float tm = 0;
+        SPECSIM_CUDA(cudaEventElapsedTime(&tm, mk.second.first, mk.second.second));
+        phase_ms[mk.first] += tm;
+      }
     StepResult res;
     res.loss = h_stats[0];
     res.valid_tokens = static_cast<int64_t>(h_stats[1]);
@@ -760,24 +802,83 @@ class DraftTrainerImpl {
     });
   }
 
+  // The device work of one step (train) or one forward (eval).
+  void enqueue(HiddenStateBuffer& buf, bool train) {
+    forward(buf);
+    if (train) {
+      upload_hyper();
+      backward();  // includes the bucketed gradient all-reduce when data-parallel
+      optimizer_update();
+    }
+    allreduce_stats();
+  }
+
+  // Runs enqueue() eagerly, or replays (capturing on first use) a CUDA graph of
+  // it: one launch per step instead of ~60, no idle gaps while the host
+  // enqueues.  Graphs are keyed by (train, timing, keep_grads, buffer).
+  void launch(HiddenStateBuffer& buf, bool train) {
+    if (!use_graphs) {
+      eager_rec.reset();
+      rec = &eager_rec;
+      SPECSIM_CUDA(cudaEventRecord(ev_begin, stream));
+      enqueue(buf, train);
+      return;
+    }
+    auto key = std::make_tuple(train, timing, keep_grads, buf.serial());
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+      auto r = std::make_unique<Recording>();
+      rec = r.get();
+      cudaGraph_t g = nullptr;
+      SPECSIM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      const unsigned long long k0 = g_kernel_launches.load();
+      try {
+        enqueue(buf, train);
+      } catch (...) {
+        capturing = false;
+        cudaStreamEndCapture(stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      capturing = false;
+      // captured launches are not executions: count them on every replay instead
+      r->kernels = g_kernel_launches.load() - k0;
+      g_kernel_launches.fetch_sub(r->kernels);
+      SPECSIM_CUDA(cudaStreamEndCapture(stream, &g));
+      SPECSIM_CUDA(cudaGraphInstantiate(&r->exec, g, 0));
+      SPECSIM_CUDA(cudaGraphDestroy(g));
+      it = graphs.emplace(key, std::move(r)).first;
+    }
+    rec = it->second.get();
+    SPECSIM_CUDA(cudaEventRecord(ev_begin, stream));
+    SPECSIM_CUDA(cudaGraphLaunch(rec->exec, stream));
+    count_launches(static_cast<unsigned>(rec->kernels));
+  }
+
+  // host-side preparation shared by step / eval
+  void prepare(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid) {
+    *h_spec = batch_spec(buf, ids, n);
+    *h_nglobal = global_valid > 0 ? global_valid : 0;
+    // order after the appends that wrote this batch's samples only, so copies
+    // issued for later steps keep overlapping (async ingest)
+    if (void* ev = buf.event_for(wait_seq))
+      SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(ev), 0));
+  }
+
   StepResult step(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid) {
     DeviceGuard dg(device);
-    const kern::BatchSpec spec = batch_spec(buf, ids, n);
-    begin_step();
-    forward(buf, spec, global_valid);
+    prepare(buf, ids, n, global_valid);
     stage_hyper();
-    backward();  // includes the bucketed gradient all-reduce when data-parallel
-    optimizer_update();
-    allreduce_stats();
+    launch(buf, true);
+    step_count += 1;
     return end_step();
   }
 
   StepResult eval(HiddenStateBuffer& buf, const int64_t* ids, int n) {
     DeviceGuard dg(device);
-    const kern::BatchSpec spec = batch_spec(buf, ids, n);
-    begin_step();
-    forward(buf, spec, 0);
-    allreduce_stats();
+    prepare(buf, ids, n, 0);
+    launch(buf, false);
     return end_step();
   }
 

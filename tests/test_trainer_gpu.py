@@ -190,3 +190,32 @@ def test_fused_adamw_equals_separate_path(monkeypatch):
     fused.get_grad("w_fin")  # norm-weight grads always exist
     dp.get_grad("lm_head")   # data-parallel path always materialises them
     fused.close(); dp.close(); buf.close()
+
+
+def test_cuda_graph_replay_equals_eager(monkeypatch):
+    """The step is captured once into a CUDA graph and replayed; per-step inputs
+    (batch spec, global count, AdamW constants) flow through captured copies
+    from pinned staging.  Replays with changing batches must equal eager runs."""
+    c = SHAPES["C1"]
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 16)
+    for i in range(12):
+        cap = oracle.synth_capture(SEED, i, 60 + 10 * i, c["vocab"], c["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+    g = api.DraftTrainer(c, lr=1e-3, seed=SEED)
+    monkeypatch.setenv("SPECSIM_NO_GRAPH", "1")
+    e = api.DraftTrainer(c, lr=1e-3, seed=SEED)
+    monkeypatch.delenv("SPECSIM_NO_GRAPH")
+    batches = [list(range(0, 8)), list(range(4, 12)), [11, 3, 5], list(range(2, 10))]
+    for k, ids in enumerate(batches):
+        gv = 0 if k != 2 else 777  # caller-provided global count on one step
+        r1, r2 = g.step(buf, ids, global_valid=gv), e.step(buf, ids, global_valid=gv)
+        assert r1["loss"] == r2["loss"] and r1["valid_tokens"] == r2["valid_tokens"], (k, r1, r2)
+        v1, v2 = g.eval(buf, ids[:4]), e.eval(buf, ids[:4])
+        assert v1["loss"] == v2["loss"] and v1["top1_correct"] == v2["top1_correct"]
+    for nm in ("lm_head", "fc", "w_fin"):
+        assert np.array_equal(g.get_param(nm), e.get_param(nm)), nm
+    g.set_timing(True)  # a timing graph is captured separately
+    r = g.step(buf, batches[0])
+    ph = g.phase_times()
+    assert ph["gemm"]["ms"] > 0 and ph["lm_head_ce"]["launches"] >= 3
+    g.close(); e.close(); buf.close()
