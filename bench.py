@@ -172,8 +172,13 @@ def run_reference(args):
     return 0
 
 
+MODEL_SHAPE = {"C1": "tiny draft head", "C2": "Llama-3.1-8B shape", "C4": "Qwen3-32B shape",
+               "C5": "Llama-3.3-70B shape"}
+
+
 def config_block(args, cfg):
-    return dict(workload=f"{args.config}: EAGLE-3-style draft head, Llama-3.1-8B shape "
+    return dict(workload=f"{args.config}: EAGLE-3-style draft head, "
+                         f"{MODEL_SHAPE.get(args.config, args.config)} "
                          f"(hidden {cfg['hidden']}, 3-layer feature concat, vocab {cfg['vocab']}, "
                          f"seq {cfg['seq_len']}), bf16 GEMMs, synthetic captured hidden states",
                 hidden=cfg["hidden"], vocab=cfg["vocab"], seq_len=cfg["seq_len"],
