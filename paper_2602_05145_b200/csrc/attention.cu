@@ -16,8 +16,11 @@
 // [nh, T] fp32; dqkv [T, NQ] bf16.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "attention.h"
 #include "common.h"
+#include "gemm.h"
 
 namespace specsim {
 namespace attn {
@@ -604,15 +607,37 @@ void check_dims(const Dims& d, int hd) {
   p.throw_if_any();
 }
 
+void forward_tc(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,
+                const CUtensorMap& tm, cudaStream_t s);
+void prepare_tc(int hd);
+
+namespace {
+bool use_tc(const Dims& d) {
+  static const bool off = [] {
+    const char* e = std::getenv("SPECSIM_ATTN_MMA_SYNC");
+    return e && e[0] == '1';
+  }();
+  return !off && d.S % 128 == 0;
+}
+}  // namespace
+
 void prepare(int hd) {
   if (hd == 128)
     prepare_t<128>();
   else
     prepare_t<64>();
+  prepare_tc(hd);
 }
 
 void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,
              cudaStream_t s) {
+  if (use_tc(d)) {
+    // tcgen05 / TMEM / TMA path (attention_tc.cu)
+    const CUtensorMap tm = gemm::make_tensor_map(qkv, static_cast<long long>(d.B) * d.S, d.NQ,
+                                                 d.NQ, 64, 128);
+    forward_tc(qkv, o, lse, d, hd, tm, s);
+    return;
+  }
   if (hd == 128)
     fwd_t<128>(qkv, o, lse, d, s);
   else

@@ -124,6 +124,11 @@ void dispatch_major(const GemmPlan& p, cudaStream_t s, bool a = false) {
 
 }  // namespace
 
+CUtensorMap make_tensor_map(const void* ptr, long long rows, long long cols, long long ld,
+                            int box_cols, int box_rows) {
+  return make_map(ptr, rows, cols, ld, box_cols, box_rows);
+}
+
 GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
                    const Args& extra, int cg) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: empty shape");

@@ -80,6 +80,10 @@ struct GemmPlan {
   void prepare() const;  // one-time kernel attributes (never inside a graph capture)
 };
 
+// 2-D bf16 TMA map (SWIZZLE_128B) over a row-major [rows, cols] matrix.
+CUtensorMap make_tensor_map(const void* ptr, long long rows, long long cols, long long ld,
+                            int box_cols, int box_rows);
+
 // Throws std::invalid_argument on bad shapes / alignment.
 GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int epi,
                    const Args& extra, int cg = 2);

@@ -46,8 +46,10 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
+# S % 128 == 0 runs the tcgen05 forward (attention_tc.cu); other lengths the
+# mma.sync fallback.  S = 1024 exercises many KV blocks and the lazy rescale.
 @pytest.mark.parametrize("B,S,nh,nkv,hd", [(2, 128, 4, 2, 64), (1, 256, 8, 2, 128), (2, 192, 4, 4, 128),
-                                           (1, 64, 2, 1, 64)])
+                                           (1, 64, 2, 1, 64), (1, 1024, 4, 1, 128), (2, 512, 4, 2, 64)])
 def test_attention_fwd_bwd(B, S, nh, nkv, hd):
     rng = np.random.default_rng(B * 1000 + S + nh)
     NQ = (nh + 2 * nkv) * hd
@@ -74,3 +76,25 @@ def test_attention_rejects_bad_shapes():
     with pytest.raises(_lib.DomainError):
         _lib.call("specsim_debug_attention", 1, 100, 2, 1, 64, _lib.ptr(z), None, _lib.ptr(z),
                   _lib.ptr(f), None)
+
+
+def test_large_logit_range_rescale():
+    """Scores that grow along the sequence force the lazy O rescale path."""
+    B, S, nh, nkv, hd = 1, 512, 2, 1, 128
+    rng = np.random.default_rng(7)
+    NQ = (nh + 2 * nkv) * hd
+    x = rng.standard_normal((B * S, NQ)).astype(np.float32)
+    ramp = np.linspace(0.5, 6.0, S, dtype=np.float32)[:, None]
+    x[:, nh * hd:(nh + nkv) * hd] *= ramp  # keys get larger later -> row max keeps growing
+    x[:, :nh * hd] *= 2.0
+    from _util import f32_to_bf16_bits
+    bits = f32_to_bf16_bits(x)
+    q = bf16_bits_to_f32(bits)
+    do_bits, do = rand_bf16(rng, (B * S, nh * hd))
+    o = np.zeros((B * S, nh * hd), np.uint16)
+    lse = np.zeros((nh, B * S), np.float32)
+    _lib.call("specsim_debug_attention", B, S, nh, nkv, hd, _lib.ptr(bits), None,
+              _lib.ptr(o), _lib.ptr(lse), None)
+    O, LSE, _ = ref(q, do, B, S, nh, nkv, hd)
+    assert rel(bf16_bits_to_f32(o), O) < 1e-2
+    np.testing.assert_allclose(lse, LSE, rtol=1e-4, atol=2e-3)
