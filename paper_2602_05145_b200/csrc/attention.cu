@@ -610,6 +610,8 @@ void check_dims(const Dims& d, int hd) {
 void forward_tc(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,
                 const CUtensorMap& tm, cudaStream_t s);
 void prepare_tc(int hd);
+void backward_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
+                 const float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, int hd, cudaStream_t s);
 
 namespace {
 bool use_tc(const Dims& d) {
@@ -647,6 +649,14 @@ void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims&
 void backward(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16* dout,
               const float* lse, float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, int hd,
               cudaStream_t s) {
+  if (use_tc(d)) {
+    const long long T = static_cast<long long>(d.B) * d.S;
+    count_launches();
+    attn_bwd_dot_kernel<<<static_cast<unsigned>((T * d.nh * 32 + 255) / 256), 256, 0, s>>>(
+        dout, o, Dbuf, d, hd);
+    backward_tc(qkv, dout, lse, Dbuf, dqkv, d, hd, s);
+    return;
+  }
   if (hd == 128)
     bwd_t<128>(qkv, o, dout, lse, Dbuf, dqkv, d, s);
   else

@@ -14,6 +14,7 @@
 
 #include "attention.h"
 #include "common.h"
+#include "gemm.h"
 #include "ptx.cuh"
 
 namespace specsim {
@@ -289,6 +290,461 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+
+// ======================================================================
+// Backward.  D = rowsum(dO * O) comes from attn_bwd_dot_kernel (attention.cu).
+//
+// dK / dV kernel: one CTA = (sample, KV head, 128-key block); loops over the
+// query heads of the GQA group and every 64-query block at or after the key
+// block.  Per block: S^T = K Q^T and dP^T = V dO^T (M = 128 keys, N = 64 q)
+// into double-buffered TMEM; the "softmax" warps (one key row per thread)
+// form P^T = exp2(S^T*scale*log2e - lse2) and dS^T = P^T (dP^T - D) as bf16
+// K-major tiles in smem; then dV += P^T dO and dK += dS^T Q accumulate in
+// TMEM (the Q / dO tiles double as MN-major B operands).
+constexpr int BQB = 64;               // query block of the dK/dV kernel
+constexpr int TILE64 = BQB * 64 * 2;  // [64 x 64] bf16 SW128 tile = 8 KB
+
+template <int HD>
+struct KvSmem {
+  static constexpr int ATOMS = HD / 64;
+  static constexpr int KV = ATOMS * TILE;       // [128 keys x HD]
+  static constexpr int QT = ATOMS * TILE64;     // [64 q x HD]
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV;
+  static constexpr int OFF_Q = OFF_V + KV;      // 2 stages
+  static constexpr int OFF_DO = OFF_Q + 2 * QT;  // 2 stages
+  static constexpr int OFF_P = OFF_DO + 2 * QT;  // 2 x [128 keys x 64 q]
+  static constexpr int OFF_DS = OFF_P + 2 * TILE;
+  static constexpr int OFF_LD = OFF_DS + 2 * TILE;  // 2 stages x (lse[64], D[64]) fp32
+  static constexpr int OFF_BAR = OFF_LD + 2 * 2 * BQB * 4;
+  static constexpr int BYTES = 1024 + OFF_BAR + 256;
+};
+
+__device__ __forceinline__ uint64_t kdesc64(uint32_t base, int kk) {
+  return ptx::make_sw128_desc(base + (kk >> 2) * TILE64 + (kk & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t mndesc64(uint32_t base, int kk) {
+  return ptx::make_sw128_desc(base + kk * 2048, TILE64, 1024);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_kv_tc_kernel(const __grid_constant__ CUtensorMap tm_kv,  // qkv, box {64,128}
+                          const __grid_constant__ CUtensorMap tm_q,   // qkv, box {64,64}
+                          const __grid_constant__ CUtensorMap tm_do,  // dO,  box {64,64}
+                          const float* __restrict__ lse, const float* __restrict__ Dv,
+                          __nv_bfloat16* __restrict__ dqkv, Dims d) {
+  using L = KvSmem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;   // [2]
+  uint64_t* qd_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_free = bar + 7;    // [2]
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* p_free = bar + 11;   // [2]
+  uint64_t* all_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  float* sLD = reinterpret_cast<float*>(smem + L::OFF_LD);
+
+  const int kb = blockIdx.x;  // key block; early keys see the most queries
+  const int g = blockIdx.y, b = blockIdx.z;
+  const int rep = d.nh / d.nkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = b * d.S;
+  const long long T = static_cast<long long>(d.B) * d.S;
+  const int qb0 = kb * (BKV / BQB), nqb = d.S / BQB;
+  const int per_head = nqb - qb0;
+  const int n_it = rep * per_head;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_kv);
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qd_full[i], 1);
+      ptx::mbar_init(&qd_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_free[i], 4);
+      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&p_free[i], 1);
+    }
+    ptx::mbar_init(all_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem, tdK = tmem + HD;
+  const uint32_t tSt[2] = {tmem + 2 * HD, tmem + 2 * HD + 64};
+  const uint32_t tdPt[2] = {tmem + 2 * HD + 128, tmem + 2 * HD + 192};
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA
+      constexpr int A = L::ATOMS;
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * L::KV);
+      for (int a = 0; a < A; ++a) {
+        ptx::tma_load_2d(&tm_kv, kv_full, smem + L::OFF_K + a * TILE, d.Q + g * HD + 64 * a,
+                         row0 + kb * BKV);
+        ptx::tma_load_2d(&tm_kv, kv_full, smem + L::OFF_V + a * TILE,
+                         d.Q + d.KV + g * HD + 64 * a, row0 + kb * BKV);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const int h = g * rep + it / per_head;
+        const int q0 = (qb0 + it % per_head) * BQB;
+        ptx::mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * L::QT + 2 * BQB * 4);
+        for (int a = 0; a < A; ++a) {
+          ptx::tma_load_2d(&tm_q, &qd_full[st], smem + L::OFF_Q + st * L::QT + a * TILE64,
+                           h * HD + 64 * a, row0 + q0);
+          ptx::tma_load_2d(&tm_do, &qd_full[st], smem + L::OFF_DO + st * L::QT + a * TILE64,
+                           h * HD + 64 * a, row0 + q0);
+        }
+        ptx::bulk_load(sLD + st * 2 * BQB, lse + h * T + row0 + q0, BQB * 4, &qd_full[st]);
+        ptx::bulk_load(sLD + st * 2 * BQB + BQB, Dv + h * T + row0 + q0, BQB * 4, &qd_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA
+      constexpr uint32_t idS = ptx::make_idesc_bf16(BKV, BQB, false, false);
+      constexpr uint32_t idG = ptx::make_idesc_bf16(BKV, HD, false, true);
+      const uint32_t aK = ptx::smem_u32(smem + L::OFF_K), aV = ptx::smem_u32(smem + L::OFF_V);
+      auto issue_s = [&](int it) {
+        const int st = it & 1;
+        ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);
+        ptx::mbar_wait(&s_free[st], ((it >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + st * L::QT);
+        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + st * L::QT);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          ptx::umma_bf16(tSt[st], kdesc(aK, kk), kdesc64(aQ, kk), idS, kk > 0 ? 1u : 0u);
+          ptx::umma_bf16(tdPt[st], kdesc(aV, kk), kdesc64(adO, kk), idS, kk > 0 ? 1u : 0u);
+        }
+        ptx::umma_commit(&s_full[st]);
+      };
+      ptx::mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int it = 0; it < n_it; ++it) {
+        if (it + 1 < n_it) issue_s(it + 1);
+        const int st = it & 1;
+        ptx::mbar_wait(&p_full[st], (it >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t aP = ptx::smem_u32(smem + L::OFF_P + st * TILE);
+        const uint32_t aS = ptx::smem_u32(smem + L::OFF_DS + st * TILE);
+        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + st * L::QT);
+        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + st * L::QT);
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk) {
+          ptx::umma_bf16(tdV, kdesc(aP, kk), mndesc64(adO, kk), idG, (it > 0 || kk > 0) ? 1u : 0u);
+          ptx::umma_bf16(tdK, kdesc(aS, kk), mndesc64(aQ, kk), idG, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        ptx::umma_commit(&p_free[st]);
+        ptx::umma_commit(&qd_empty[st]);
+      }
+      ptx::umma_commit(all_done);
+    }
+  } else {
+    // ------------------------------------------------------------ P^T / dS^T
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // key row within the block (TMEM lane)
+    const int key = kb * BKV + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const float sl2 = d.scale * kLog2e;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const int q0 = (qb0 + it % per_head) * BQB;
+      ptx::mbar_wait(&s_full[st], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t sv[2][32], pv[2][32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        ptx::tmem_ld_32x32b_x32(tSt[st] + lane_off + c * 32, sv[c]);
+        ptx::tmem_ld_32x32b_x32(tdPt[st] + lane_off + c * 32, pv[c]);
+      }
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&s_free[st]);
+      // lse / D slices arrived with this stage's TMA bytes: observe that
+      // barrier directly (cannot have advanced: the stage is only refilled
+      // after the dV/dK MMAs that need this iteration's P / dS)
+      ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);
+      const float* l2 = sLD + st * 2 * BQB;
+      const float* Dq = l2 + BQB;
+      // the P / dS smem buffer of this stage is free once the MMAs of it-2 ran
+      ptx::mbar_wait(&p_free[st], ((it >> 1) & 1) ^ 1);
+      uint8_t* sP = smem + L::OFF_P + st * TILE;
+      uint8_t* sS = smem + L::OFF_DS + st * TILE;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float p[8], ds[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int qi = c * 32 + i + e;
+            float v = exp2f(__uint_as_float(sv[c][i + e]) * sl2 - l2[qi] * kLog2e);
+            if (q0 + qi < key) v = 0.f;  // causal: query before key
+            p[e] = v;
+            ds[e] = v * (__uint_as_float(pv[c][i + e]) - Dq[qi]);
+          }
+          const int cc = (c * 32 + i) >> 3;  // 16-byte chunk within the 128-byte row
+          const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(sP + off) =
+              make_uint4(ptx::pack_bf16x2(p[0], p[1]), ptx::pack_bf16x2(p[2], p[3]),
+                         ptx::pack_bf16x2(p[4], p[5]), ptx::pack_bf16x2(p[6], p[7]));
+          *reinterpret_cast<uint4*>(sS + off) =
+              make_uint4(ptx::pack_bf16x2(ds[0], ds[1]), ptx::pack_bf16x2(ds[2], ds[3]),
+                         ptx::pack_bf16x2(ds[4], ds[5]), ptx::pack_bf16x2(ds[6], ds[7]));
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[st]);
+    }
+    // epilogue: dV, dK (x scale) rows -> dqkv
+    ptx::mbar_wait(all_done, 0);
+    ptx::tc_fence_after();
+    __nv_bfloat16* kp = dqkv + static_cast<long long>(row0 + key) * d.NQ + d.Q + g * HD;
+    __nv_bfloat16* vp = kp + d.KV;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t o[32];
+      ptx::tmem_ld_32x32b_x32(tdV + lane_off + c * 32, o);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        ptx::st_global_v4(vp + c * 32 + i,
+                          ptx::pack_bf16x2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])),
+                          ptx::pack_bf16x2(__uint_as_float(o[i + 2]), __uint_as_float(o[i + 3])),
+                          ptx::pack_bf16x2(__uint_as_float(o[i + 4]), __uint_as_float(o[i + 5])),
+                          ptx::pack_bf16x2(__uint_as_float(o[i + 6]), __uint_as_float(o[i + 7])));
+      ptx::tmem_ld_32x32b_x32(tdK + lane_off + c * 32, o);
+      ptx::tmem_ld_wait();
+      const float sc = d.scale;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        ptx::st_global_v4(
+            kp + c * 32 + i,
+            ptx::pack_bf16x2(__uint_as_float(o[i]) * sc, __uint_as_float(o[i + 1]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * sc, __uint_as_float(o[i + 3]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * sc, __uint_as_float(o[i + 5]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * sc, __uint_as_float(o[i + 7]) * sc));
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+// dQ kernel: one CTA = (sample, query head, 128-query block); loops over the
+// key blocks up to the diagonal.  S = Q K^T and dP = dO V^T (M = 128 q,
+// N = 128 keys) into TMEM; dS = P (dP - D) as a bf16 K-major smem tile; then
+// dQ += dS K with the K tile doubling as an MN-major B operand.
+template <int HD>
+struct QSmem {
+  static constexpr int ATOMS = HD / 64;
+  static constexpr int T128 = ATOMS * TILE;  // [128 x HD]
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + T128;
+  static constexpr int OFF_K = OFF_DO + T128;   // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * T128;  // 2 stages
+  static constexpr int OFF_DS = OFF_V + 2 * T128;
+  static constexpr int OFF_BAR = OFF_DS + 2 * TILE;
+  static constexpr int BYTES = 1024 + OFF_BAR + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_q_tc_kernel(const __grid_constant__ CUtensorMap tm_kv,  // qkv, box {64,128}
+                         const __grid_constant__ CUtensorMap tm_do,  // dO,  box {64,128}
+                         const float* __restrict__ lse, const float* __restrict__ Dv,
+                         __nv_bfloat16* __restrict__ dqkv, Dims d) {
+  using L = QSmem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_free = bar + 6;
+  uint64_t* ds_full = bar + 7;
+  uint64_t* ds_free = bar + 8;
+  uint64_t* all_done = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+
+  const int qb = gridDim.x - 1 - blockIdx.x;  // most keys first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int g = h / (d.nh / d.nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = b * d.S;
+  const int nkv = qb + 1;
+  const long long T = static_cast<long long>(d.B) * d.S;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_kv);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+    }
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_free, 4);
+    ptx::mbar_init(ds_full, 4);
+    ptx::mbar_init(ds_free, 1);
+    ptx::mbar_init(all_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdQ = tmem, tS = tmem + 128, tdP = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      constexpr int A = L::ATOMS;
+      ptx::mbar_arrive_expect_tx(q_full, 2 * L::T128);
+      for (int a = 0; a < A; ++a) {
+        ptx::tma_load_2d(&tm_kv, q_full, smem + L::OFF_Q + a * TILE, h * HD + 64 * a,
+                         row0 + qb * BQ);
+        ptx::tma_load_2d(&tm_do, q_full, smem + L::OFF_DO + a * TILE, h * HD + 64 * a,
+                         row0 + qb * BQ);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        ptx::mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&k_full[st], 2 * L::T128);
+        for (int a = 0; a < A; ++a) {
+          ptx::tma_load_2d(&tm_kv, &k_full[st], smem + L::OFF_K + st * L::T128 + a * TILE,
+                           d.Q + g * HD + 64 * a, row0 + j * BKV);
+          ptx::tma_load_2d(&tm_kv, &k_full[st], smem + L::OFF_V + st * L::T128 + a * TILE,
+                           d.Q + d.KV + g * HD + 64 * a, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = ptx::make_idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idQ = ptx::make_idesc_bf16(BQ, HD, false, true);
+      const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q), adO = ptx::smem_u32(smem + L::OFF_DO);
+      const uint32_t aS = ptx::smem_u32(smem + L::OFF_DS);
+      ptx::mbar_wait(q_full, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
+        ptx::mbar_wait(s_free, (j & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
+        const uint32_t aV = ptx::smem_u32(smem + L::OFF_V + st * L::T128);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          ptx::umma_bf16(tS, kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
+          ptx::umma_bf16(tdP, kdesc(adO, kk), kdesc(aV, kk), idS, kk > 0 ? 1u : 0u);
+        }
+        ptx::umma_commit(s_full);
+        ptx::mbar_wait(ds_full, j & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          ptx::umma_bf16(tdQ, kdesc(aS, kk), mndesc(aK, kk), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        ptx::umma_commit(ds_free);
+        ptx::umma_commit(&k_empty[st]);
+      }
+      ptx::umma_commit(all_done);
+    }
+  } else {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int q = qb * BQ + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const float sl2 = d.scale * kLog2e;
+    const float l2 = lse[h * T + row0 + q] * kLog2e;
+    const float Dr = Dv[h * T + row0 + q];
+    uint8_t* sS = smem + L::OFF_DS;
+    for (int j = 0; j < nkv; ++j) {
+      ptx::mbar_wait(s_full, j & 1);
+      ptx::tc_fence_after();
+      // dS is written straight into the (single) smem tile, so wait for the
+      // dQ MMA of j-1 to have consumed it
+      ptx::mbar_wait(ds_free, (j & 1) ^ 1);
+      const bool diag = (j == qb);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32], pv[32];
+        ptx::tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        ptx::tmem_ld_32x32b_x32(tdP + lane_off + c * 32, pv);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float ds[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int kcol = c * 32 + i + e;
+            float p = exp2f(__uint_as_float(sv[i + e]) * sl2 - l2);
+            if (diag && kcol > r) p = 0.f;
+            ds[e] = p * (__uint_as_float(pv[i + e]) - Dr);
+          }
+          const int key = c * 32 + i;
+          const int t = key >> 6, cc = (key & 63) >> 3;
+          *reinterpret_cast<uint4*>(sS + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) =
+              make_uint4(ptx::pack_bf16x2(ds[0], ds[1]), ptx::pack_bf16x2(ds[2], ds[3]),
+                         ptx::pack_bf16x2(ds[4], ds[5]), ptx::pack_bf16x2(ds[6], ds[7]));
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(s_free);
+        ptx::mbar_arrive(ds_full);
+      }
+    }
+    ptx::mbar_wait(all_done, 0);
+    ptx::tc_fence_after();
+    __nv_bfloat16* qp = dqkv + static_cast<long long>(row0 + q) * d.NQ + h * HD;
+    const float sc = d.scale;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t o[32];
+      ptx::tmem_ld_32x32b_x32(tdQ + lane_off + c * 32, o);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        ptx::st_global_v4(
+            qp + c * 32 + i,
+            ptx::pack_bf16x2(__uint_as_float(o[i]) * sc, __uint_as_float(o[i + 1]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * sc, __uint_as_float(o[i + 3]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * sc, __uint_as_float(o[i + 5]) * sc),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * sc, __uint_as_float(o[i + 7]) * sc));
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 template <int HD>
@@ -315,7 +771,44 @@ void forward_tc(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Di
     forward_tc_t<64>(qkv, o, lse, d, tm, s);
 }
 
+template <int HD>
+void backward_tc_t(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
+                   const float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, cudaStream_t s) {
+  const long long T = static_cast<long long>(d.B) * d.S;
+  const CUtensorMap kv = gemm::make_tensor_map(qkv, T, d.NQ, d.NQ, 64, 128);
+  const CUtensorMap q64 = gemm::make_tensor_map(qkv, T, d.NQ, d.NQ, 64, 64);
+  const CUtensorMap do64 = gemm::make_tensor_map(dout, T, d.Q, d.Q, 64, 64);
+  const CUtensorMap do128 = gemm::make_tensor_map(dout, T, d.Q, d.Q, 64, 128);
+  count_launches(2);
+  attn_bwd_kv_tc_kernel<HD><<<dim3(d.S / BKV, d.nkv, d.B), 192, KvSmem<HD>::BYTES, s>>>(
+      kv, q64, do64, lse, Dbuf, dqkv, d);
+  attn_bwd_q_tc_kernel<HD><<<dim3(d.S / BQ, d.nh, d.B), 192, QSmem<HD>::BYTES, s>>>(
+      kv, do128, lse, Dbuf, dqkv, d);
+}
+
+void backward_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
+                 const float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, int hd, cudaStream_t s) {
+  if (hd == 128)
+    backward_tc_t<128>(qkv, dout, lse, Dbuf, dqkv, d, s);
+  else
+    backward_tc_t<64>(qkv, dout, lse, Dbuf, dqkv, d, s);
+}
+
+template <int HD>
+void prepare_bwd_t() {
+  static_assert(KvSmem<HD>::BYTES <= 232448 && QSmem<HD>::BYTES <= 232448, "smem budget");
+  SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_kv_tc_kernel<HD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    KvSmem<HD>::BYTES));
+  SPECSIM_CUDA(cudaFuncSetAttribute(attn_bwd_q_tc_kernel<HD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, QSmem<HD>::BYTES));
+}
+
 void prepare_tc(int hd) {
+  if (hd == 128)
+    prepare_bwd_t<128>();
+  else
+    prepare_bwd_t<64>();
   if (hd == 128)
     SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<128>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,

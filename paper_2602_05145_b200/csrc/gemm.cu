@@ -152,10 +152,25 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   p.args.num_m_blocks = (M + tile_m - 1) / tile_m;
   p.args.num_n_blocks = (N + BN - 1) / BN;
   p.args.num_tiles = p.args.num_m_blocks * p.args.num_n_blocks;
-  // Row group: keep the group's A panel (tile_m x K bf16 per row block) within
-  // ~64 MB of the 126 MB L2 so B panels stream from DRAM about once.
-  const long long panel = static_cast<long long>(tile_m) * K * 2;
-  long long gm = (64ll << 20) / (panel > 0 ? panel : 1);
+  // L2-aware rasterisation.  If all of B fits in L2 (<= 72 MB), walk the
+  // column blocks fastest (group_m = 1) with B resident: A streams from DRAM
+  // once.  Else if all of A fits, walk row blocks fastest over the whole M
+  // with A resident: B streams once.  Otherwise group row blocks so the
+  // group's A panel stays within ~32 MB.
+  const long long a_bytes = static_cast<long long>(M) * K * 2;
+  const long long b_bytes = static_cast<long long>(N) * K * 2;
+  const long long fit = 72ll << 20;
+  long long gm;
+  p.args.keep_b = 0;
+  if (b_bytes <= fit && b_bytes <= a_bytes) {
+    gm = 1;
+    p.args.keep_b = 1;
+  } else if (a_bytes <= fit) {
+    gm = p.args.num_m_blocks;
+  } else {
+    const long long panel = static_cast<long long>(tile_m) * K * 2;
+    gm = (32ll << 20) / (panel > 0 ? panel : 1);
+  }
   if (gm < 1) gm = 1;
   if (gm > p.args.num_m_blocks) gm = p.args.num_m_blocks;
   p.args.group_m = static_cast<int>(gm);

@@ -118,11 +118,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+      // the operand the rasterisation reuses (see make_plan) is loaded
+      // evict_last so streaming outputs / optimizer state do not flush it
+      const uint64_t pol_a = args.keep_b ? ptx::policy_evict_normal() : ptx::policy_evict_last();
+      const uint64_t pol_b = args.keep_b ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+      auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1,
+                      uint64_t pol) {
         if constexpr (CG == 2)
-          ptx::tma_load_2d_pair(m, bar, dst, c0, c1);
+          ptx::tma_load_2d_pair(m, bar, dst, c0, c1, pol);
         else
-          ptx::tma_load_2d(m, bar, dst, c0, c1);
+          ptx::tma_load_2d_hint(m, bar, dst, c0, c1, pol);
       };
       for (int tile = unit; tile < args.num_tiles; tile += num_units) {
         int mb, nb;
@@ -137,18 +142,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* b_dst = smB + stage * B_STAGE_BYTES;
           const int k0 = kb * BK;
           if constexpr (!A_MN) {
-            load(&tmA, &full_bar[stage], a_dst, k0, m0);
+            load(&tmA, &full_bar[stage], a_dst, k0, m0, pol_a);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              load(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, k0);
+              load(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, k0, pol_a);
           }
           if constexpr (!B_MN) {
-            load(&tmB, &full_bar[stage], b_dst, k0, n0);
+            load(&tmB, &full_bar[stage], b_dst, k0, n0, pol_b);
           } else {
 #pragma unroll
             for (int j = 0; j < C_::BN_CTA / 64; ++j)
-              load(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, k0);
+              load(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, k0, pol_b);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -330,10 +335,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (ok[it])
                 x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e[it]);
             } else if constexpr (EPI == EPI_ADAMW) {
-              if (ok[it]) {
-                x1[it] = *reinterpret_cast<const float4*>(args.opt_p + e[it]);
-                x2[it] = *reinterpret_cast<const float4*>(args.opt_m + e[it]);
-                x3[it] = *reinterpret_cast<const float4*>(args.opt_v + e[it]);
+              if (ok[it]) {  // optimizer state streams once: evict-first
+                x1[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_p + e[it]));
+                x2[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_m + e[it]));
+                x3[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_v + e[it]));
               }
             } else if constexpr (EPI == EPI_CE_BWD) {
               // row constants: x1 = {lse, coef, target (bits)}
@@ -391,12 +396,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float denom = sqrtf(sa[j]) / hp.bc2_sqrt + hp.eps;
                 pa[j] = pi - hp.step_size * (ma[j] / denom);
               }
-              *reinterpret_cast<float4*>(args.opt_p + e[it]) = p;
-              *reinterpret_cast<float4*>(args.opt_m + e[it]) = m;
-              *reinterpret_cast<float4*>(args.opt_v + e[it]) = s2;
-              *reinterpret_cast<uint2*>(args.opt_p16 + e[it]) =
-                  make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w));
-              if (args.opt_g) *reinterpret_cast<float4*>(args.opt_g + e[it]) = w;
+              __stcs(reinterpret_cast<float4*>(args.opt_p + e[it]), p);
+              __stcs(reinterpret_cast<float4*>(args.opt_m + e[it]), m);
+              __stcs(reinterpret_cast<float4*>(args.opt_v + e[it]), s2);
+              __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e[it]),
+                     make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w)));
+              if (args.opt_g) __stcs(reinterpret_cast<float4*>(args.opt_g + e[it]), w);
             }
           }
         }

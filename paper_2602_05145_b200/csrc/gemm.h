@@ -53,6 +53,7 @@ struct Args {
   int vocab_offset;        // vocabulary index of output column 0
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;  // rasterisation group (row blocks)
+  int keep_b;   // 1: B is the L2-resident operand (column-block order), else A
   // fused AdamW epilogue: parameter tensors laid out like C (ldc)
   float *opt_p, *opt_m, *opt_v;
   __nv_bfloat16* opt_p16;
