@@ -152,28 +152,22 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   p.args.num_m_blocks = (M + tile_m - 1) / tile_m;
   p.args.num_n_blocks = (N + BN - 1) / BN;
   p.args.num_tiles = p.args.num_m_blocks * p.args.num_n_blocks;
-  // L2-aware rasterisation.  If all of B fits in L2 (<= 72 MB), walk the
-  // column blocks fastest (group_m = 1) with B resident: A streams from DRAM
-  // once.  Else if all of A fits, walk row blocks fastest over the whole M
-  // with A resident: B streams once.  Otherwise group row blocks so the
-  // group's A panel stays within ~32 MB.
+  // L2-aware rasterisation: the smaller operand is kept resident in groups of
+  // panels totalling ~32 MB (loaded evict_last; measured: larger resident
+  // sets do not survive in the two-die L2 next to streaming traffic) while the
+  // larger operand streams from DRAM once per group.
   const long long a_bytes = static_cast<long long>(M) * K * 2;
   const long long b_bytes = static_cast<long long>(N) * K * 2;
-  const long long fit = 72ll << 20;
-  long long gm;
-  p.args.keep_b = 0;
-  if (b_bytes <= fit && b_bytes <= a_bytes) {
-    gm = 1;
-    p.args.keep_b = 1;
-  } else if (a_bytes <= fit) {
-    gm = p.args.num_m_blocks;
-  } else {
-    const long long panel = static_cast<long long>(tile_m) * K * 2;
-    gm = (32ll << 20) / (panel > 0 ? panel : 1);
-  }
-  if (gm < 1) gm = 1;
-  if (gm > p.args.num_m_blocks) gm = p.args.num_m_blocks;
+  const long long budget = 32ll << 20;
+  p.args.keep_b = b_bytes < a_bytes ? 1 : 0;
+  const long long a_panel = static_cast<long long>(tile_m) * K * 2;
+  const long long b_panel = static_cast<long long>(BN) * K * 2;
+  long long gm = budget / (a_panel > 0 ? a_panel : 1);
+  long long gn = budget / (b_panel > 0 ? b_panel : 1);
+  gm = gm < 1 ? 1 : (gm > p.args.num_m_blocks ? p.args.num_m_blocks : gm);
+  gn = gn < 1 ? 1 : (gn > p.args.num_n_blocks ? p.args.num_n_blocks : gn);
   p.args.group_m = static_cast<int>(gm);
+  p.args.group_n = static_cast<int>(gn);
   const int units = num_sms() / cg;  // CTA pairs (or CTAs) resident at once
   p.grid = (p.args.num_tiles < units ? p.args.num_tiles : units) * cg;
   p.flops = 2.0 * M * static_cast<double>(N) * K;

@@ -49,17 +49,28 @@ constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
 
 __device__ __forceinline__ void tile_coords(int tile, const Args& a, int& mb, int& nb) {
-  // Grouped rasterisation: consecutive tiles walk group_m row blocks first so
-  // the concurrently resident CTAs share B column panels in L2; group_m is
-  // chosen on the host so the A panel of a group stays L2-resident and B
-  // streams through DRAM about once.
-  const int group_size = a.group_m * a.num_n_blocks;
-  const int group = tile / group_size;
-  const int first_m = group * a.group_m;
-  const int gm = min(a.num_m_blocks - first_m, a.group_m);
-  const int in_group = tile - group * group_size;
-  mb = first_m + in_group % gm;
-  nb = in_group / gm;
+  // Grouped rasterisation (group sizes chosen on the host, make_plan): the
+  // smaller operand is walked in groups of panels that stay L2-resident
+  // (loaded evict_last) while the other operand streams through DRAM once
+  // per group.  keep_b: groups of group_n column blocks, row blocks inside;
+  // else groups of group_m row blocks, column blocks inside.
+  if (a.keep_b) {
+    const int group_size = a.group_n * a.num_m_blocks;
+    const int group = tile / group_size;
+    const int first_n = group * a.group_n;
+    const int gn = min(a.num_n_blocks - first_n, a.group_n);
+    const int in_group = tile - group * group_size;
+    nb = first_n + in_group % gn;
+    mb = in_group / gn;
+  } else {
+    const int group_size = a.group_m * a.num_n_blocks;
+    const int group = tile / group_size;
+    const int first_m = group * a.group_m;
+    const int gm = min(a.num_m_blocks - first_m, a.group_m);
+    const int in_group = tile - group * group_size;
+    mb = first_m + in_group % gm;
+    nb = in_group / gm;
+  }
 }
 
 template <bool A_MN, bool B_MN, int EPI, int CG>

@@ -52,8 +52,9 @@ struct Args {
   CePartial* partials;     // [num_n_blocks, M] (fwd)
   int vocab_offset;        // vocabulary index of output column 0
   int num_m_blocks, num_n_blocks, num_tiles;
-  int group_m;  // rasterisation group (row blocks)
-  int keep_b;   // 1: B is the L2-resident operand (column-block order), else A
+  int group_m;  // rasterisation group (row blocks), used when keep_b == 0
+  int group_n;  // rasterisation group (column blocks), used when keep_b == 1
+  int keep_b;   // 1: B panels are the L2-resident operand, else A panels
   // fused AdamW epilogue: parameter tensors laid out like C (ldc)
   float *opt_p, *opt_m, *opt_v;
   __nv_bfloat16* opt_p16;
