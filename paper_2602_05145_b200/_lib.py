@@ -12,7 +12,8 @@ import os
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libspecsim_draft.so"
+# SPECSIM_LIB selects another build of the same library (A/B experiments)
+LIB_PATH = pathlib.Path(os.environ.get("SPECSIM_LIB", str(_HERE / "libspecsim_draft.so")))
 
 OK, EDOMAIN, ECONFIG, ECUDA, ENCCL = 0, 1, 2, 3, 4
 

@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -158,7 +159,11 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   // larger operand streams from DRAM once per group.
   const long long a_bytes = static_cast<long long>(M) * K * 2;
   const long long b_bytes = static_cast<long long>(N) * K * 2;
-  const long long budget = 32ll << 20;
+  static const long long budget = [] {
+    const char* e = std::getenv("SPECSIM_L2_BUDGET_MB");  // A/B experiments
+    const long long mb = e ? std::atoll(e) : 32;
+    return (mb > 0 ? mb : 32) << 20;
+  }();
   p.args.keep_b = b_bytes < a_bytes ? 1 : 0;
   const long long a_panel = static_cast<long long>(tile_m) * K * 2;
   const long long b_panel = static_cast<long long>(BN) * K * 2;

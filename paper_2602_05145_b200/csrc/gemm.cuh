@@ -40,12 +40,13 @@ struct Cfg {
   static constexpr int A_STAGE = BM * BK * 2;            // 16 KB
   static constexpr int B_STAGE = BN_CTA * BK * 2;        // 32 KB (CG1) / 16 KB (CG2)
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int EPI_STAGE = 4 * 32 * 36 * 4;     // per-warp 32x32 fp32 (+pad) staging
+  static constexpr int STAGES = CG == 1 ? 3 : 5;
+  static constexpr int EPI_STAGE = 8 * 32 * 36 * 4;     // per-warp 32x32 fp32 (+pad) staging
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + EPI_STAGE;
   static constexpr int TILE_M = BM * CG;                 // rows per (pair) tile
 };
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_EPI_WARPS = 8;  // two per TMEM lane quadrant, each half the columns
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int TMEM_COLS = 512;
 
 __device__ __forceinline__ void tile_coords(int tile, const Args& a, int& mb, int& nb) {
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull_bar[s], 1);
-      ptx::mbar_init(&tempty_bar[s], 4 * CG);  // every epilogue warp of the group
+      ptx::mbar_init(&tempty_bar[s], NUM_EPI_WARPS * CG);  // every epilogue warp of the group
     }
     ptx::fence_barrier_init();
   }
@@ -230,8 +231,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // free float4 writes and reads) and then walks it row-contiguously, 4 rows
     // x 8 lanes x float4 per warp instruction, so global loads / stores are
     // coalesced 128-byte row segments.
-    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32)
-    float* stg = epi_stage + quad * (32 * 36);
+    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) (hardware rule: warp % 4)
+    const int half = (warp - 2) >> 2;  // which 128 columns of the 256-wide tile
+    float* stg = epi_stage + (warp - 2) * (32 * 36);
+    const int c_begin = half * (BN / 2), c_end = c_begin + BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < args.num_tiles; tile += num_units) {
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int run_arg = 0;
         const int tgt = row_ok ? args.targets[row] - args.vocab_offset : -1;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = c_begin; c < c_end; c += 32) {
           uint32_t r[32];
           __syncwarp();
           ptx::tmem_ld_32x32b_x32(t_row + c, r);
@@ -290,7 +293,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           p.sum = run_sum;
           p.target = tgt_logit;
           p.argmax = run_arg + args.vocab_offset;
-          args.partials[static_cast<long long>(nb) * args.M + row] = p;
+          // one partial per (128-column half tile, row)
+          args.partials[static_cast<long long>(2 * nb + half) * args.M + row] = p;
         }
       } else {
         // per-row constants, owned by lane (row - row_base); shuffled below
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         AdamDev hp{};
         if constexpr (EPI == EPI_ADAMW) hp = *args.opt_hp;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = c_begin; c < c_end; c += 32) {
           uint32_t r[32];
           __syncwarp();
           ptx::tmem_ld_32x32b_x32(t_row + c, r);
@@ -326,30 +330,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // (loads and stores may alias as far as the compiler knows), so the
           // 8 row groups' DRAM latencies overlap
           float4 v[8], x1[8], x2[8], x3[8];
-          bool ok[8];
-          long long e[8];
+          uint32_t okm = 0;  // bit it: row group it in range
+          // element offset of row group it (recomputed: fewer live registers)
+          const long long e0 = static_cast<long long>(row_base + (lane >> 3)) * args.ldc + col;
+          const long long estep = 4 * args.ldc;
+#define SPECSIM_E(it) (e0 + (it) * estep)
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
             const int rl = it * 4 + (lane >> 3);
             const int rr = row_base + rl;
-            ok[it] = col_ok && rr < args.M;
-            e[it] = static_cast<long long>(rr) * args.ldc + col;
+            if (col_ok && rr < args.M) okm |= 1u << it;
+            const long long e_it = SPECSIM_E(it);
             v[it] = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
             if constexpr (EPI == EPI_BF16_RESID) {
-              if (ok[it]) {
+              if (okm >> it & 1) {
                 const uint2 q = *reinterpret_cast<const uint2*>(
                     args.R + static_cast<long long>(rr) * args.ldr + col);
                 x1[it].x = __uint_as_float(q.x);
                 x1[it].y = __uint_as_float(q.y);
               }
             } else if constexpr (EPI == EPI_F32_ACC) {
-              if (ok[it])
-                x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e[it]);
+              if (okm >> it & 1)
+                x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e_it);
             } else if constexpr (EPI == EPI_ADAMW) {
-              if (ok[it]) {  // optimizer state streams once: evict-first
-                x1[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_p + e[it]));
-                x2[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_m + e[it]));
-                x3[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_v + e[it]));
+              if (okm >> it & 1) {  // optimizer state streams once: evict-first
+                x1[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_p + e_it));
+                x2[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_m + e_it));
+                x3[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_v + e_it));
               }
             } else if constexpr (EPI == EPI_CE_BWD) {
               // row constants: x1 = {lse, coef, target (bits)}
@@ -361,7 +368,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // phase 2: compute and store
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
-            if (!ok[it]) continue;
+            if (!(okm >> it & 1)) continue;
+            const long long e_it = SPECSIM_E(it);
             float4 w = v[it];
             float* wa = &w.x;
             if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   wa[j] = (p - ((c + cl + j) == tgt_x - n0 ? 1.f : 0.f)) * coef_x;
                 }
               }
-              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(args.C) + e[it]) =
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(args.C) + e_it) =
                   make_uint2(ptx::pack_bf16x2(w.x, w.y), ptx::pack_bf16x2(w.z, w.w));
             } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
               if constexpr (EPI == EPI_F32_ACC) {
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 w.z += x1[it].z;
                 w.w += x1[it].w;
               }
-              *reinterpret_cast<float4*>(static_cast<float*>(args.C) + e[it]) = w;
+              *reinterpret_cast<float4*>(static_cast<float*>(args.C) + e_it) = w;
             } else if constexpr (EPI == EPI_ADAMW) {
               float4 p = x1[it], m = x2[it], s2 = x3[it];
               float* pa = &p.x;
@@ -407,14 +415,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float denom = sqrtf(sa[j]) / hp.bc2_sqrt + hp.eps;
                 pa[j] = pi - hp.step_size * (ma[j] / denom);
               }
-              __stcs(reinterpret_cast<float4*>(args.opt_p + e[it]), p);
-              __stcs(reinterpret_cast<float4*>(args.opt_m + e[it]), m);
-              __stcs(reinterpret_cast<float4*>(args.opt_v + e[it]), s2);
-              __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e[it]),
+              __stcs(reinterpret_cast<float4*>(args.opt_p + e_it), p);
+              __stcs(reinterpret_cast<float4*>(args.opt_m + e_it), m);
+              __stcs(reinterpret_cast<float4*>(args.opt_v + e_it), s2);
+              __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e_it),
                      make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w)));
-              if (args.opt_g) __stcs(reinterpret_cast<float4*>(args.opt_g + e[it]), w);
+              if (args.opt_g) __stcs(reinterpret_cast<float4*>(args.opt_g + e_it), w);
             }
           }
+#undef SPECSIM_E
         }
       }
       ptx::tc_fence_before();

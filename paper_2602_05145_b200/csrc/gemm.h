@@ -49,7 +49,7 @@ struct Args {
   const int32_t* targets;  // [M] target vocabulary ids
   const float* lse;        // [M] log-sum-exp (bwd)
   const float* coef;       // [M] mask / global token count (bwd)
-  CePartial* partials;     // [num_n_blocks, M] (fwd)
+  CePartial* partials;     // [2 * num_n_blocks, M] (fwd): one per 128-column half tile
   int vocab_offset;        // vocabulary index of output column 0
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;  // rasterisation group (row blocks), used when keep_b == 0

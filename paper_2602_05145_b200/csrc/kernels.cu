@@ -91,7 +91,9 @@ __global__ void ce_coef_kernel(const int32_t* __restrict__ m, const long long* _
 
 // ------------------------------------------------------------ RMSNorm fwd
 constexpr int kNormThreads = 128;
-constexpr int kMaxChunks = 8;  // H <= 128 * 8 * 8 = 8192
+// Rows are cached in registers as kMaxChunks 16-byte chunks per thread
+// (H <= 1024 * kMaxChunks); the kernels are instantiated for 1, 2, 4, 8 so
+// register use (and occupancy) follows the actual hidden size.
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
@@ -105,6 +107,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return s;
 }
 
+template <int kMaxChunks>
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(
     const __nv_bfloat16* __restrict__ x, long long ldx, const int32_t* __restrict__ gather,
     const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ y, long long ldy,
@@ -147,6 +150,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(
 // ------------------------------------------------------------ RMSNorm bwd
 constexpr int kBwdRows = 16;  // rows per CTA (dw partial granularity)
 
+template <int kMaxChunks>
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
     const float* __restrict__ dy, long long lddy, const __nv_bfloat16* __restrict__ x,
     long long ldx, const int32_t* __restrict__ gather, const float* __restrict__ w,
@@ -307,44 +311,52 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu,
 }
 
 // ------------------------------------------------------------ CE reduce
-__global__ void ce_reduce_kernel(const gemm::CePartial* __restrict__ part, int num_nb, long long T,
-                                 const int32_t* __restrict__ y, const int32_t* __restrict__ m,
-                                 float* __restrict__ lse, float* __restrict__ row_loss,
-                                 int32_t* __restrict__ argmax) {
-  const long long t = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  float mx = -INFINITY, tg = -INFINITY;
-  int am = 0x7fffffff;
-  for (int nb = lane; nb < num_nb; nb += 32) {
-    const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
-    if (p.max > mx || (p.max == mx && p.argmax < am)) {
-      mx = p.max;
-      am = p.argmax;
+// Block = 32 consecutive rows x 8 warps.  Warp w merges the partial columns
+// nb = w, w+8, ... with lane = row, so every load is 32 consecutive rows x 16 B
+// (coalesced); the 8 per-warp results are merged through shared memory in
+// fixed order (deterministic).
+struct CeAcc {
+  float max, sum, tgt;
+  int arg;
+};
+
+__device__ __forceinline__ void ce_merge(CeAcc& a, float pmax, float psum, float ptgt, int parg) {
+  if (pmax > a.max || (pmax == a.max && parg < a.arg)) {
+    if (psum > 0.f) a.sum = a.sum * exp2f((a.max - pmax) * 1.4426950408889634f) + psum;
+    a.max = pmax;
+    a.arg = parg;
+  } else if (psum > 0.f) {
+    a.sum += psum * exp2f((pmax - a.max) * 1.4426950408889634f);
+  }
+  a.tgt = fmaxf(a.tgt, ptgt);
+}
+
+__global__ void __launch_bounds__(256) ce_reduce_kernel(
+    const gemm::CePartial* __restrict__ part, int num_nb, long long T,
+    const int32_t* __restrict__ y, const int32_t* __restrict__ m, float* __restrict__ lse,
+    float* __restrict__ row_loss, int32_t* __restrict__ argmax) {
+  __shared__ CeAcc red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t = static_cast<long long>(blockIdx.x) * 32 + lane;
+  CeAcc a{-INFINITY, 0.f, -INFINITY, 0x7fffffff};
+  if (t < T) {
+    for (int nb = warp; nb < num_nb; nb += 8) {
+      const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
+      ce_merge(a, p.max, p.sum, p.target, p.argmax);
     }
-    tg = fmaxf(tg, p.target);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const float omx = __shfl_xor_sync(0xffffffff, mx, o);
-    const int oam = __shfl_xor_sync(0xffffffff, am, o);
-    if (omx > mx || (omx == mx && oam < am)) {
-      mx = omx;
-      am = oam;
+  red[warp][lane] = a;
+  __syncthreads();
+  if (warp == 0 && t < T) {
+    CeAcc r = red[0][lane];
+    for (int w = 1; w < 8; ++w) {
+      const CeAcc o = red[w][lane];
+      ce_merge(r, o.max, o.sum, o.tgt, o.arg);
     }
-    tg = fmaxf(tg, __shfl_xor_sync(0xffffffff, tg, o));
-  }
-  float s = 0.f;
-  for (int nb = lane; nb < num_nb; nb += 32) {
-    const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
-    if (p.sum > 0.f) s += p.sum * exp2f((p.max - mx) * 1.4426950408889634f);
-  }
-  s = warp_sum(s);
-  if (lane == 0) {
-    const float l = mx + logf(s);
+    const float l = r.max + logf(r.sum);
     lse[t] = l;
-    argmax[t] = am;
-    row_loss[t] = m[t] ? (l - tg) : 0.f;
+    argmax[t] = r.arg;
+    row_loss[t] = m[t] ? (l - r.tgt) : 0.f;
   }
 }
 
@@ -485,8 +497,15 @@ void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, c
                  float eps, __nv_bfloat16* y, long long ldy, float* rstd, long long T, int H,
                  cudaStream_t s) {
   count_launches();
-  rmsnorm_fwd_kernel<<<static_cast<unsigned>(T), kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y,
-                                                                       ldy, rstd, H);
+  const unsigned g = static_cast<unsigned>(T);
+  if (H <= 1024)
+    rmsnorm_fwd_kernel<1><<<g, kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y, ldy, rstd, H);
+  else if (H <= 2048)
+    rmsnorm_fwd_kernel<2><<<g, kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y, ldy, rstd, H);
+  else if (H <= 4096)
+    rmsnorm_fwd_kernel<4><<<g, kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y, ldy, rstd, H);
+  else
+    rmsnorm_fwd_kernel<8><<<g, kNormThreads, 0, s>>>(x, ldx, gather, w, eps, y, ldy, rstd, H);
 }
 
 long long rmsnorm_bwd_partial_rows(long long T) { return (T + kBwdRows - 1) / kBwdRows; }
@@ -497,8 +516,19 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
                  float* dw_partial, long long T, int H, cudaStream_t s) {
   const long long nb = rmsnorm_bwd_partial_rows(T);
   count_launches();
-  rmsnorm_bwd_kernel<<<static_cast<unsigned>(nb), kNormThreads, 0, s>>>(
-      dy, lddy, x, ldx, gather, w, rstd, resid, out_f32, out_bf16, ldo, dw_partial, T, H);
+  const unsigned g = static_cast<unsigned>(nb);
+#define SPECSIM_RMS_BWD(C)                                                                     \
+  rmsnorm_bwd_kernel<C><<<g, kNormThreads, 0, s>>>(dy, lddy, x, ldx, gather, w, rstd, resid, \
+                                                   out_f32, out_bf16, ldo, dw_partial, T, H)
+  if (H <= 1024)
+    SPECSIM_RMS_BWD(1);
+  else if (H <= 2048)
+    SPECSIM_RMS_BWD(2);
+  else if (H <= 4096)
+    SPECSIM_RMS_BWD(4);
+  else
+    SPECSIM_RMS_BWD(8);
+#undef SPECSIM_RMS_BWD
   count_launches();
   colsum_kernel<<<blocks_for(H, 256), 256, 0, s>>>(dw_partial, nb, H, dw);
 }
@@ -525,8 +555,8 @@ void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat1
 void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,
                const int32_t* m, float* lse, float* row_loss, int32_t* argmax, cudaStream_t s) {
   count_launches();
-  ce_reduce_kernel<<<blocks_for(T * 32, 256), 256, 0, s>>>(partials, num_nb, T, y, m, lse,
-                                                           row_loss, argmax);
+  ce_reduce_kernel<<<blocks_for(T, 32), 256, 0, s>>>(partials, num_nb, T, y, m, lse, row_loss,
+                                                     argmax);
 }
 
 void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,

@@ -284,7 +284,7 @@ class DraftTrainerImpl {
     arena.reserve(&rstd_fin, T);
     arena.reserve(&lse, T);
     arena.reserve(&row_loss, T);
-    arena.reserve(&partials, nb_ce * T);
+    arena.reserve(&partials, 2 * nb_ce * T);
     arena.reserve(&n_global, 2);
     arena.reserve(&stats, 4);
     arena.reserve(&dlog, T * Vc);
@@ -515,7 +515,7 @@ class DraftTrainerImpl {
   // weight-gradient GEMM: fused AdamW on a single replica, plain fp32 grads
   // (then bucketed all-reduce) when data-parallel
   void run_dw(const gemm::GemmPlan& plain, const gemm::GemmPlan& fusedp, int phase = PH_GEMM) {
-    if (use_nccl) {
+    if (!fused_adamw()) {
       run(plain, phase);
       return;
     }
@@ -625,7 +625,8 @@ class DraftTrainerImpl {
     });
     run(p_ce_fwd, PH_LM);
     timed(PH_ELEM, 0, [&] {
-      kern::ce_reduce(partials, p_ce_fwd.args.num_n_blocks, T, y, m, lse, row_loss, argmax, stream);
+      kern::ce_reduce(partials, 2 * p_ce_fwd.args.num_n_blocks, T, y, m, lse, row_loss, argmax,
+                      stream);
       kern::ce_finalize(row_loss, argmax, y, m, n_global, T, stats, stream);
     });
   }
@@ -750,8 +751,19 @@ class DraftTrainerImpl {
                                  stream));
   }
 
+  // AdamW fused into the weight-gradient epilogues: single replica only (the
+  // data-parallel path needs the all-reduced gradient first).
+  // SPECSIM_NO_FUSED_ADAMW=1 selects the standalone kernel (A/B experiments).
+  bool fused_adamw() const {
+    static const bool off = [] {
+      const char* e = std::getenv("SPECSIM_NO_FUSED_ADAMW");
+      return e && e[0] == '1';
+    }();
+    return !use_nccl && !off;
+  }
+
   void optimizer_update() {
-    if (use_nccl) {
+    if (!fused_adamw()) {
       timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, adam_dev, stream); });
       return;
     }
@@ -1108,7 +1120,7 @@ int specsim_trainer_get_grad(const specsim_trainer* t, const char* name, float* 
   return guard([&] {
     auto& im = impl_of(t);
     const auto& p = im.param(name ? name : "");
-    if (!im.use_nccl && !im.keep_grads && !p.norm)
+    if (im.fused_adamw() && !im.keep_grads && !p.norm)
       throw std::invalid_argument(
           "gradients of GEMM weights are consumed by the fused AdamW epilogue; enable "
           "specsim_trainer_keep_grads before the step to materialise them");
