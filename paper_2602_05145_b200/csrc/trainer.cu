@@ -147,8 +147,21 @@ class DraftTrainerImpl {
   // pinned host scalars
   long long* h_nglobal = nullptr;
   double* h_stats = nullptr;
-  gemm::AdamDev* adam_dev = nullptr;  // this step's AdamW constants (device)
-  gemm::AdamDev* h_adam = nullptr;    // pinned staging
+  // Per-step inputs (batch spec, caller's global token count, AdamW
+  // constants).  The captured step reads them from device memory; the host
+  // fills one of two pinned slots and a stream-ordered copy (outside the
+  // graph) moves it, so train() can enqueue steps back-to-back.
+  struct StepInputs {
+    kern::BatchSpec spec;
+    long long nglobal;  // > 0: caller-provided global valid-token count
+    long long pad;
+    gemm::AdamDev hp;
+  };
+  StepInputs* d_in = nullptr;
+  StepInputs* h_in = nullptr;  // pinned, 2 slots
+  cudaEvent_t in_ev[2] = {nullptr, nullptr};
+  int in_slot = 0;
+  gemm::AdamDev* adam_dev = nullptr;  // = &d_in->hp
   bool keep_grads = false;            // materialise fp32 grads in the fused-AdamW path
 
   // GEMM plans
@@ -186,9 +199,6 @@ class DraftTrainerImpl {
   bool use_graphs = true;
   bool capturing = false;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
-  // per-step inputs, staged in pinned memory and copied by the step itself
-  kern::BatchSpec* d_spec = nullptr;
-  kern::BatchSpec* h_spec = nullptr;
   long long* n_counted = nullptr;
   cudaEvent_t ev_region[2] = {nullptr, nullptr};
 
@@ -302,12 +312,13 @@ class DraftTrainerImpl {
     arena.reserve(&dU, T * 2 * H);
     arena.reserve(&Dattn, T * sh.n_heads);
     arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(T) * H);
-    arena.reserve(&adam_dev, 1);
-    arena.reserve(&d_spec, 1);
+    arena.reserve(&d_in, 1);
     arena.reserve(&n_counted, 1);
     arena.commit();
-    SPECSIM_CUDA(cudaMallocHost(&h_adam, sizeof(gemm::AdamDev)));
-    SPECSIM_CUDA(cudaMallocHost(&h_spec, sizeof(kern::BatchSpec)));
+    adam_dev = &d_in->hp;
+    SPECSIM_CUDA(cudaMallocHost(&h_in, 2 * sizeof(StepInputs)));
+    std::memset(h_in, 0, 2 * sizeof(StepInputs));
+    for (auto& e : in_ev) SPECSIM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const char* ng = std::getenv("SPECSIM_NO_GRAPH");
     use_graphs = !(ng && ng[0] == '1');
     SPECSIM_CUDA(cudaMallocHost(&h_nglobal, sizeof(long long)));
@@ -353,8 +364,9 @@ class DraftTrainerImpl {
       if (e) cudaEventDestroy(e);
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
-    if (h_adam) cudaFreeHost(h_adam);
-    if (h_spec) cudaFreeHost(h_spec);
+    if (h_in) cudaFreeHost(h_in);
+    for (auto e : in_ev)
+      if (e) cudaEventDestroy(e);
     graphs.clear();
     if (stream) cudaStreamDestroy(stream);
   }
@@ -574,19 +586,15 @@ class DraftTrainerImpl {
   }
   int64_t wait_seq = 0;  // latest append the current batch depends on
 
-  // Device work of the forward.  Everything that varies per step comes from
-  // pinned staging (h_spec, h_nglobal) through copies issued here, so the
-  // whole step can be captured once into a CUDA graph and replayed.
+  // Device work of the forward.  Everything that varies per step is read from
+  // d_in (filled by stage() before the launch), so the whole step can be
+  // captured once into a CUDA graph and replayed.
   void forward(HiddenStateBuffer& buf) {
     const int S = sh.seq_len;
     timed(PH_INGEST, 0, [&] {
-      SPECSIM_CUDA(cudaMemcpyAsync(d_spec, h_spec, sizeof(kern::BatchSpec), cudaMemcpyHostToDevice,
-                                   stream));
-      SPECSIM_CUDA(cudaMemcpyAsync(n_global + 1, h_nglobal, sizeof(long long),
-                                   cudaMemcpyHostToDevice, stream));
       kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
-                         buf.capacity(), static_cast<int>(W3), d_spec, sh.micro_batch, S, F, u, y,
-                         m, stream);
+                         buf.capacity(), static_cast<int>(W3), &d_in->spec, sh.micro_batch, S, F,
+                         u, y, m, stream);
       kern::mask_count(m, T, n_counted, stream);
     });
     if (use_nccl)
@@ -594,8 +602,8 @@ class DraftTrainerImpl {
         SPECSIM_NCCL(nccl::api().AllReduce(n_counted, n_counted, 1, ncclInt64, ncclSum, comm, stream));
       });
     timed(PH_ELEM, 0, [&] {
-      // caller-provided global count (n_global[1]) wins over the counted one
-      kern::select_count(n_global + 1, n_counted, n_global, stream);
+      // caller-provided global count wins over the counted one
+      kern::select_count(&d_in->nglobal, n_counted, n_global, stream);
       kern::ce_coef(m, n_global, coef, T, stream);
     });
     run(p_fc);
@@ -738,17 +746,22 @@ class DraftTrainerImpl {
     return hp;
   }
 
-  // host: this step's AdamW constants into pinned staging (before launch)
-  void stage_hyper() {
-    const kern::AdamHyper hp = next_hyper();
-    *h_adam = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
-                            hp.bc2_sqrt, 0.f};
-  }
-
-  // device: copy the constants (read by the fused epilogues and AdamW kernels)
-  void upload_hyper() {
-    SPECSIM_CUDA(cudaMemcpyAsync(adam_dev, h_adam, sizeof(gemm::AdamDev), cudaMemcpyHostToDevice,
-                                 stream));
+  // Host: fill the next pinned slot and enqueue its copy to d_in (stream
+  // ordered before the step's launch, after the previous step).  A slot is
+  // reused only once the copy issued from it two steps ago has executed.
+  void stage(const kern::BatchSpec& spec, int64_t global_valid, bool train) {
+    in_slot ^= 1;
+    SPECSIM_CUDA(cudaEventSynchronize(in_ev[in_slot]));
+    StepInputs& s = h_in[in_slot];
+    s.spec = spec;
+    s.nglobal = global_valid > 0 ? global_valid : 0;
+    if (train) {
+      const kern::AdamHyper hp = next_hyper();
+      s.hp = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
+                           hp.bc2_sqrt, 0.f};
+    }
+    SPECSIM_CUDA(cudaMemcpyAsync(d_in, &s, sizeof(StepInputs), cudaMemcpyHostToDevice, stream));
+    SPECSIM_CUDA(cudaEventRecord(in_ev[in_slot], stream));
   }
 
   // AdamW fused into the weight-gradient epilogues: single replica only (the
@@ -818,7 +831,6 @@ class DraftTrainerImpl {
   void enqueue(HiddenStateBuffer& buf, bool train) {
     forward(buf);
     if (train) {
-      upload_hyper();
       backward();  // includes the bucketed gradient all-reduce when data-parallel
       optimizer_update();
     }
@@ -868,20 +880,20 @@ class DraftTrainerImpl {
     count_launches(static_cast<unsigned>(rec->kernels));
   }
 
-  // host-side preparation shared by step / eval
-  void prepare(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid) {
-    *h_spec = batch_spec(buf, ids, n);
-    *h_nglobal = global_valid > 0 ? global_valid : 0;
-    // order after the appends that wrote this batch's samples only, so copies
-    // issued for later steps keep overlapping (async ingest)
+  // Host-side preparation shared by step / eval: batch spec + inputs staged,
+  // and the stream ordered after the appends that wrote this batch's samples
+  // only (so copies issued for later steps keep overlapping: async ingest).
+  void prepare(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid,
+               bool train) {
+    const kern::BatchSpec spec = batch_spec(buf, ids, n);
     if (void* ev = buf.event_for(wait_seq))
       SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(ev), 0));
+    stage(spec, global_valid, train);
   }
 
   StepResult step(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid) {
     DeviceGuard dg(device);
-    prepare(buf, ids, n, global_valid);
-    stage_hyper();
+    prepare(buf, ids, n, global_valid, true);
     launch(buf, true);
     step_count += 1;
     return end_step();
@@ -889,7 +901,7 @@ class DraftTrainerImpl {
 
   StepResult eval(HiddenStateBuffer& buf, const int64_t* ids, int n) {
     DeviceGuard dg(device);
-    prepare(buf, ids, n, 0);
+    prepare(buf, ids, n, 0, false);
     launch(buf, false);
     return end_step();
   }
@@ -905,41 +917,61 @@ class DraftTrainerImpl {
     for (int i = 0; i < cnt; ++i) mine.push_back(ids[idx[i]]);
   }
 
+  // train(job): every step and eval forward is enqueued back-to-back (no host
+  // synchronisation between steps); per-step loss / counters are copied into a
+  // pinned history and read once at the end.
   TrainingOutcome train(HiddenStateBuffer& buf, const TrainJob& job) {
     Problems p("train job");
     p.check(!job.train_ids.empty(), "D_train must be non-empty (SPEC.md:398 requires n > 0)");
     p.check(job.epochs >= 1, "epochs must be >= 1");
     p.throw_if_any();
+    DeviceGuard dg(device);
     const auto t0 = std::chrono::steady_clock::now();
     const long long per_step = static_cast<long long>(sh.micro_batch) * world;
-    double loss_sum = 0;
-    int64_t steps = 0;
+    const long long n = static_cast<long long>(job.train_ids.size());
+    const long long ne = static_cast<long long>(job.eval_ids.size());
+    const long long train_steps = ((n + per_step - 1) / per_step) * job.epochs;
+    const long long eval_steps = (ne + per_step - 1) / per_step;
+    const long long total_launch = train_steps + eval_steps;
+    double* hist = nullptr;
+    SPECSIM_CUDA(cudaMallocHost(&hist, sizeof(double) * 3 * (total_launch > 0 ? total_launch : 1)));
+    std::unique_ptr<double, decltype(&cudaFreeHost)> hist_guard(hist, &cudaFreeHost);
     std::vector<int64_t> mine;
+    long long k = 0;
     for (int ep = 0; ep < job.epochs; ++ep) {
-      const long long n = static_cast<long long>(job.train_ids.size());
-      for (long long s0 = 0, k = 0; s0 < n; s0 += per_step, ++k) {
-        shard(n, k, mine, job.train_ids);
-        const StepResult r = step(buf, mine.data(), static_cast<int>(mine.size()), 0);
-        loss_sum += r.loss;
-        ++steps;
+      for (long long s0 = 0, j = 0; s0 < n; s0 += per_step, ++j) {
+        shard(n, j, mine, job.train_ids);
+        prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, true);
+        launch(buf, true);
+        step_count += 1;
+        SPECSIM_CUDA(cudaMemcpyAsync(hist + 3 * k++, stats, 3 * sizeof(double),
+                                     cudaMemcpyDeviceToHost, stream));
       }
     }
     // alpha_eval = top-1 accuracy of the new draft on D_eval
-    int64_t valid = 0, correct = 0;
-    const long long ne = static_cast<long long>(job.eval_ids.size());
-    for (long long s0 = 0, k = 0; s0 < ne; s0 += per_step, ++k) {
-      shard(ne, k, mine, job.eval_ids);
-      const StepResult r = eval(buf, mine.data(), static_cast<int>(mine.size()));
-      valid += r.valid_tokens;
-      correct += r.top1_correct;
+    for (long long s0 = 0, j = 0; s0 < ne; s0 += per_step, ++j) {
+      shard(ne, j, mine, job.eval_ids);
+      prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, false);
+      launch(buf, false);
+      SPECSIM_CUDA(cudaMemcpyAsync(hist + 3 * k++, stats, 3 * sizeof(double),
+                                   cudaMemcpyDeviceToHost, stream));
+    }
+    SPECSIM_CHECK_LAUNCH();
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    double loss_sum = 0;
+    for (long long i = 0; i < train_steps; ++i) loss_sum += hist[3 * i];
+    double valid = 0, correct = 0;
+    for (long long i = train_steps; i < total_launch; ++i) {
+      valid += hist[3 * i + 1];
+      correct += hist[3 * i + 2];
     }
     const auto t1 = std::chrono::steady_clock::now();
     TrainingOutcome out;
     out.duration_hours = std::chrono::duration<double>(t1 - t0).count() / 3600.0;
-    out.alpha_eval = valid > 0 ? static_cast<double>(correct) / static_cast<double>(valid) : 0.0;
+    out.alpha_eval = valid > 0 ? correct / valid : 0.0;
     out.new_version = ++version;
-    out.steps = steps;
-    out.mean_loss = steps ? loss_sum / steps : 0.0;
+    out.steps = train_steps;
+    out.mean_loss = train_steps ? loss_sum / static_cast<double>(train_steps) : 0.0;
     return out;
   }
 };
