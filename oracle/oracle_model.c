@@ -8,6 +8,7 @@
 
 #include <math.h>
 #include <stdlib.h>
+#include <stdio.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -61,71 +62,128 @@ void orc_gather_batch(const orc_shape* s, int nsamples, const int32_t* const* id
 }
 
 /* ============================================================== dense math */
-/* C[M,N] (+)= A[M,K] . B[N,K]^T, fp32, cache-blocked. */
-static void mm_nt(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-                  int64_t ldb, float* C, int64_t ldc, int accumulate) {
-  enum { MB = 32, NB = 64, KB = 256 };
-  const int64_t nbm = (M + MB - 1) / MB, nbn = (N + NB - 1) / NB;
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t blk = 0; blk < nbm * nbn; ++blk) {
-    const int64_t i0 = (blk / nbn) * MB, j0 = (blk % nbn) * NB;
-    const int64_t i1 = i0 + MB < M ? i0 + MB : M, j1 = j0 + NB < N ? j0 + NB : N;
-    float acc[MB][NB];
-    for (int64_t i = i0; i < i1; ++i)
-      for (int64_t j = j0; j < j1; ++j)
-        acc[i - i0][j - j0] = accumulate ? C[i * ldc + j] : 0.f;
-    for (int64_t k0 = 0; k0 < K; k0 += KB) {
-      const int64_t kl = (k0 + KB < K ? KB : K - k0);
-      for (int64_t i = i0; i < i1; ++i) {
-        const float* a = A + i * lda + k0;
-        for (int64_t j = j0; j < j1; ++j) {
-          const float* b = B + j * ldb + k0;
-          float part[16] = {0};
-          int64_t k = 0;
-          for (; k + 16 <= kl; k += 16)
-            for (int t = 0; t < 16; ++t) part[t] += a[k + t] * b[k + t];
-          float sum = 0.f;
-          for (int t = 0; t < 16; ++t) sum += part[t];
-          for (; k < kl; ++k) sum += a[k] * b[k];
-          acc[i - i0][j - j0] += sum;
-        }
-      }
+/* C[M,N] (+)= A[M,K] . B[N,K]^T, fp32.  Packed, register-blocked GEMM:
+ * B is packed per (128-column block, 256-deep K block) into 16-wide panels,
+ * A into 6-row panels; a 6x16 AVX2/FMA micro-kernel keeps the C tile in 12
+ * ymm registers (outer products: 2 B loads + 6 broadcasts per 12 FMAs).
+ * Parallel over column blocks (each thread owns disjoint C columns). */
+#include <immintrin.h>
+
+enum { MR = 6, NR = 16, KC = 256, NB = 128, MB = 96 };
+
+static void micro_6x16(int64_t kc, const float* Ap, const float* Bp, float* C, int64_t ldc,
+                       int mr, int nr) {
+  __m256 c[MR][2];
+  for (int i = 0; i < MR; ++i) c[i][0] = c[i][1] = _mm256_setzero_ps();
+  for (int64_t k = 0; k < kc; ++k) {
+    const __m256 b0 = _mm256_loadu_ps(Bp + k * NR), b1 = _mm256_loadu_ps(Bp + k * NR + 8);
+    const float* a = Ap + k * MR;
+    for (int i = 0; i < MR; ++i) {
+      const __m256 ai = _mm256_broadcast_ss(a + i);
+      c[i][0] = _mm256_fmadd_ps(ai, b0, c[i][0]);
+      c[i][1] = _mm256_fmadd_ps(ai, b1, c[i][1]);
     }
-    for (int64_t i = i0; i < i1; ++i)
-      for (int64_t j = j0; j < j1; ++j) C[i * ldc + j] = acc[i - i0][j - j0];
+  }
+  if (mr == MR && nr == NR) {
+    for (int i = 0; i < MR; ++i) {
+      float* cr = C + i * ldc;
+      _mm256_storeu_ps(cr, _mm256_add_ps(_mm256_loadu_ps(cr), c[i][0]));
+      _mm256_storeu_ps(cr + 8, _mm256_add_ps(_mm256_loadu_ps(cr + 8), c[i][1]));
+    }
+  } else {
+    float t[MR][NR];
+    for (int i = 0; i < MR; ++i) {
+      _mm256_storeu_ps(t[i], c[i][0]);
+      _mm256_storeu_ps(t[i] + 8, c[i][1]);
+    }
+    for (int i = 0; i < mr; ++i)
+      for (int j = 0; j < nr; ++j) C[i * ldc + j] += t[i][j];
   }
 }
 
-static float* transpose(const float* X, int64_t rows, int64_t cols, int64_t ld) {
-  float* T = (float*)malloc(sizeof(float) * rows * cols);
-  enum { TB = 64 };
-#pragma omp parallel for schedule(static)
-  for (int64_t i0 = 0; i0 < rows; i0 += TB)
-    for (int64_t j0 = 0; j0 < cols; j0 += TB)
-      for (int64_t i = i0; i < i0 + TB && i < rows; ++i)
-        for (int64_t j = j0; j < j0 + TB && j < cols; ++j) T[j * rows + i] = X[i * ld + j];
-  return T;
+/* C[M,N] (+)= op(A) op(B)^T with op(A)[i][k] = at ? A[k*lda+i] : A[i*lda+k] and
+ * op(B)[j][k] = bt ? B[k*ldb+j] : B[j*ldb+k]: the transposes happen while
+ * packing, never as separate passes. */
+static void mm_gen(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int at,
+                   const float* B, int64_t ldb, int bt, float* C, int64_t ldc, int accumulate) {
+  const int64_t nblocks = (N + NB - 1) / NB;
+#pragma omp parallel
+  {
+    float* Bp = (float*)aligned_alloc(64, sizeof(float) * NB * KC);
+    float* Ap = (float*)aligned_alloc(64, sizeof(float) * (MB + MR) * KC);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t jb = 0; jb < nblocks; ++jb) {
+      const int64_t j0 = jb * NB, nj = (j0 + NB < N ? NB : N - j0);
+      if (!accumulate)
+        for (int64_t i = 0; i < M; ++i) memset(C + i * ldc + j0, 0, sizeof(float) * nj);
+      for (int64_t k0 = 0; k0 < K; k0 += KC) {
+        const int64_t kc = (k0 + KC < K ? KC : K - k0);
+        /* pack B[j0 .. j0+nj) x [k0 .. k0+kc) into 16-column panels, k-major */
+        for (int64_t p = 0; p < (nj + NR - 1) / NR; ++p)
+          for (int64_t k = 0; k < kc; ++k)
+            for (int j = 0; j < NR; ++j) {
+              const int64_t jj = p * NR + j;
+              Bp[(p * KC + k) * NR + j] =
+                  jj < nj ? (bt ? B[(k0 + k) * ldb + j0 + jj] : B[(j0 + jj) * ldb + k0 + k]) : 0.f;
+            }
+        for (int64_t i0 = 0; i0 < M; i0 += MB) {
+          const int64_t mi = (i0 + MB < M ? MB : M - i0);
+          /* pack A rows into 6-row panels, k-major */
+          for (int64_t p = 0; p < (mi + MR - 1) / MR; ++p)
+            for (int64_t k = 0; k < kc; ++k)
+              for (int i = 0; i < MR; ++i) {
+                const int64_t ii = p * MR + i;
+                Ap[(p * KC + k) * MR + i] =
+                    ii < mi ? (at ? A[(k0 + k) * lda + i0 + ii] : A[(i0 + ii) * lda + k0 + k]) : 0.f;
+              }
+          for (int64_t pi = 0; pi < (mi + MR - 1) / MR; ++pi)
+            for (int64_t pj = 0; pj < (nj + NR - 1) / NR; ++pj) {
+              const int mr = (int)((mi - pi * MR) < MR ? (mi - pi * MR) : MR);
+              const int nr = (int)((nj - pj * NR) < NR ? (nj - pj * NR) : NR);
+              micro_6x16(kc, Ap + pi * KC * MR, Bp + pj * KC * NR,
+                         C + (i0 + pi * MR) * ldc + j0 + pj * NR, ldc, mr, nr);
+            }
+        }
+      }
+    }
+    free(Bp);
+    free(Ap);
+  }
+}
+
+static void mm_nt(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                  int64_t ldb, float* C, int64_t ldc, int accumulate) {
+  mm_gen(M, N, K, A, lda, 0, B, ldb, 0, C, ldc, accumulate);
 }
 
 /* C[M,K'] (+)= A[M,N'] . B[N',K']  (data-gradient form) */
 static void mm_nn(int64_t M, int64_t Kp, int64_t Np, const float* A, int64_t lda, const float* B,
                   int64_t ldb, float* C, int64_t ldc, int accumulate) {
-  float* Bt = transpose(B, Np, Kp, ldb); /* [K', N'] */
-  mm_nt(M, Kp, Np, A, lda, Bt, Np, C, ldc, accumulate);
-  free(Bt);
+  mm_gen(M, Kp, Np, A, lda, 0, B, ldb, 1, C, ldc, accumulate);
 }
 
 /* C[N,K] = A[T,N]^T . X[T,K]  (weight-gradient form) */
 static void mm_tn(int64_t N, int64_t K, int64_t T, const float* A, int64_t lda, const float* X,
                   int64_t ldx, float* C, int64_t ldc) {
-  float* At = transpose(A, T, N, lda); /* [N, T] */
-  float* Xt = transpose(X, T, K, ldx); /* [K, T] */
-  mm_nt(N, K, T, At, T, Xt, T, C, ldc, 0);
-  free(At);
-  free(Xt);
+  mm_gen(N, K, T, A, lda, 1, X, ldx, 1, C, ldc, 0);
 }
 
 static float* falloc(int64_t n) { return (float*)calloc((size_t)n, sizeof(float)); }
+
+/* optional section timing (ORACLE_PROFILE=1), printed to stderr */
+static double prof_t0 = 0;
+static int prof_on = -1;
+static void prof(const char* what) {
+  if (prof_on < 0) prof_on = getenv("ORACLE_PROFILE") != NULL;
+  if (!prof_on) return;
+#ifdef _OPENMP
+  const double t = omp_get_wtime();
+#else
+  const double t = 0;
+#endif
+  if (what) fprintf(stderr, "[oracle] %-28s %8.3f s\n", what, t - prof_t0);
+  prof_t0 = t;
+}
 
 /* y = x * rstd * w ; returns rstd per row */
 static void rmsnorm_fwd(int64_t T, int64_t H, const float* x, int64_t ldx, const float* w,
@@ -377,11 +435,23 @@ static void ce_stats(const orc_shape* s, acts* a, const int32_t* y, const int32_
   (void)s;
 }
 
+/* bf16-rounded GEMM weights: one persistent buffer (re-used across steps, so
+ * its pages are touched once) filled by a single parallel rounding pass. */
+static float* wb_cache = NULL;
+static int64_t wb_cache_n = 0;
+
 static void weights_bf16(const orc_shape* s, const float* P, const int64_t* off, int rnd,
                          float** Wb) {
   int64_t rows[ORC_NPARAMS], cols[ORC_NPARAMS];
-  orc_param_layout(s, NULL, rows, cols, NULL);
-  for (int p = 0; p < ORC_NPARAMS; ++p) Wb[p] = wcopy(P + off[p], rows[p] * cols[p], rnd);
+  const int64_t total = orc_param_layout(s, NULL, rows, cols, NULL);
+  if (wb_cache_n != total) {
+    free(wb_cache);
+    wb_cache = (float*)malloc(sizeof(float) * total);
+    wb_cache_n = total;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < total; ++i) wb_cache[i] = rnd ? rb(P[i]) : P[i];
+  for (int p = 0; p < ORC_NPARAMS; ++p) Wb[p] = wb_cache + off[p];
 }
 
 int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, const uint16_t* F,
@@ -398,7 +468,6 @@ int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, cons
   if (lse_out) memcpy(lse_out, a.lse, sizeof(float) * a.T);
   if (argmax_out) memcpy(argmax_out, a.argmax, sizeof(int32_t) * a.T);
   acts_free(&a);
-  for (int p = 0; p < ORC_NPARAMS; ++p) free(Wb[p]);
   return 0;
 }
 
@@ -432,11 +501,15 @@ int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, floa
   int64_t off[ORC_NPARAMS], rows[ORC_NPARAMS], cols[ORC_NPARAMS];
   const int64_t total = orc_param_layout(s, NULL, rows, cols, off);
   float* Wb[ORC_NPARAMS];
+  prof(NULL);
   weights_bf16(s, params, off, rnd, Wb);
+  prof("bf16 weight copies");
   acts a;
   memset(&a, 0, sizeof(a));
   forward_core(s, params, off, E, F16, u, rnd, &a, Wb);
+  prof("forward (incl. LM head)");
   ce_stats(s, &a, y, mask, global_valid, out);
+  prof("CE stats");
   const int64_t T = a.T, H = a.H, Q = a.Q, KV = a.KV, NQ = a.NQKV, I = a.I, V = a.V, W3 = a.W3;
   int64_t nvalid = 0;
   for (int64_t t = 0; t < T; ++t) nvalid += mask[t] ? 1 : 0;
@@ -454,9 +527,12 @@ int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, floa
       l[v] = rnd ? rb(gval) : gval;
     }
   }
+  prof("CE backward (softmax grad)");
   float* dn = falloc(T * H);
   mm_nn(T, H, V, a.dlog, V, Wb[ORC_LM], H, dn, H, 0);
+  prof("LM head dX");
   mm_tn(V, H, T, a.dlog, V, a.nrm, H, grads + off[ORC_LM], H);
+  prof("LM head dW");
 
   /* ---- final norm */
   float* dh = falloc(T * H);
@@ -573,12 +649,13 @@ int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, floa
   round_vec(dg, T * H, rnd);
   mm_tn(H, W3, T, dg, H, a.F, W3, grads + off[ORC_FC], W3);
 
+  prof("decoder backward");
   if (do_update) orc_adamw(total, params, mst, vst, grads, adamw5, step_k);
+  prof("AdamW");
 
   free(dn); free(dh); free(dh_b); free(dact); free(dgu); free(dz); free(dr); free(dr_b);
   free(dO); free(dqkv); free(dU);
   acts_free(&a);
-  for (int p = 0; p < ORC_NPARAMS; ++p) free(Wb[p]);
   (void)rows; (void)cols;
   return 0;
 }
