@@ -26,6 +26,10 @@ SHAPES = {
     # (exercises the chunk loop, the fp32-accumulate dX epilogue and N tails, as C2/C4 do)
     "bigvocab": dict(hidden=256, vocab=40000, seq_len=128, n_heads=4, n_kv_heads=2, head_dim=64,
                      ffn=512, micro_batch=4, rms_eps=1e-5, rope_theta=10000.0),
+    # several 128-query / 128-key attention blocks per sample (causal tiling, lazy
+    # rescale and the tcgen05 backward's multi-block loops inside the full step)
+    "s384": dict(hidden=256, vocab=2048, seq_len=384, n_heads=4, n_kv_heads=2, head_dim=128,
+                 ffn=512, micro_batch=2, rms_eps=1e-5, rope_theta=10000.0),
 }
 
 
@@ -219,3 +223,46 @@ def test_cuda_graph_replay_equals_eager(monkeypatch):
     ph = g.phase_times()
     assert ph["gemm"]["ms"] > 0 and ph["lm_head_ce"]["launches"] >= 3
     g.close(); e.close(); buf.close()
+
+
+def test_all_masked_batch_is_finite():
+    """Samples too short to have a target (L <= 2) contribute no valid tokens:
+    loss 0, zero gradients, finite parameters afterwards."""
+    c = SHAPES["C1"]
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 4096)
+    for i, L in enumerate([1, 2]):
+        cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+        buf.append_packed(i, 0.5, cap["features"], cap["ids"])
+    tr = api.DraftTrainer(c, seed=SEED)
+    tr.keep_grads(True)
+    before = tr.get_param("lm_head")
+    r = tr.step(buf, [0, 1])
+    assert r["valid_tokens"] == 0 and r["loss"] == 0.0 and r["top1_correct"] == 0
+    for nm in ("lm_head", "qkv", "fc", "w_fin"):
+        g = tr.get_grad(nm)
+        assert np.isfinite(g).all() and np.abs(g).max() == 0.0, nm
+    after = tr.get_param("lm_head")
+    assert np.isfinite(after).all() and np.array_equal(before, after)
+    ev = tr.eval(buf, [0])
+    assert ev["valid_tokens"] == 0 and np.isfinite(ev["loss"])
+    tr.close(); buf.close()
+
+
+def test_partial_batch_matches_oracle():
+    """n < micro_batch: missing samples are padding rows (zero features, no
+    targets); the step equals the oracle's on the same padded batch."""
+    c = SHAPES["C1"]
+    c, shp, tr, buf, ids, (F, u, y, m) = setup("C1", [130, 90, 130], n_present=3)
+    P = oracle.init_params(shp, SEED)
+    E = oracle.init_embedding(shp, SEED)
+    z = np.zeros_like(P)
+    out, grads = oracle.train_step(shp, HP, 1, P, z, z.copy(), E, F, u, y, m, update=False)
+    r = tr.step(buf, ids)
+    assert r["valid_tokens"] == out.valid == int(m.sum())
+    assert abs(r["loss"] - out.loss) <= 2e-3 * out.loss
+    layout, _ = oracle.param_layout(shp)
+    off = {n: (o, rr * cc) for n, rr, cc, o in layout}
+    for nm in ("lm_head", "fc"):
+        o, n = off[nm]
+        assert rel(tr.get_grad(nm).reshape(-1), grads[o:o + n]) < 1e-2, nm
+    tr.close(); buf.close()
