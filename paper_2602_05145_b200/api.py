@@ -55,9 +55,9 @@ class Rng:
         call("specsim_rng_create", seed, C.byref(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            _lib.lib().specsim_rng_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_rng_destroy(self.h)
+        self.h = None
 
     def uniform(self) -> float:
         o = C.c_double()
@@ -149,9 +149,9 @@ class HiddenStateBuffer:
              C.byref(self.h))
 
     def close(self):
-        if getattr(self, "h", None):
-            _lib.lib().specsim_hsbuf_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_hsbuf_destroy(self.h)
+        self.h = None
 
     __del__ = close
 
@@ -221,9 +221,9 @@ class DraftTrainer:
              C.cast(nid, C.c_void_p) if nid is not None else None, device, C.byref(self.h))
 
     def close(self):
-        if getattr(self, "h", None):
-            _lib.lib().specsim_trainer_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_trainer_destroy(self.h)
+        self.h = None
 
     __del__ = close
 

@@ -365,6 +365,7 @@ class DraftTrainerImpl {
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
     if (h_in) cudaFreeHost(h_in);
+    if (hist_buf) cudaFreeHost(hist_buf);
     for (auto e : in_ev)
       if (e) cudaEventDestroy(e);
     graphs.clear();
@@ -585,6 +586,8 @@ class DraftTrainerImpl {
     return spec;
   }
   int64_t wait_seq = 0;  // latest append the current batch depends on
+  double* hist_buf = nullptr;  // pinned per-step stats of train()
+  size_t hist_cap = 0;
 
   // Device work of the forward.  Everything that varies per step is read from
   // d_in (filled by stage() before the launch), so the whole step can be
@@ -933,9 +936,15 @@ class DraftTrainerImpl {
     const long long train_steps = ((n + per_step - 1) / per_step) * job.epochs;
     const long long eval_steps = (ne + per_step - 1) / per_step;
     const long long total_launch = train_steps + eval_steps;
-    double* hist = nullptr;
-    SPECSIM_CUDA(cudaMallocHost(&hist, sizeof(double) * 3 * (total_launch > 0 ? total_launch : 1)));
-    std::unique_ptr<double, decltype(&cudaFreeHost)> hist_guard(hist, &cudaFreeHost);
+    // pinned per-step history, grown on demand and kept (pinning is slow)
+    const size_t need = static_cast<size_t>(3 * (total_launch > 0 ? total_launch : 1));
+    if (need > hist_cap) {
+      if (hist_buf) cudaFreeHost(hist_buf);
+      hist_buf = nullptr;
+      SPECSIM_CUDA(cudaMallocHost(&hist_buf, sizeof(double) * need * 2));
+      hist_cap = need * 2;
+    }
+    double* hist = hist_buf;
     std::vector<int64_t> mine;
     long long k = 0;
     for (int ep = 0; ep < job.epochs; ++ep) {
