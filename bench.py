@@ -230,11 +230,21 @@ def run_ours(args):
         ids = torch.empty(L, dtype=torch.int32, pin_memory=True)
         ids.numpy()[:] = c["ids"]
         pinned.append((t, ids, c["alpha_s"]))
+    # Sample ids are global: rank r's samples are RID * r + p.  train(job) takes
+    # the GLOBAL job list (identical on every rank) and shards it: item i of a
+    # step's B*world slice goes to rank i mod world (specsim_dp_shard), so rank r
+    # must hold exactly the ids at slice positions == r (mod world).
+    RID = 10 ** 9
     for i, (t, ids, a) in enumerate(pinned):
-        _lib.call("specsim_hsbuf_append_packed", buf.h, i, a, t.data_ptr(), ids.data_ptr(), L, 0)
+        _lib.call("specsim_hsbuf_append_packed", buf.h, rank * RID + i, a, t.data_ptr(),
+                  ids.data_ptr(), L, 0)
 
     def batch(k):
-        return [(k * B + j) % pool_n for j in range(B)]
+        """this rank's B pool samples for step k (step / eval calls: local ids)"""
+        return [rank * RID + (k * B + j) % pool_n for j in range(B)]
+
+    def global_job(steps, id_of):
+        return api.global_job(steps, B, world, id_of)
 
     def barrier():
         torch.cuda.synchronize()
@@ -256,7 +266,8 @@ def run_ours(args):
     # trainer's stream.
     for k in range(args.warmup):
         tr.step(buf, batch(k))
-    job = [j for k in range(args.steps) for j in batch(args.warmup + k)]
+    job = global_job(args.steps,
+                     lambda r, k, j: r * RID + ((args.warmup + k) * B + j) % pool_n)
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -295,26 +306,24 @@ def run_ours(args):
     # losses / counters come back to the host.
     e2e = None
     if not args.no_e2e:
-        next_id = [pool_n]
+        next_id = [pool_n]  # same sequence on every rank -> globally known ids
         h2d = B * L * (W * 2 + 4)
 
-        def append_batch(k):
-            ids = []
-            for j in range(B):
-                t, idt, a = pinned[(k * B + j) % pool_n]
-                _lib.call("specsim_hsbuf_append_packed", buf.h, next_id[0], a, t.data_ptr(),
-                          idt.data_ptr(), L, 2)
-                ids.append(next_id[0])
-                next_id[0] += 1
-            return ids
-
         def run_e2e(nsteps, per_job=16):
-            # jobs of <= 16 steps bound the ring (each job's batches are appended
-            # asynchronously, then trained on)
+            # jobs of <= 16 steps bound the ring: each job's batches are appended
+            # (asynchronously, this rank's own samples), then the global job trains
             done = 0
             while done < nsteps:
                 n = min(per_job, nsteps - done)
-                ids = [i for k in range(done, done + n) for i in append_batch(k)]
+                base = next_id[0]
+                for k in range(n):
+                    for j in range(B):
+                        t, idt, a = pinned[((done + k) * B + j) % pool_n]
+                        _lib.call("specsim_hsbuf_append_packed", buf.h,
+                                  rank * RID + base + k * B + j, a, t.data_ptr(), idt.data_ptr(),
+                                  L, 2)
+                next_id[0] += n * B
+                ids = global_job(n, lambda r, k, j: r * RID + base + k * B + j)
                 o = tr.train(buf, ids, [], epochs=1)  # the job's loss comes back to the host
                 losses.append(o.mean_loss)
                 done += n

@@ -110,6 +110,14 @@ def dp_shard(n_items: int, per_rank: int, world: int, rank: int, step: int):
     return idx[: n.value].tolist()
 
 
+def global_job(steps: int, per_rank: int, world: int, id_of):
+    """Global train(job) list for data parallelism: slot j of step k belongs to
+    rank j % world (the specsim_dp_shard rule) and holds id_of(rank, k, j // world),
+    i.e. that rank's (j // world)-th sample of step k.  Every rank passes the
+    same list; each trains only its own ids."""
+    return [id_of(j % world, k, j // world) for k in range(steps) for j in range(per_rank * world)]
+
+
 @dataclass
 class SignalGeometry:
     hidden_dim: int

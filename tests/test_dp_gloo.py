@@ -75,6 +75,18 @@ def test_sharding_rule():
     assert api.dp_shard(10, 2, 4, 3, 1) == [] and api.dp_shard(10, 2, 4, 1, 1) == [9]
 
 
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_global_job_routes_each_rank_its_own_samples(world):
+    """bench.py / callers build ONE global job list; train(job) shards it by
+    specsim_dp_shard.  Every rank must get exactly its own B samples per step."""
+    B, RID, steps = 4, 10 ** 9, 5
+    job = api.global_job(steps, B, world, lambda r, k, j: r * RID + k * B + j)
+    for r in range(world):
+        for k in range(steps):
+            mine = [job[i] for i in api.dp_shard(len(job), B, world, r, k)]
+            assert mine == [r * RID + k * B + j for j in range(B)], (world, r, k)
+
+
 def test_world2_equals_single_process_global_batch():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
