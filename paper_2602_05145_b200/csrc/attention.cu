@@ -646,7 +646,7 @@ void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims&
     fwd_t<64>(qkv, o, lse, d, s);
 }
 
-void backward(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16* dout,
+bool backward(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16* dout,
               const float* lse, float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, int hd,
               cudaStream_t s) {
   if (use_tc(d)) {
@@ -655,12 +655,13 @@ void backward(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloa
     attn_bwd_dot_kernel<<<static_cast<unsigned>((T * d.nh * 32 + 255) / 256), 256, 0, s>>>(
         dout, o, Dbuf, d, hd);
     backward_tc(qkv, dout, lse, Dbuf, dqkv, d, hd, s);
-    return;
+    return d.rope_cos != nullptr;
   }
   if (hd == 128)
     bwd_t<128>(qkv, o, dout, lse, Dbuf, dqkv, d, s);
   else
     bwd_t<64>(qkv, o, dout, lse, Dbuf, dqkv, d, s);
+  return false;
 }
 
 }  // namespace attn

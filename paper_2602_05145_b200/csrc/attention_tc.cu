@@ -301,6 +301,52 @@ __global__ void __launch_bounds__(192, 1)
 // form P^T = exp2(S^T*scale*log2e - lse2) and dS^T = P^T (dP^T - D) as bf16
 // K-major tiles in smem; then dV += P^T dO and dK += dS^T Q accumulate in
 // TMEM (the Q / dO tiles double as MN-major B operands).
+// Stores one dq / dk row (TMEM lane = row, HD fp32 columns at tm) scaled by
+// sc as bf16.  With RoPE tables the row is first rounded to bf16 (the value
+// the unfused path stores) and then inverse-rotated in registers:
+// x1' = x1 c + x2 s, x2' = x2 c - x1 s.
+template <int HD>
+__device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, float sc,
+                                               const Dims& d, int pos) {
+  constexpr int HALF = HD / 2;
+  // rotation partners (i, i + HD/2) sit in chunks p and p + HD/64: process one
+  // such pair of 32-column chunks at a time (64 live registers)
+#pragma unroll
+  for (int p = 0; p < HD / 64; ++p) {
+    uint32_t a[32], b[32];
+    ptx::tmem_ld_32x32b_x32(tm + p * 32, a);
+    ptx::tmem_ld_32x32b_x32(tm + HALF + p * 32, b);
+    ptx::tmem_ld_wait();
+    float s = sc;
+    if (d.rope_cos != nullptr) {
+      const float* cs = d.rope_cos + static_cast<long long>(p * 32) * d.S + pos;
+      const float* sn = d.rope_sin + static_cast<long long>(p * 32) * d.S + pos;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float cv = __ldg(cs + static_cast<long long>(i) * d.S);
+        const float sv = __ldg(sn + static_cast<long long>(i) * d.S);
+        const float x1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(a[i]) * sc));
+        const float x2 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(b[i]) * sc));
+        a[i] = __float_as_uint(x1 * cv + x2 * sv);
+        b[i] = __float_as_uint(x2 * cv - x1 * sv);
+      }
+      s = 1.f;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t* o = h ? b : a;
+      __nv_bfloat16* out = dst + h * HALF + p * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        ptx::st_global_v4(
+            out + i, ptx::pack_bf16x2(__uint_as_float(o[i]) * s, __uint_as_float(o[i + 1]) * s),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * s, __uint_as_float(o[i + 3]) * s),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * s, __uint_as_float(o[i + 5]) * s),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * s, __uint_as_float(o[i + 7]) * s));
+    }
+  }
+}
+
 constexpr int BQB = 64;               // query block of the dK/dV kernel
 constexpr int TILE64 = BQB * 64 * 2;  // [64 x 64] bf16 SW128 tile = 8 KB
 
@@ -530,18 +576,8 @@ __global__ void __launch_bounds__(192, 1)
                           ptx::pack_bf16x2(__uint_as_float(o[i + 2]), __uint_as_float(o[i + 3])),
                           ptx::pack_bf16x2(__uint_as_float(o[i + 4]), __uint_as_float(o[i + 5])),
                           ptx::pack_bf16x2(__uint_as_float(o[i + 6]), __uint_as_float(o[i + 7])));
-      ptx::tmem_ld_32x32b_x32(tdK + lane_off + c * 32, o);
-      ptx::tmem_ld_wait();
-      const float sc = d.scale;
-#pragma unroll
-      for (int i = 0; i < 32; i += 8)
-        ptx::st_global_v4(
-            kp + c * 32 + i,
-            ptx::pack_bf16x2(__uint_as_float(o[i]) * sc, __uint_as_float(o[i + 1]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * sc, __uint_as_float(o[i + 3]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * sc, __uint_as_float(o[i + 5]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * sc, __uint_as_float(o[i + 7]) * sc));
     }
+    store_grad_row<HD>(tdK + lane_off, kp, d.scale, d, (row0 + key) % d.S);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -721,21 +757,7 @@ __global__ void __launch_bounds__(192, 1)
     ptx::mbar_wait(all_done, 0);
     ptx::tc_fence_after();
     __nv_bfloat16* qp = dqkv + static_cast<long long>(row0 + q) * d.NQ + h * HD;
-    const float sc = d.scale;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      ptx::tmem_ld_32x32b_x32(tdQ + lane_off + c * 32, o);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; i += 8)
-        ptx::st_global_v4(
-            qp + c * 32 + i,
-            ptx::pack_bf16x2(__uint_as_float(o[i]) * sc, __uint_as_float(o[i + 1]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * sc, __uint_as_float(o[i + 3]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * sc, __uint_as_float(o[i + 5]) * sc),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * sc, __uint_as_float(o[i + 7]) * sc));
-    }
+    store_grad_row<HD>(tdQ + lane_off, qp, d.scale, d, (row0 + q) % d.S);
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -107,6 +107,7 @@ void dispatch_epi(const GemmPlan& p, cudaStream_t s, bool a = false) {
     case EPI_CE_FWD: launch_t<A_MN, B_MN, EPI_CE_FWD, CG>(p, s, a); break;
     case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s, a); break;
     case EPI_ADAMW: launch_t<A_MN, B_MN, EPI_ADAMW, CG>(p, s, a); break;
+    case EPI_BF16_ROPE: launch_t<A_MN, B_MN, EPI_BF16_ROPE, CG>(p, s, a); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
 }
@@ -182,8 +183,13 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
       throw std::invalid_argument("gemm: AdamW epilogue needs p/m/v/p16/hp");
     if ((p.args.ldc * 4) % 16 != 0) throw std::invalid_argument("gemm: ldc not 16B aligned");
   }
+  if (epi == EPI_BF16_ROPE) {
+    if (!p.args.rope_cos || !p.args.rope_sin || p.args.rope_S <= 0 ||
+        (p.args.rope_hd != 64 && p.args.rope_hd != 128) || p.args.rope_cols % p.args.rope_hd)
+      throw std::invalid_argument("gemm: bad RoPE epilogue arguments");
+  }
   if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
-      epi == EPI_F32_ACC) {
+      epi == EPI_F32_ACC || epi == EPI_BF16_ROPE) {
     if (!p.args.C) throw std::invalid_argument("gemm: missing output");
     if ((p.args.ldc * (epi == EPI_F32 || epi == EPI_F32_ACC ? 4 : 2)) % 16 != 0)
       throw std::invalid_argument("gemm: ldc not 16B aligned");

@@ -296,6 +296,80 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // one partial per (128-column half tile, row)
           args.partials[static_cast<long long>(2 * nb + half) * args.M + row] = p;
         }
+      } else if constexpr (EPI == EPI_BF16_ROPE) {
+        // qkv projection + RoPE: a 128-column half tile holds whole heads
+        // (head_dim 64 or 128), so each rotation pair (i, i + hd/2) lives in
+        // this thread's registers.  Values are rounded to bf16 before rotating
+        // (the unfused path rotates the stored bf16 projection).
+        uint32_t rr[4][32];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ptx::tmem_ld_32x32b_x32(t_row + c_begin + 32 * q, rr[q]);
+        ptx::tmem_ld_wait();
+        const int colh = n0 + c_begin;  // first column of this half tile
+        if (row_ok && colh < args.N) {
+          const int pos = row % args.rope_S;
+          auto rot = [&](float& a, float& b, float cs, float sn) {
+            const float x1 = __bfloat162float(__float2bfloat16_rn(a));
+            const float x2 = __bfloat162float(__float2bfloat16_rn(b));
+            a = x1 * cs - x2 * sn;
+            b = x2 * cs + x1 * sn;
+          };
+          const long long S = args.rope_S;
+          // tables [hd/2, S]: lanes hold consecutive rows, so each load is coalesced
+          if (args.rope_hd == 128) {
+            if (colh < args.rope_cols) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const long long ti = (q * 32 + i) * S + pos;
+                  float a = __uint_as_float(rr[q][i]), b = __uint_as_float(rr[q + 2][i]);
+                  rot(a, b, __ldg(args.rope_cos + ti), __ldg(args.rope_sin + ti));
+                  rr[q][i] = __float_as_uint(a);
+                  rr[q + 2][i] = __float_as_uint(b);
+                }
+            }
+          } else {  // head_dim 64: two heads per half tile
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              if (colh + 64 * hh < args.rope_cols) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const long long ti = i * S + pos;
+                  float a = __uint_as_float(rr[2 * hh][i]), b = __uint_as_float(rr[2 * hh + 1][i]);
+                  rot(a, b, __ldg(args.rope_cos + ti), __ldg(args.rope_sin + ti));
+                  rr[2 * hh][i] = __float_as_uint(a);
+                  rr[2 * hh + 1][i] = __float_as_uint(b);
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col0 = colh + 32 * q;
+          if (col0 >= args.N) break;  // warp-uniform
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(stg + lane * 36 + i) =
+                make_float4(__uint_as_float(rr[q][i]), __uint_as_float(rr[q][i + 1]),
+                            __uint_as_float(rr[q][i + 2]), __uint_as_float(rr[q][i + 3]));
+          __syncwarp();
+          const int cl = (lane & 7) * 4;
+          const int col = col0 + cl;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + (lane >> 3);
+            const int rw = row_base + rl;
+            const float4 w = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
+            if (rw < args.M && col < args.N)
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(args.C) +
+                                        static_cast<long long>(rw) * args.ldc + col) =
+                  make_uint2(ptx::pack_bf16x2(w.x, w.y), ptx::pack_bf16x2(w.z, w.w));
+          }
+        }
       } else {
         // per-row constants, owned by lane (row - row_base); shuffled below
         float lse_r = 0.f, coef_r = 0.f;

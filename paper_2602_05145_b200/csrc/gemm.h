@@ -22,6 +22,7 @@ enum Epi : int {
   EPI_CE_FWD = 4,      // per-row partial (max, sum exp, target logit, argmax) per N tile
   EPI_CE_BWD = 5,      // C(bf16) = (exp(acc - lse[row]) - [col == y[row]]) * coef[row]
   EPI_ADAMW = 6,       // acc is a weight gradient: fused PyTorch-AdamW update of p/m/v (+ bf16 p)
+  EPI_BF16_ROPE = 7,   // C(bf16) = acc with NeoX RoPE applied to columns < rope_cols (q | k heads)
 };
 
 // Device-resident AdamW hyper-parameters of the current step (updated per step
@@ -60,6 +61,10 @@ struct Args {
   __nv_bfloat16* opt_p16;
   float* opt_g;  // optional gradient store (nullable)
   const AdamDev* opt_hp;
+  // RoPE epilogue: row r is position r % rope_S; tables transposed [rope_hd / 2, rope_S]
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_S, rope_cols, rope_hd;
 };
 
 // A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).

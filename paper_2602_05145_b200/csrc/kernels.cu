@@ -228,14 +228,27 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
   }
 }
 
-// dw[i] = sum over partial rows (fixed order)
-__global__ void colsum_kernel(const float* __restrict__ part, long long rows, int H,
-                              float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= H) return;
+// dw[i] = sum over partial rows.  Block = 32 columns x 8 row-slices: each
+// thread sums a strided slice (rows r, r+8, ...) for one column (coalesced 128-B
+// row segments across the warp), then the 8 slices are added in fixed order
+// (deterministic).
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ part,
+                                                     long long rows, int H,
+                                                     float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, slice = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (long long r = 0; r < rows; ++r) s += part[r * H + i];
-  out[i] = s;
+  if (col < H)
+    for (long long r = slice; r < rows; r += 8) s += part[r * H + col];
+  red[slice][lane] = s;
+  __syncthreads();
+  if (slice == 0 && col < H) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    out[col] = t;
+  }
 }
 
 // ------------------------------------------------------------------ RoPE
@@ -530,7 +543,7 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
     SPECSIM_RMS_BWD(8);
 #undef SPECSIM_RMS_BWD
   count_launches();
-  colsum_kernel<<<blocks_for(H, 256), 256, 0, s>>>(dw_partial, nb, H, dw);
+  colsum_kernel<<<blocks_for(H, 32), 256, 0, s>>>(dw_partial, nb, H, dw);
 }
 
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,

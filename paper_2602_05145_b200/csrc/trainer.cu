@@ -133,7 +133,8 @@ class DraftTrainerImpl {
   float *P = nullptr, *Mst = nullptr, *Vst = nullptr, *G = nullptr;
   __nv_bfloat16* P16 = nullptr;
   __nv_bfloat16* E = nullptr;  // frozen embedding [V, H]
-  float *cos_t = nullptr, *sin_t = nullptr;
+  float *cos_t = nullptr, *sin_t = nullptr;    // [S, hd/2] (standalone RoPE kernel)
+  float *cos_tr = nullptr, *sin_tr = nullptr;  // [hd/2, S] (fused epilogues: lane = position)
   // activations
   __nv_bfloat16 *F, *g, *U, *qkv, *o, *r, *z, *gu, *act, *h, *nrm;
   int32_t *u, *y, *m, *argmax;
@@ -271,6 +272,8 @@ class DraftTrainerImpl {
     arena.reserve(&E, V * H);
     arena.reserve(&cos_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
     arena.reserve(&sin_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
+    arena.reserve(&cos_tr, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
+    arena.reserve(&sin_tr, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
     arena.reserve(&F, T * W3);
     arena.reserve(&g, T * H);
     arena.reserve(&U, T * 2 * H);
@@ -437,6 +440,14 @@ class DraftTrainerImpl {
       }
     SPECSIM_CUDA(cudaMemcpy(cos_t, c.data(), sizeof(float) * c.size(), cudaMemcpyHostToDevice));
     SPECSIM_CUDA(cudaMemcpy(sin_t, s.data(), sizeof(float) * s.size(), cudaMemcpyHostToDevice));
+    std::vector<float> ct(c.size()), st(c.size());
+    for (int pos = 0; pos < sh.seq_len; ++pos)
+      for (int i = 0; i < half; ++i) {
+        ct[static_cast<size_t>(i) * sh.seq_len + pos] = c[static_cast<size_t>(pos) * half + i];
+        st[static_cast<size_t>(i) * sh.seq_len + pos] = s[static_cast<size_t>(pos) * half + i];
+      }
+    SPECSIM_CUDA(cudaMemcpy(cos_tr, ct.data(), sizeof(float) * ct.size(), cudaMemcpyHostToDevice));
+    SPECSIM_CUDA(cudaMemcpy(sin_tr, st.data(), sizeof(float) * st.size(), cudaMemcpyHostToDevice));
   }
 
   // ------------------------------------------------------------ plans
@@ -455,8 +466,15 @@ class DraftTrainerImpl {
     using namespace gemm;
     // forward: Y = X W^T (both K-major)
     p_fc = make_plan({F, W3, false}, {pb("fc"), W3, false}, T, H, W3, EPI_BF16, out_args(g, H));
-    p_qkv = make_plan({U, 2 * H, false}, {pb("qkv"), 2 * H, false}, T, NQ, 2 * H, EPI_BF16,
-                      out_args(qkv, NQ));
+    // q / k heads rotated in the epilogue (NeoX RoPE); v columns stored as is
+    Args qa = out_args(qkv, NQ);
+    qa.rope_cos = cos_tr;
+    qa.rope_sin = sin_tr;
+    qa.rope_S = sh.seq_len;
+    qa.rope_cols = static_cast<int>(Q + KV);
+    qa.rope_hd = sh.head_dim;
+    p_qkv = make_plan({U, 2 * H, false}, {pb("qkv"), 2 * H, false}, T, NQ, 2 * H, EPI_BF16_ROPE,
+                      qa);
     p_o = make_plan({o, Q, false}, {pb("o"), Q, false}, T, H, Q, EPI_BF16_RESID,
                     out_args(r, H, g, H));
     p_gu = make_plan({z, H, false}, {pb("gate_up"), H, false}, T, 2 * I, H, EPI_BF16,
@@ -615,11 +633,7 @@ class DraftTrainerImpl {
       kern::rmsnorm_fwd(g, H, nullptr, pf("w_hid"), sh.rms_eps, U + H, 2 * H, rstd_b, T,
                         sh.hidden, stream);
     });
-    run(p_qkv);
-    timed(PH_ELEM, 0, [&] {
-      kern::rope(qkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim, cos_t,
-                 sin_t, false, stream);
-    });
+    run(p_qkv);  // RoPE fused into the epilogue
     const attn::Dims ad = attn_dims();
     timed(PH_ATTN, 2.0 * Q * (S + 1) * T, [&] { attn::forward(qkv, o, lse_attn, ad, sh.head_dim, stream); });
     run(p_o);
@@ -704,14 +718,18 @@ class DraftTrainerImpl {
     run(p_dO);
     run_dw(p_dw_o, f_dw_o);
     bucket_ready("o", "w_post");
-    const attn::Dims ad = attn_dims();
+    attn::Dims ad = attn_dims();
+    ad.rope_cos = cos_tr;
+    ad.rope_sin = sin_tr;
+    bool rope_fused = false;
     timed(PH_ATTN, 4.0 * Q * (S + 1) * T, [&] {
-      attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
+      rope_fused = attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
     });
-    timed(PH_ELEM, 0, [&] {
-      kern::rope(dqkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim, cos_t,
-                 sin_t, true, stream);
-    });
+    if (!rope_fused)
+      timed(PH_ELEM, 0, [&] {
+        kern::rope(dqkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim,
+                   cos_t, sin_t, true, stream);
+      });
     run(p_dU);
     run_dw(p_dw_qkv, f_dw_qkv);
     bucket_ready("qkv", "qkv");

@@ -30,6 +30,10 @@ SHAPES = {
     # rescale and the tcgen05 backward's multi-block loops inside the full step)
     "s384": dict(hidden=256, vocab=2048, seq_len=384, n_heads=4, n_kv_heads=2, head_dim=128,
                  ffn=512, micro_batch=2, rms_eps=1e-5, rope_theta=10000.0),
+    # seq_len not a multiple of 128: mma.sync attention fallback, whose backward
+    # leaves the inverse RoPE to the standalone kernel (the tcgen05 one fuses it)
+    "s192": dict(hidden=256, vocab=2048, seq_len=192, n_heads=4, n_kv_heads=2, head_dim=64,
+                ffn=512, micro_batch=3, rms_eps=1e-5, rope_theta=10000.0),
 }
 
 
