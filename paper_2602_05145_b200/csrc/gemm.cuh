@@ -259,6 +259,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::tmem_ld_32x32b_x32(t_row + c, r);
           ptx::tmem_ld_wait();
           const int col0 = n0 + c;
+          if (args.C != nullptr && col0 < args.N) {
+            // fp32 logits kept for the backward (no recompute): staged through
+            // smem so each store instruction writes 4 full 128-byte row segments
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(stg + lane * 36 + i) =
+                  make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                              __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            __syncwarp();
+            const int cl = (lane & 7) * 4;
+            const int col = col0 + cl;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int rl = it * 4 + (lane >> 3);
+              const int rw = row_base + rl;
+              if (rw < args.M && col < args.N)
+                __stcs(reinterpret_cast<float4*>(static_cast<float*>(args.C) +
+                                                 static_cast<long long>(rw) * args.ldc + col),
+                       *reinterpret_cast<const float4*>(stg + rl * 36 + cl));
+            }
+          }
           if (!row_ok || col0 >= args.N) continue;
           const int ncol = min(32, args.N - col0);
           float cmax = -INFINITY;

@@ -19,7 +19,8 @@ enum Epi : int {
   EPI_F32 = 1,         // C(f32)  = acc
   EPI_F32_ACC = 2,     // C(f32) += acc
   EPI_BF16_RESID = 3,  // C(bf16) = acc + R(bf16)
-  EPI_CE_FWD = 4,      // per-row partial (max, sum exp, target logit, argmax) per N tile
+  EPI_CE_FWD = 4,      // per-row partial (max, sum exp, target logit, argmax) per N tile;
+                       // also C(f32) = acc when C is set (logits kept for the backward)
   EPI_CE_BWD = 5,      // C(bf16) = (exp(acc - lse[row]) - [col == y[row]]) * coef[row]
   EPI_ADAMW = 6,       // acc is a weight gradient: fused PyTorch-AdamW update of p/m/v (+ bf16 p)
   EPI_BF16_ROPE = 7,   // C(bf16) = acc with NeoX RoPE applied to columns < rope_cols (q | k heads)

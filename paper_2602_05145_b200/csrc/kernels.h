@@ -65,6 +65,12 @@ void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat1
 // Combine per-N-tile softmax partials into lse / per-row loss / argmax.
 void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,
                const int32_t* m, float* lse, float* row_loss, int32_t* argmax, cudaStream_t s);
+// CE gradient from stored fp32 logits (same arithmetic as the EPI_CE_BWD
+// recompute epilogue): dlog[t, j] = bf16((exp(l[t, v0 + j] - lse[t]) -
+// [v0 + j == y[t]]) * coef[t]) for j < vn.  vn % 8 == 0.
+void ce_grad(const float* logits, long long ldl, const float* lse, const float* coef,
+             const int32_t* y, int v0, long long T, int vn, __nv_bfloat16* dlog, long long ldd,
+             cudaStream_t s);
 // stats[0] = sum row_loss / n_global (double), stats[1] = valid (as double),
 // stats[2] = top-1 correct.  Single block, fixed order.
 void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,

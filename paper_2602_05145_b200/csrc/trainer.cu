@@ -143,6 +143,8 @@ class DraftTrainerImpl {
   long long* n_global;
   double* stats;
   // backward
+  float* logits = nullptr;  // [T, V] fp32 when keep_logits
+  bool keep_logits = false;
   __nv_bfloat16 *dlog, *dh_b, *dact, *dgu, *dr_b, *dO, *dqkv, *dg_b;
   float *dn, *dh, *dz, *dr, *dU, *Dattn, *dw_part;
   // pinned host scalars
@@ -301,6 +303,14 @@ class DraftTrainerImpl {
     arena.reserve(&n_global, 2);
     arena.reserve(&stats, 4);
     arena.reserve(&dlog, T * Vc);
+    // fp32 logits [T, V] kept from the forward so the backward needs no logit
+    // recompute (4.2 GB at C2); SPECSIM_CE_RECOMPUTE=1 or a > 32 GB table
+    // selects the recompute path instead
+    {
+      const char* e = std::getenv("SPECSIM_CE_RECOMPUTE");
+      keep_logits = !(e && e[0] == '1') && T * V * 4 <= (32ll << 30);
+      if (keep_logits) arena.reserve(&logits, T * V);
+    }
     arena.reserve(&dh_b, T * H);
     arena.reserve(&dact, T * I);
     arena.reserve(&dgu, T * 2 * I);
@@ -484,6 +494,10 @@ class DraftTrainerImpl {
     Args ce{};
     ce.targets = y;
     ce.partials = partials;
+    if (keep_logits) {
+      ce.C = logits;
+      ce.ldc = V;
+    }
     p_ce_fwd = make_plan({nrm, H, false}, {pb("lm_head"), H, false}, T, V, H, EPI_CE_FWD, ce);
     // LM head backward, vocabulary chunks
     for (int c = 0; c < n_chunks; ++c) {
@@ -693,11 +707,17 @@ class DraftTrainerImpl {
     const int S = sh.seq_len;
     bucket_next = 0;
     for (int c = 0; c < n_chunks; ++c) {
-      run(p_ce_bwd[c], PH_LM, 0.0);  // logit recompute: not algorithmic work
+      const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
+      if (keep_logits)
+        timed(PH_LM, 0, [&] {
+          kern::ce_grad(logits, V, lse, coef, y, static_cast<int>(v0), T, static_cast<int>(vn),
+                        dlog, Vc, stream);
+        });
+      else
+        run(p_ce_bwd[c], PH_LM, 0.0);  // logit recompute: not algorithmic work
       run(p_lm_dx[c], PH_LM);
       run_dw(p_lm_dw[c], f_lm_dw[c], PH_LM);
       // LM-head rows of this chunk are final: their all-reduce overlaps the rest
-      const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
       bucket_ready("lm_head", "lm_head", vn * H, param("lm_head").off + v0 * H);
     }
     timed(PH_ELEM, 0, [&] {

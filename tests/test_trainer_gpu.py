@@ -270,3 +270,26 @@ def test_partial_batch_matches_oracle():
         o, n = off[nm]
         assert rel(tr.get_grad(nm).reshape(-1), grads[o:o + n]) < 1e-2, nm
     tr.close(); buf.close()
+
+
+@pytest.mark.parametrize("name", ["bigvocab", "gqa128"])
+def test_stored_logits_equal_recompute(name, monkeypatch):
+    """The default backward reads the fp32 logits the forward GEMM stored; the
+    SPECSIM_CE_RECOMPUTE path recomputes them chunk by chunk (EPI_CE_BWD).
+    Both apply the same softmax-gradient arithmetic to the same accumulator
+    values, so the step's loss and every gradient agree to fp32 noise."""
+    c = SHAPES[name]
+    S, B = c["seq_len"], c["micro_batch"]
+    lens = [S + 2] * (B - 1) + [S // 2 + 5]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SPECSIM_CE_RECOMPUTE", mode)
+        c, shp, tr, buf, ids, _ = setup(name, lens)
+        r = tr.step(buf, ids)
+        out[mode] = (r["loss"], {nm: tr.get_grad(nm).copy() for nm in ("lm_head", "fc", "qkv")})
+        tr.close()
+        buf.close()
+    (l0, g0), (l1, g1) = out["0"], out["1"]
+    assert abs(l0 - l1) <= 1e-6 * abs(l1)
+    for nm in g0:
+        assert rel(g0[nm], g1[nm]) <= 1e-5, (nm, rel(g0[nm], g1[nm]))
