@@ -289,8 +289,9 @@ def run_ours(args):
     tr.set_timing(True)
     phase_acc = {p: dict(ms=0.0, flops=0.0, launches=0) for p in api.DraftTrainer.PHASES}
     barrier()
+    prof_step_ms = 0.0
     for k in range(n_prof):
-        tr.step(buf, batch(k))
+        prof_step_ms += tr.step(buf, batch(k))["ms"]
         for p, v in tr.phase_times().items():
             for f in ("ms", "flops", "launches"):
                 phase_acc[p][f] += v[f]
@@ -363,6 +364,11 @@ def run_ours(args):
     phases = {p: dict(ms_per_step=round(v["ms"] / n_prof, 3),
                       launches_per_step=v["launches"] // max(1, n_prof))
               for p, v in phase_acc.items()}
+    # device time of the profiled steps not inside any timed launch (launch
+    # gaps, event nodes, staging copies)
+    phases["untimed_gaps"] = dict(
+        ms_per_step=round((prof_step_ms - sum(v["ms"] for v in phase_acc.values())) / n_prof, 3),
+        launches_per_step=0)
     whole_step_tflops = fl["total"] * T / (step_ms / 1e3) / 1e12
 
     line = dict(metric="draft-train tokens/sec", value=round(value, 1), unit="tokens/s",

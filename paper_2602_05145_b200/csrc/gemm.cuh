@@ -424,15 +424,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // phase 1: every global load of the chunk is issued before any store
           // (loads and stores may alias as far as the compiler knows), so the
           // 8 row groups' DRAM latencies overlap
-          float4 v[8], x1[8], x2[8], x3[8];
-          uint32_t okm = 0;  // bit it: row group it in range
+          // AdamW keeps three state vectors per row group in flight: hoist 4
+          // row groups at a time so everything stays in registers
+          constexpr int RG = EPI == EPI_ADAMW ? 4 : 8;
+#pragma unroll
+          for (int g0 = 0; g0 < 8; g0 += RG) {
+          float4 v[RG], x1[RG], x2[RG], x3[RG];
+          uint32_t okm = 0;  // bit it: row group g0 + it in range
           // element offset of row group it (recomputed: fewer live registers)
-          const long long e0 = static_cast<long long>(row_base + (lane >> 3)) * args.ldc + col;
+          const long long e0 =
+              static_cast<long long>(row_base + 4 * g0 + (lane >> 3)) * args.ldc + col;
           const long long estep = 4 * args.ldc;
 #define SPECSIM_E(it) (e0 + (it) * estep)
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rl = it * 4 + (lane >> 3);
+          for (int it = 0; it < RG; ++it) {
+            const int rl = (g0 + it) * 4 + (lane >> 3);
             const int rr = row_base + rl;
             if (col_ok && rr < args.M) okm |= 1u << it;
             const long long e_it = SPECSIM_E(it);
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           // phase 2: compute and store
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
+          for (int it = 0; it < RG; ++it) {
             if (!(okm >> it & 1)) continue;
             const long long e_it = SPECSIM_E(it);
             float4 w = v[it];
@@ -518,6 +524,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (args.opt_g) __stcs(reinterpret_cast<float4*>(args.opt_g + e_it), w);
             }
           }
+          }  // g0
 #undef SPECSIM_E
         }
       }
