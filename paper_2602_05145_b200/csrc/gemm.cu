@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -175,6 +176,22 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   p.args.group_m = static_cast<int>(gm);
   p.args.group_n = static_cast<int>(gn);
   const int units = num_sms() / cg;  // CTA pairs (or CTAs) resident at once
+  // Long K: when at most two panels of the smaller operand fit the budget the
+  // resident walk degenerates to streaming the larger operand once per one or
+  // two blocks; walk compact waves instead (group_m ~ sqrt(units * b/a) rows).
+  static const int raster = [] {
+    const char* e = std::getenv("SPECSIM_RASTER");  // A/B: "resident" | "wave"
+    if (!e) return 0;
+    return std::string(e) == "resident" ? 1 : (std::string(e) == "wave" ? 2 : 0);
+  }();
+  const long long g_res = p.args.keep_b ? gn : gm;
+  if (raster == 2 || (raster == 0 && g_res <= 2)) {
+    const double w = std::sqrt(static_cast<double>(units) * b_panel / static_cast<double>(a_panel));
+    long long gw = static_cast<long long>(w + 0.5);
+    gw = gw < 1 ? 1 : (gw > p.args.num_m_blocks ? p.args.num_m_blocks : gw);
+    p.args.keep_b = 2;
+    p.args.group_m = static_cast<int>(gw);
+  }
   p.grid = (p.args.num_tiles < units ? p.args.num_tiles : units) * cg;
   p.flops = 2.0 * M * static_cast<double>(N) * K;
   p.prepare();

@@ -54,8 +54,11 @@ __device__ __forceinline__ void tile_coords(int tile, const Args& a, int& mb, in
   // smaller operand is walked in groups of panels that stay L2-resident
   // (loaded evict_last) while the other operand streams through DRAM once
   // per group.  keep_b: groups of group_n column blocks, row blocks inside;
-  // else groups of group_m row blocks, column blocks inside.
-  if (a.keep_b) {
+  // else groups of group_m row blocks, column blocks inside (keep_b == 2:
+  // the same walk for long-K GEMMs whose panels do not fit L2 -- group_m is
+  // chosen so each wave of concurrent tiles is a compact block whose CTAs
+  // share A / B k-slices in L2 while they advance through K together).
+  if (a.keep_b == 1) {
     const int group_size = a.group_n * a.num_m_blocks;
     const int group = tile / group_size;
     const int first_n = group * a.group_n;
@@ -132,8 +135,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       // the operand the rasterisation reuses (see make_plan) is loaded
       // evict_last so streaming outputs / optimizer state do not flush it
-      const uint64_t pol_a = args.keep_b ? ptx::policy_evict_normal() : ptx::policy_evict_last();
-      const uint64_t pol_b = args.keep_b ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+      const uint64_t pol_a =
+          args.keep_b == 0 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+      const uint64_t pol_b =
+          args.keep_b == 1 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
       auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1,
                       uint64_t pol) {
         if constexpr (CG == 2)
