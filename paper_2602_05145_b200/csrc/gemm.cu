@@ -169,8 +169,10 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   p.args.keep_b = b_bytes < a_bytes ? 1 : 0;
   const long long a_panel = static_cast<long long>(tile_m) * K * 2;
   const long long b_panel = static_cast<long long>(BN) * K * 2;
-  long long gm = budget / (a_panel > 0 ? a_panel : 1);
-  long long gn = budget / (b_panel > 0 ? b_panel : 1);
+  const long long bud = extra.l2_budget_mb > 0 ? static_cast<long long>(extra.l2_budget_mb) << 20
+                                               : budget;
+  long long gm = bud / (a_panel > 0 ? a_panel : 1);
+  long long gn = bud / (b_panel > 0 ? b_panel : 1);
   gm = gm < 1 ? 1 : (gm > p.args.num_m_blocks ? p.args.num_m_blocks : gm);
   gn = gn < 1 ? 1 : (gn > p.args.num_n_blocks ? p.args.num_n_blocks : gn);
   p.args.group_m = static_cast<int>(gm);
@@ -184,8 +186,12 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
     if (!e) return 0;
     return std::string(e) == "resident" ? 1 : (std::string(e) == "wave" ? 2 : 0);
   }();
+  static const long long wave_g = [] {
+    const char* e = std::getenv("SPECSIM_RASTER_WAVE_G");  // A/B: resident-group threshold
+    return e ? std::atoll(e) : 2;
+  }();
   const long long g_res = p.args.keep_b ? gn : gm;
-  if (raster == 2 || (raster == 0 && g_res <= 2)) {
+  if (raster == 2 || (raster == 0 && g_res <= wave_g)) {
     const double w = std::sqrt(static_cast<double>(units) * b_panel / static_cast<double>(a_panel));
     long long gw = static_cast<long long>(w + 0.5);
     gw = gw < 1 ? 1 : (gw > p.args.num_m_blocks ? p.args.num_m_blocks : gw);

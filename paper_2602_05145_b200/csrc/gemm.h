@@ -56,6 +56,7 @@ struct Args {
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;  // rasterisation group (row blocks), used when keep_b == 0
   int group_n;  // rasterisation group (column blocks), used when keep_b == 1
+  int l2_budget_mb;  // host hint for make_plan: resident-panel budget (0: default)
   int keep_b;   // 1: B panels are the L2-resident operand, 0: A panels, 2: compact waves (long K)
   // fused AdamW epilogue: parameter tensors laid out like C (ldc)
   float *opt_p, *opt_m, *opt_v;

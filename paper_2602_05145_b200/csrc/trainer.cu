@@ -498,6 +498,7 @@ class DraftTrainerImpl {
       ce.C = logits;
       ce.ldc = V;
     }
+    if (const char* e = std::getenv("SPECSIM_CE_L2_MB")) ce.l2_budget_mb = std::atoi(e);
     p_ce_fwd = make_plan({nrm, H, false}, {pb("lm_head"), H, false}, T, V, H, EPI_CE_FWD, ce);
     // LM head backward, vocabulary chunks
     for (int c = 0; c < n_chunks; ++c) {
