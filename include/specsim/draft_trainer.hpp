@@ -173,11 +173,89 @@ class DraftTrainer {
   StepResult step(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid);
   StepResult eval(HiddenStateBuffer& buf, const int64_t* ids, int n);
   TrainingOutcome train(HiddenStateBuffer& buf, const TrainJob& job);
+  // Deploy gate support: device copy of the model (fp32 master, bf16 copy,
+  // AdamW m / v, step count) and its restore (M_draft kept when M_new is not
+  // deployed).
+  void snapshot();
+  void restore();
   DraftTrainerImpl& impl() { return *impl_; }
   const DraftTrainerImpl& impl() const { return *impl_; }
 
  private:
   std::unique_ptr<DraftTrainerImpl> impl_;
+};
+
+// ------------------------------------------------------------ controller
+// Algorithm 1 (SPEC.md adapt_control): dual-EMA collection
+// gate, sample store, and maybe_trigger_training -- the caller of train(job)
+// -- with the deploy-if-improved gate.  Host logic in double precision, same
+// operation order as the SPEC recurrences (bit-reproducible).
+struct ControllerConfig {
+  double lambda_short = 0.9;  // SPEC adapt_control DESIGN DECISIONS defaults
+  double lambda_long = 0.99;
+  double epsilon = 0.05;
+  int32_t n_init = 32;
+  int64_t n_threshold = 2048;
+  void validate() const;  // throws ConfigError (every problem in one message)
+};
+
+enum class ControllerEventKind : int32_t {
+  COLLECT_ON = 0,
+  COLLECT_OFF = 1,
+  TRAIN_TRIGGER = 2,
+  DEPLOY = 3,
+  REJECT = 4,
+};
+struct ControllerEvent {
+  ControllerEventKind kind;
+  int64_t observation;  // observations seen when it happened (the clock of this API)
+};
+
+struct TriggerDecision {
+  bool triggered = false;
+  TrainingOutcome outcome;
+  double alpha_train = 0;  // mean alpha label of D_train, sequential order
+  int64_t n_train = 0, n_eval = 0;
+  int32_t action = -1;     // 1 deploy, 0 tie (neither), -1 reject / not triggered
+};
+
+class AdaptiveController {
+ public:
+  explicit AdaptiveController(const ControllerConfig& cfg);
+  // Warm-up: the first n_init observations initialise both EMAs to their mean
+  // (init_from_warmup); afterwards Eq. 6 plus the epsilon-gap gate.
+  void observe(double alpha);
+  // Store (h, alpha) when collection is enabled; returns whether it was stored.
+  bool record_sample(int64_t sample_id, double alpha);
+  // At >= n_threshold stored samples: chronological 9:1 split, train, deploy
+  // if alpha_eval > alpha_train, disable collection if <, neither on a tie;
+  // pending set cleared.  A throwing trainer leaves state, pending set and the
+  // model unchanged (the exception propagates).
+  TriggerDecision maybe_trigger_training(DraftTrainer& trainer, HiddenStateBuffer& buf,
+                                         int epochs = 1);
+
+  const ControllerConfig& config() const { return cfg_; }
+  bool initialized() const { return initialized_; }
+  double ema_short() const { return ema_short_; }
+  double ema_long() const { return ema_long_; }
+  bool collection_enabled() const { return collection_enabled_; }
+  int64_t stored_samples() const { return static_cast<int64_t>(pending_ids_.size()); }
+  int64_t draft_version() const { return draft_version_; }
+  int64_t observations() const { return observations_; }
+  const std::vector<ControllerEvent>& events() const { return events_; }
+  const std::vector<int64_t>& pending_ids() const { return pending_ids_; }
+
+ private:
+  ControllerConfig cfg_;
+  bool initialized_ = false;
+  std::vector<double> warmup_;
+  double ema_short_ = 0, ema_long_ = 0;
+  bool collection_enabled_ = false;
+  std::vector<int64_t> pending_ids_;
+  std::vector<double> pending_alpha_;
+  int64_t draft_version_ = 0;
+  int64_t observations_ = 0;
+  std::vector<ControllerEvent> events_;
 };
 
 }  // namespace specsim

@@ -234,6 +234,55 @@ int specsim_trainer_train(specsim_trainer* t, specsim_hsbuf* buf, const int64_t*
                           int64_t n_train, const int64_t* eval_ids, int64_t n_eval,
                           int32_t epochs, specsim_training_outcome* out);
 
+/* ---------------------------------------------------------- deploy gate
+ * Device snapshot / restore of the model (fp32 master, bf16 working copy,
+ * AdamW m / v, step count): M_draft is kept when M_new is not deployed
+ * (PAPER.md:209-213).  restore without a snapshot -> SPECSIM_EDOMAIN. */
+int specsim_trainer_snapshot(specsim_trainer* t);
+int specsim_trainer_restore(specsim_trainer* t);
+
+/* ------------------------------------------------- adaptive controller
+ * Algorithm 1 (SPEC.md adapt_control): the caller of
+ * train(job).  observe() = Eq. 6 dual EMA + epsilon-gap collection gate
+ * (first n_init observations initialise both EMAs to their mean);
+ * record_sample() = "Store (h, alpha)" (no-op when collection is off);
+ * maybe_trigger_training() = SPEC.md:345-353: at >= n_threshold stored
+ * samples, chronological 9:1 split, alpha_train = mean alpha of D_train,
+ * train, deploy iff alpha_eval > alpha_train (version + 1), disable
+ * collection iff alpha_eval < alpha_train, neither on a tie; the model is
+ * restored unless deployed; pending set cleared.  A failing trainer leaves
+ * controller state, pending set and model unchanged. */
+typedef struct specsim_controller specsim_controller;
+typedef struct specsim_controller_config {
+  double lambda_short, lambda_long, epsilon;
+  int32_t n_init;
+  int64_t n_threshold;
+} specsim_controller_config;
+typedef struct specsim_controller_state {
+  int32_t initialized, collection_enabled;
+  double ema_short, ema_long;
+  int64_t stored_samples, draft_version, observations, n_events;
+} specsim_controller_state;
+typedef struct specsim_trigger_decision {
+  int32_t triggered, action; /* action: 1 deploy, 0 tie, -1 reject / not triggered */
+  double alpha_train;
+  int64_t n_train, n_eval;
+  specsim_training_outcome outcome;
+} specsim_trigger_decision;
+/* event kinds: 0 COLLECT_ON, 1 COLLECT_OFF, 2 TRAIN_TRIGGER, 3 DEPLOY, 4 REJECT */
+int specsim_controller_create(const specsim_controller_config* cfg, specsim_controller** out);
+void specsim_controller_destroy(specsim_controller* c);
+int specsim_controller_observe(specsim_controller* c, double alpha);
+int specsim_controller_record_sample(specsim_controller* c, int64_t sample_id, double alpha,
+                                     int32_t* stored);
+int specsim_controller_maybe_trigger_training(specsim_controller* c, specsim_trainer* t,
+                                              specsim_hsbuf* buf, int32_t epochs,
+                                              specsim_trigger_decision* out);
+int specsim_controller_state_get(const specsim_controller* c, specsim_controller_state* out);
+/* copies up to cap events (kind, observation index); *n = total events */
+int specsim_controller_events(const specsim_controller* c, int32_t* kinds, int64_t* at,
+                              int64_t cap, int64_t* n);
+
 /* Parameter registry (fp32 master copies; names: fc, w_in, w_hid, qkv, o,
  * w_post, gate_up, down, w_fin, lm_head).  Frozen embedding: "embed". */
 int specsim_trainer_num_params(const specsim_trainer* t, int32_t* count, int64_t* total_elems);

@@ -65,6 +65,23 @@ class TrainingOutcome(C.Structure):
                 ("new_version", C.c_int64), ("mean_loss", C.c_double), ("steps", C.c_int64)]
 
 
+class ControllerConfig(C.Structure):
+    _fields_ = [("lambda_short", C.c_double), ("lambda_long", C.c_double),
+                ("epsilon", C.c_double), ("n_init", C.c_int32), ("n_threshold", C.c_int64)]
+
+
+class ControllerState(C.Structure):
+    _fields_ = [("initialized", C.c_int32), ("collection_enabled", C.c_int32),
+                ("ema_short", C.c_double), ("ema_long", C.c_double),
+                ("stored_samples", C.c_int64), ("draft_version", C.c_int64),
+                ("observations", C.c_int64), ("n_events", C.c_int64)]
+
+
+class TriggerDecision(C.Structure):
+    _fields_ = [("triggered", C.c_int32), ("action", C.c_int32), ("alpha_train", C.c_double),
+                ("n_train", C.c_int64), ("n_eval", C.c_int64), ("outcome", TrainingOutcome)]
+
+
 P = C.c_void_p
 I32, I64, U64, F32, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
 PI32, PI64, PU64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)
@@ -115,6 +132,15 @@ SIGNATURES = {
     "specsim_trainer_set_timing": [P, C.c_int],
     "specsim_trainer_region": [P, C.c_int, PF64],
     "specsim_trainer_phase_times": [P, PF64, PF64, PI32],
+    "specsim_trainer_snapshot": [P],
+    "specsim_trainer_restore": [P],
+    "specsim_controller_create": [C.POINTER(ControllerConfig), C.POINTER(P)],
+    "specsim_controller_destroy": [P],
+    "specsim_controller_observe": [P, F64],
+    "specsim_controller_record_sample": [P, I64, F64, PI32],
+    "specsim_controller_maybe_trigger_training": [P, P, P, I32, C.POINTER(TriggerDecision)],
+    "specsim_controller_state_get": [P, C.POINTER(ControllerState)],
+    "specsim_controller_events": [P, PI32, PI64, I64, PI64],
     "specsim_debug_gemm": [C.c_int, C.c_int, C.c_int, I32, I32, I32, P, I64, P, I64, P, I64, P,
                            I64, I32, PF32],
     "specsim_debug_attention": [I32, I32, I32, I32, I32, P, P, P, P, P],

@@ -311,6 +311,13 @@ class DraftTrainer:
     def set_step_count(self, k):
         call("specsim_trainer_set_step_count", self.h, k)
 
+    def snapshot(self):
+        """Device copy of the model (deploy gate)."""
+        call("specsim_trainer_snapshot", self.h)
+
+    def restore(self):
+        call("specsim_trainer_restore", self.h)
+
     def region_begin(self):
         call("specsim_trainer_region", self.h, 0, None)
 
@@ -328,3 +335,67 @@ class DraftTrainer:
         ln = (C.c_int32 * 7)()
         call("specsim_trainer_phase_times", self.h, ms, fl, ln)
         return {p: dict(ms=ms[i], flops=fl[i], launches=ln[i]) for i, p in enumerate(self.PHASES)}
+
+
+# ---------------------------------------------------------------- controller
+EVENT_NAMES = ("COLLECT_ON", "COLLECT_OFF", "TRAIN_TRIGGER", "DEPLOY", "REJECT")
+
+
+@dataclass
+class TriggerDecision:
+    triggered: bool
+    action: int  # 1 deploy, 0 tie, -1 reject / not triggered
+    alpha_train: float
+    n_train: int
+    n_eval: int
+    outcome: TrainingOutcome | None
+
+
+class AdaptiveController:
+    """Algorithm 1 (SPEC.md adapt_control) over the C ABI:
+    observe() / record_sample() / maybe_trigger_training(trainer, buf)."""
+
+    def __init__(self, lambda_short=0.9, lambda_long=0.99, epsilon=0.05, n_init=32,
+                 n_threshold=2048):
+        cfg = _lib.ControllerConfig(lambda_short, lambda_long, epsilon, n_init, n_threshold)
+        self.h = C.c_void_p()
+        call("specsim_controller_create", C.byref(cfg), C.byref(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_controller_destroy(self.h)
+        self.h = None
+
+    __del__ = close
+
+    def observe(self, alpha: float):
+        call("specsim_controller_observe", self.h, alpha)
+
+    def record_sample(self, sample_id: int, alpha: float) -> bool:
+        s = C.c_int32()
+        call("specsim_controller_record_sample", self.h, sample_id, alpha, C.byref(s))
+        return bool(s.value)
+
+    def maybe_trigger_training(self, trainer: "DraftTrainer", buf: HiddenStateBuffer,
+                               epochs: int = 1) -> TriggerDecision:
+        d = _lib.TriggerDecision()
+        call("specsim_controller_maybe_trigger_training", self.h, trainer.h, buf.h, epochs,
+             C.byref(d))
+        o = d.outcome
+        out = TrainingOutcome(o.duration_hours, o.alpha_eval, o.new_version, o.mean_loss,
+                              o.steps) if d.triggered else None
+        return TriggerDecision(bool(d.triggered), d.action, d.alpha_train, d.n_train, d.n_eval,
+                               out)
+
+    def state(self) -> dict:
+        s = _lib.ControllerState()
+        call("specsim_controller_state_get", self.h, C.byref(s))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def events(self):
+        n = C.c_int64()
+        call("specsim_controller_events", self.h, None, None, 0, C.byref(n))
+        k = (C.c_int32 * max(1, n.value))()
+        t = (C.c_int64 * max(1, n.value))()
+        call("specsim_controller_events", self.h, k, t, n.value, C.byref(n))
+        return [(EVENT_NAMES[k[i]], t[i]) for i in range(n.value)]

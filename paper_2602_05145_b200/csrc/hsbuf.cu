@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include "common.h"
+#include "handles.h"
 #include "kernels.h"
 #include "specsim/draft_trainer.hpp"
 
@@ -300,9 +301,6 @@ void HiddenStateBuffer::read_sample(int64_t id, uint16_t* features, int32_t* ids
 // ================================================================== C ABI
 using namespace specsim;
 
-struct specsim_hsbuf {
-  HiddenStateBuffer* b;
-};
 
 extern "C" {
 

@@ -21,6 +21,7 @@
 
 #include "attention.h"
 #include "common.h"
+#include "handles.h"
 #include "gemm.h"
 #include "kernels.h"
 #include "nccl_dyn.h"
@@ -117,6 +118,9 @@ class DraftTrainerImpl {
   int64_t step_count = 0;
   int64_t version = 0;
   bool timing = false;
+  // deploy gate: device copy of the model [P | Mst | Vst] fp32 + P16 bf16
+  void* snap = nullptr;
+  int64_t snap_step = -1;
   double phase_ms[PH_N] = {}, phase_flops[PH_N] = {};
   int phase_launches[PH_N] = {};
 
@@ -366,6 +370,7 @@ class DraftTrainerImpl {
   ~DraftTrainerImpl() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (snap) cudaFree(snap);
     if (comm_stream) cudaStreamSynchronize(comm_stream);
     if (comm) nccl::api().CommDestroy(comm);
     for (auto e : bucket_events) cudaEventDestroy(e);
@@ -773,6 +778,33 @@ class DraftTrainerImpl {
     }
   }
 
+  void snapshot() {
+    SPECSIM_CUDA(cudaSetDevice(device));
+    const size_t f = sizeof(float) * static_cast<size_t>(total);
+    if (!snap) SPECSIM_CUDA(cudaMalloc(&snap, 3 * f + sizeof(__nv_bfloat16) * total));
+    char* s = static_cast<char*>(snap);
+    SPECSIM_CUDA(cudaMemcpyAsync(s, P, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(s + f, Mst, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(s + 2 * f, Vst, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(s + 3 * f, P16, sizeof(__nv_bfloat16) * total,
+                                 cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    snap_step = step_count;
+  }
+  void restore() {
+    if (snap_step < 0) throw std::invalid_argument("restore: no snapshot taken");
+    SPECSIM_CUDA(cudaSetDevice(device));
+    const size_t f = sizeof(float) * static_cast<size_t>(total);
+    const char* s = static_cast<const char*>(snap);
+    SPECSIM_CUDA(cudaMemcpyAsync(P, s, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(Mst, s + f, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(Vst, s + 2 * f, f, cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaMemcpyAsync(P16, s + 3 * f, sizeof(__nv_bfloat16) * total,
+                                 cudaMemcpyDeviceToDevice, stream));
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    step_count = snap_step;
+  }
+
   kern::AdamHyper next_hyper() const {
     const int64_t k = step_count + 1;
     const double bc1 = 1.0 - std::pow(static_cast<double>(opt.beta1), static_cast<double>(k));
@@ -1038,15 +1070,14 @@ StepResult DraftTrainer::eval(HiddenStateBuffer& buf, const int64_t* ids, int n)
 TrainingOutcome DraftTrainer::train(HiddenStateBuffer& buf, const TrainJob& job) {
   return impl_->train(buf, job);
 }
+void DraftTrainer::snapshot() { impl_->snapshot(); }
+void DraftTrainer::restore() { impl_->restore(); }
 
 }  // namespace specsim
 
 // ================================================================== C ABI
 using namespace specsim;
 
-struct specsim_trainer {
-  DraftTrainer* t;
-};
 
 namespace {
 DraftTrainerImpl& impl_of(const specsim_trainer* t) {
@@ -1229,6 +1260,12 @@ int specsim_trainer_get_embedding(const specsim_trainer* t, uint16_t* host_bf16)
   });
 }
 
+int specsim_trainer_snapshot(specsim_trainer* t) {
+  return guard([&] { t->t->snapshot(); });
+}
+int specsim_trainer_restore(specsim_trainer* t) {
+  return guard([&] { t->t->restore(); });
+}
 int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step) {
   return guard([&] {
     if (step < 0) throw std::invalid_argument("step must be >= 0");
