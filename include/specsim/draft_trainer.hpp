@@ -163,6 +163,69 @@ struct TrainingOutcome {
   int64_t steps = 0;
 };
 
+// ------------------------------------------------------- capture side
+// Serving-GPU side of the signal path (PAPER.md:130,
+// SPEC.md:267-275, 293): each verify step's accepted-token hidden states of
+// the tapped layers are packed on the device (on the serving stream: one
+// small kernel) and copied D2H on the capture's own stream into a pinned
+// host segment, so the copy overlaps the next verification step.  When the
+// buffered bytes exceed the flush threshold (64 MiB default; SPEC
+// accounting: n x bytes_per_token, ids not counted) the segment is handed to
+// a writer thread that persists it as one shard file while capture continues
+// into the other segment.  Shard format ("TIDESIG1"):
+//   header  : char magic[8] = "TIDESIG1"; u32 version = 1; u32 layers;
+//             u32 hidden; u32 bytes_per_element = 2; u64 n_records;
+//             u64 payload_bytes                                  (40 B)
+//   record  : i64 sample_id; f64 alpha; i32 n; i32 width (= layers*hidden);
+//             i64 flags (1 = sample complete); bf16 features[n][width];
+//             i32 ids[n]; zero padding to 16 B
+//   batch record (flags 2, capture_batch): sample_id = -1, alpha = n_req,
+//             n = total rows; i64 sample_ids[n_req]; i32 counts[n_req];
+//             zero padding to 16 B; bf16 features[n][width]; i32 ids[n];
+//             zero padding to 16 B
+// A request's rows may be split over several records (one per verify step,
+// interleaved with other requests of the batch); end_sample() writes its
+// final alpha label.  load_shards() regroups records per sample.
+class SignalCapture {
+ public:
+  struct Stats {
+    int64_t records = 0, bytes = 0, flushes = 0, cumulative_bytes = 0;  // SPEC accounting
+    int64_t samples = 0, files = 0, file_bytes = 0;
+  };
+  SignalCapture(const SignalGeometry& g, const std::string& directory, int64_t flush_threshold,
+                int device);
+  ~SignalCapture();  // close()
+  SignalCapture(const SignalCapture&) = delete;
+  SignalCapture& operator=(const SignalCapture&) = delete;
+
+  // layer_ptrs[l]: device [rows, ld] bf16 hidden states of tapped layer l,
+  // valid on `stream` (the serving stream) at the time of the call; host
+  // token_ids[n] and accepted_idx[n] (NULL = rows 0..n).  Returns without
+  // waiting for the copy.
+  void capture(int64_t sample_id, const void* const* layer_ptrs, int64_t rows, int64_t ld,
+               const int32_t* token_ids, const int32_t* accepted_idx, int n, void* stream);
+  // One serving iteration for the whole batch (one pack kernel, one D2H):
+  // request r's accepted rows are accepted_rows[offsets[r] .. offsets[r+1])
+  // of the [rows, ld] layer matrices, token_ids likewise.
+  void capture_batch(const int64_t* sample_ids, int n_req, const int32_t* offsets,
+                     const int32_t* accepted_rows, const void* const* layer_ptrs, int64_t rows,
+                     int64_t ld, const int32_t* token_ids, void* stream);
+  void end_sample(int64_t sample_id, double alpha);  // record_sample: final alpha label
+  void flush();  // persist the buffered records now (extra shard, not a SPEC flush)
+  void close();  // flush + join the writer; idempotent
+  Stats stats() const;
+  std::vector<std::string> files() const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+// Loads shard files (in order) into the device ring: records are regrouped
+// per sample_id (first-appearance order) and each sample appended
+// contiguously.  Returns the number of samples loaded.
+int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& paths);
+
 class DraftTrainerImpl;
 
 class DraftTrainer {

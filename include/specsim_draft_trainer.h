@@ -163,6 +163,42 @@ int specsim_hsbuf_sample_info(const specsim_hsbuf* buf, int64_t sample_id, int32
 int specsim_hsbuf_read_sample(const specsim_hsbuf* buf, int64_t sample_id, uint16_t* features,
                               int32_t* token_ids);
 
+/* ------------------------------------------------------- capture side
+ * Serving-GPU capture (PAPER.md:130, SPEC.md:267-275,
+ * 293): pack accepted-token states on the serving stream, D2H on a side
+ * stream into pinned segments, flush to "TIDESIG1" shard files in
+ * `directory` on a writer thread at the flush threshold (<= 0: 64 MiB).
+ * See include/specsim/draft_trainer.hpp for the file format. */
+typedef struct specsim_capture specsim_capture;
+typedef struct specsim_capture_stats {
+  int64_t records, bytes, flushes, cumulative_bytes; /* SPEC extract_signals accounting */
+  int64_t samples, files, file_bytes;
+} specsim_capture_stats;
+int specsim_capture_create(const specsim_signal_geometry* geometry, const char* directory,
+                           int64_t flush_threshold_bytes, int device, specsim_capture** out);
+/* closes (flushes, joins the writer) and frees */
+int specsim_capture_destroy(specsim_capture* c);
+/* layer_ptrs: device pointers valid on `stream` (cudaStream_t, NULL = legacy
+ * default stream); token_ids / accepted_idx: host arrays read during the call. */
+int specsim_capture_append(specsim_capture* c, int64_t sample_id, const void* const* layer_ptrs,
+                           int64_t rows, int64_t ld, const int32_t* token_ids,
+                           const int32_t* accepted_idx, int32_t n, void* stream);
+/* one serving iteration for a batch: request r's accepted rows are
+ * accepted_rows[offsets[r] .. offsets[r+1]) (offsets has n_req + 1 entries) */
+int specsim_capture_append_batch(specsim_capture* c, const int64_t* sample_ids, int32_t n_req,
+                                 const int32_t* offsets, const int32_t* accepted_rows,
+                                 const void* const* layer_ptrs, int64_t rows, int64_t ld,
+                                 const int32_t* token_ids, void* stream);
+int specsim_capture_end_sample(specsim_capture* c, int64_t sample_id, double alpha);
+int specsim_capture_flush(specsim_capture* c);
+int specsim_capture_close(specsim_capture* c);
+int specsim_capture_stats_get(const specsim_capture* c, specsim_capture_stats* out);
+/* path of shard i (i < files) into buf (cap bytes, NUL-terminated) */
+int specsim_capture_file(const specsim_capture* c, int64_t i, char* buf, int64_t cap);
+/* load shard files into a device ring; *samples = samples appended */
+int specsim_hsbuf_load_shards(specsim_hsbuf* buf, const char* const* paths, int32_t n_paths,
+                              int64_t* samples);
+
 /* ---------------------------------------------------------- draft trainer */
 /* EAGLE-3 style draft head:
  *   g = W_fc f, u = [RMSNorm(E[x_{t+1}]); RMSNorm(g)], one decoder layer

@@ -65,6 +65,12 @@ class TrainingOutcome(C.Structure):
                 ("new_version", C.c_int64), ("mean_loss", C.c_double), ("steps", C.c_int64)]
 
 
+class CaptureStats(C.Structure):
+    _fields_ = [("records", C.c_int64), ("bytes", C.c_int64), ("flushes", C.c_int64),
+                ("cumulative_bytes", C.c_int64), ("samples", C.c_int64), ("files", C.c_int64),
+                ("file_bytes", C.c_int64)]
+
+
 class ControllerConfig(C.Structure):
     _fields_ = [("lambda_short", C.c_double), ("lambda_long", C.c_double),
                 ("epsilon", C.c_double), ("n_init", C.c_int32), ("n_threshold", C.c_int64)]
@@ -132,6 +138,16 @@ SIGNATURES = {
     "specsim_trainer_set_timing": [P, C.c_int],
     "specsim_trainer_region": [P, C.c_int, PF64],
     "specsim_trainer_phase_times": [P, PF64, PF64, PI32],
+    "specsim_capture_create": [C.POINTER(SignalGeometry), C.c_char_p, I64, C.c_int, C.POINTER(P)],
+    "specsim_capture_destroy": [P],
+    "specsim_capture_append": [P, I64, C.POINTER(P), I64, I64, P, P, I32, P],
+    "specsim_capture_append_batch": [P, P, I32, P, P, C.POINTER(P), I64, I64, P, P],
+    "specsim_capture_end_sample": [P, I64, F64],
+    "specsim_capture_flush": [P],
+    "specsim_capture_close": [P],
+    "specsim_capture_stats_get": [P, C.POINTER(CaptureStats)],
+    "specsim_capture_file": [P, I64, C.c_char_p, I64],
+    "specsim_hsbuf_load_shards": [P, C.POINTER(C.c_char_p), I32, PI64],
     "specsim_trainer_snapshot": [P],
     "specsim_trainer_restore": [P],
     "specsim_controller_create": [C.POINTER(ControllerConfig), C.POINTER(P)],

@@ -180,6 +180,13 @@ class HiddenStateBuffer:
         ids = np.ascontiguousarray(token_ids, np.int32)
         call("specsim_hsbuf_append_packed", self.h, sample_id, alpha, ptr(f), ptr(ids), len(ids), 0)
 
+    def load_shards(self, paths) -> int:
+        """Append the samples of TIDESIG1 shard files (SignalCapture output)."""
+        arr = (C.c_char_p * max(1, len(paths)))(*[str(p).encode() for p in paths])
+        n = C.c_int64()
+        call("specsim_hsbuf_load_shards", self.h, arr, len(paths), C.byref(n))
+        return n.value
+
     def stats(self) -> dict:
         s = _lib.HsbufStats()
         call("specsim_hsbuf_stats_get", self.h, C.byref(s))
@@ -198,6 +205,76 @@ class HiddenStateBuffer:
         ids = np.zeros(n, np.int32)
         call("specsim_hsbuf_read_sample", self.h, sample_id, ptr(f), ptr(ids))
         return f, ids
+
+
+class SignalCapture:
+    """Serving-side capture: pack on the serving stream,
+    D2H into pinned segments on a side stream, TIDESIG1 shards at the flush
+    threshold.  Layer arguments are device pointers (ints) valid on `stream`
+    (a cudaStream_t as int; 0 = legacy default stream)."""
+
+    def __init__(self, geometry: SignalGeometry, directory, flush_threshold: int = 0,
+                 device: int = 0):
+        self.geometry = geometry
+        self.h = C.c_void_p()
+        g = geometry.c()
+        call("specsim_capture_create", C.byref(g), str(directory).encode(), flush_threshold,
+             device, C.byref(self.h))
+
+    def append(self, sample_id, layer_ptrs, rows, ld, token_ids, accepted_idx=None, stream=0):
+        arr = (C.c_void_p * len(layer_ptrs))(*layer_ptrs)
+        ids = np.ascontiguousarray(token_ids, np.int32)
+        idx = None if accepted_idx is None else np.ascontiguousarray(accepted_idx, np.int32)
+        call("specsim_capture_append", self.h, sample_id, C.cast(arr, C.POINTER(C.c_void_p)),
+             rows, ld, ptr(ids), ptr(idx), len(ids), stream)
+
+    def append_batch(self, sample_ids, counts, accepted_rows, layer_ptrs, rows, ld, token_ids,
+                     stream=0):
+        """One serving iteration: request r's accepted rows are the next counts[r]
+        entries of accepted_rows (rows of the [rows, ld] layer matrices)."""
+        sid = np.ascontiguousarray(sample_ids, np.int64)
+        off = np.zeros(len(sid) + 1, np.int32)
+        off[1:] = np.cumsum(np.asarray(counts, np.int64))
+        acc = np.ascontiguousarray(accepted_rows, np.int32)
+        ids = np.ascontiguousarray(token_ids, np.int32)
+        arr = (C.c_void_p * len(layer_ptrs))(*layer_ptrs)
+        call("specsim_capture_append_batch", self.h, ptr(sid), len(sid), ptr(off), ptr(acc),
+             C.cast(arr, C.POINTER(C.c_void_p)), rows, ld, ptr(ids), stream)
+
+    def end_sample(self, sample_id, alpha):
+        call("specsim_capture_end_sample", self.h, sample_id, alpha)
+
+    def flush(self):
+        call("specsim_capture_flush", self.h)
+
+    def stats(self) -> dict:
+        s = _lib.CaptureStats()
+        call("specsim_capture_stats_get", self.h, C.byref(s))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def files(self):
+        out = []
+        b = C.create_string_buffer(4096)
+        for i in range(self.stats()["files"]):
+            call("specsim_capture_file", self.h, i, b, 4096)
+            out.append(b.value.decode())
+        return out
+
+    def close(self):
+        """Flush, join the writer; returns the shard paths."""
+        if getattr(self, "h", None) is None:
+            return []
+        call("specsim_capture_close", self.h)
+        files = self.files()
+        if _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_capture_destroy(self.h)
+        self.h = None
+        return files
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.specsim_capture_destroy(self.h)
+            self.h = None
 
 
 # ---------------------------------------------------------------- trainer
