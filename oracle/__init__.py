@@ -25,7 +25,8 @@ class RngState(C.Structure):
 class Shape(C.Structure):
     _fields_ = [("H", C.c_int), ("V", C.c_int), ("S", C.c_int), ("nh", C.c_int),
                 ("nkv", C.c_int), ("hd", C.c_int), ("I", C.c_int), ("layers", C.c_int),
-                ("B", C.c_int), ("eps", C.c_float), ("theta", C.c_double)]
+                ("B", C.c_int), ("eps", C.c_float), ("theta", C.c_double), ("ttt", C.c_int),
+                ("ttt_decay", C.c_float)]
 
 
 class StepOut(C.Structure):
@@ -177,8 +178,13 @@ def synth_capture(seed, index, length, vocab, hidden, layers=3, alpha=0.6, gamma
                 alpha_s=a_s.value)
 
 
-def make_shape(H, V, S, nh, nkv, hd, I, B, layers=3, eps=1e-5, theta=10000.0):
-    return Shape(H, V, S, nh, nkv, hd, I, layers, B, eps, theta)
+def make_shape(H, V, S, nh, nkv, hd, I, B, layers=3, eps=1e-5, theta=10000.0, ttt=1,
+               ttt_decay=0.8):
+    return Shape(H, V, S, nh, nkv, hd, I, layers, B, eps, theta, ttt, ttt_decay)
+
+
+def ttt_of(shape):
+    return max(1, shape.ttt)
 
 
 def param_layout(shape):
@@ -224,10 +230,11 @@ def bf16_to_f32(b):
 
 
 def gather_batch(shape, samples):
-    """samples: list of (ids int32[L], feats uint16[L, 3H]); len <= B."""
-    T = shape.B * shape.S
+    """samples: list of (ids int32[L], feats uint16[L, 3H]); len <= B.
+    u / y / m hold ttt slices of B*S rows (slice j shifted by j tokens)."""
+    T = shape.B * shape.S * ttt_of(shape)
     W = shape.layers * shape.H
-    F = np.zeros((T, W), np.uint16)
+    F = np.zeros((shape.B * shape.S, W), np.uint16)
     u = np.zeros(T, np.int32)
     y = np.zeros(T, np.int32)
     m = np.zeros(T, np.int32)
@@ -257,11 +264,12 @@ def train_step(shape, adamw, step_k, params, mst, vst, E, F, u, y, m, global_val
 
 def forward(shape, params, E, F, u, y, m, global_valid=0, round_bf16=True):
     out = StepOut()
-    T = shape.B * shape.S
+    T = shape.B * shape.S * ttt_of(shape)
     lse = np.zeros(T, np.float32)
     am = np.zeros(T, np.int32)
-    lib().orc_forward(C.byref(shape), _p(params), _p(E), _p(F), _p(u), _p(y), _p(m),
-                      global_valid, 1 if round_bf16 else 0, C.byref(out), _p(lse), _p(am))
+    if lib().orc_forward(C.byref(shape), _p(params), _p(E), _p(F), _p(u), _p(y), _p(m),
+                         global_valid, 1 if round_bf16 else 0, C.byref(out), _p(lse), _p(am)):
+        raise ValueError("bad shape")
     return out, lse, am
 
 

@@ -42,10 +42,14 @@ int64_t orc_param_layout(const orc_shape* s, const char** names, int64_t* rows, 
 }
 
 /* ========================================================= batch assembly */
+static int ttt_of(const orc_shape* s) { return s->ttt > 0 ? s->ttt : 1; }
+static float decay_of(const orc_shape* s) { return s->ttt_decay > 0.f ? s->ttt_decay : 0.8f; }
+
 void orc_gather_batch(const orc_shape* s, int nsamples, const int32_t* const* ids,
                       const uint16_t* const* feats, const int32_t* lens, uint16_t* F,
                       int32_t* u, int32_t* y, int32_t* m) {
-  const int64_t w = (int64_t)s->layers * s->H;
+  const int64_t w = (int64_t)s->layers * s->H, T = (int64_t)s->B * s->S;
+  const int K = ttt_of(s);
   for (int b = 0; b < s->B; ++b) {
     const int L = b < nsamples ? lens[b] : 0;
     for (int t = 0; t < s->S; ++t) {
@@ -54,9 +58,12 @@ void orc_gather_batch(const orc_shape* s, int nsamples, const int32_t* const* id
         memcpy(F + row * w, feats[b] + (int64_t)t * w, (size_t)w * 2);
       else
         memset(F + row * w, 0, (size_t)w * 2);
-      u[row] = (t + 1 < L) ? ids[b][t + 1] : 0;
-      y[row] = (t + 2 < L) ? ids[b][t + 2] : 0;
-      m[row] = (t + 2 < L) ? 1 : 0;
+      for (int j = 0; j < K; ++j) {
+        const int64_t r = (int64_t)j * T + row;
+        u[r] = (t + 1 + j < L) ? ids[b][t + 1 + j] : 0;
+        y[r] = (t + 2 + j < L) ? ids[b][t + 2 + j] : 0;
+        m[r] = (t + 2 + j < L) ? 1 : 0;
+      }
     }
   }
 }
@@ -162,10 +169,11 @@ static void mm_nn(int64_t M, int64_t Kp, int64_t Np, const float* A, int64_t lda
   mm_gen(M, Kp, Np, A, lda, 0, B, ldb, 1, C, ldc, accumulate);
 }
 
-/* C[N,K] = A[T,N]^T . X[T,K]  (weight-gradient form) */
+/* C[N,K] (+)= A[T,N]^T . X[T,K]  (weight-gradient form; accumulates over
+ * the unroll steps of a training-time-test step) */
 static void mm_tn(int64_t N, int64_t K, int64_t T, const float* A, int64_t lda, const float* X,
-                  int64_t ldx, float* C, int64_t ldc) {
-  mm_gen(N, K, T, A, lda, 1, X, ldx, 1, C, ldc, 0);
+                  int64_t ldx, float* C, int64_t ldc, int accumulate) {
+  mm_gen(N, K, T, A, lda, 1, X, ldx, 1, C, ldc, accumulate);
 }
 
 static float* falloc(int64_t n) { return (float*)calloc((size_t)n, sizeof(float)); }
@@ -199,10 +207,10 @@ static void rmsnorm_fwd(int64_t T, int64_t H, const float* x, int64_t ldx, const
   }
 }
 
-/* dx (+)= rstd * (dy*w) - x * rstd^3 * mean((dy*w) * x) ; dw += sum_t dy * x * rstd */
+/* dx (+)= rstd * (dy*w) - x * rstd^3 * mean((dy*w) * x) ; dw (+)= sum_t dy * x * rstd */
 static void rmsnorm_bwd(int64_t T, int64_t H, const float* dy, int64_t lddy, const float* x,
                         int64_t ldx, const float* w, const float* rstd, float* dx, int64_t lddx,
-                        int accumulate_dx, float* dw) {
+                        int accumulate_dx, float* dw, int accumulate_dw) {
   if (dx) {
 #pragma omp parallel for schedule(static)
     for (int64_t t = 0; t < T; ++t) {
@@ -226,7 +234,7 @@ static void rmsnorm_bwd(int64_t T, int64_t H, const float* dy, int64_t lddy, con
     for (int64_t i = 0; i < H; ++i) {
       double s = 0.0;
       for (int64_t t = 0; t < T; ++t) s += (double)dy[t * lddy + i] * x[t * ldx + i] * rstd[t];
-      dw[i] = (float)s;
+      dw[i] = accumulate_dw ? dw[i] + (float)s : (float)s;
     }
   }
 }
@@ -265,23 +273,41 @@ static void rope_row(float* x, int n_heads, int hd, const float* cs, const float
 static float silu(float x) { return x / (1.0f + expf(-x)); }
 
 /* ============================================================ model state */
-typedef struct acts {
-  int64_t T, H, Q, KV, NQKV, I, V, W3;
-  float *F, *E_rows, *g, *U, *rstd_a, *rstd_b, *qkv, *o, *lse_attn, *r, *z, *rstd_post, *gu,
-      *act, *h, *nrm, *rstd_fin, *lse, *dlog;
-  int32_t* argmax;
-  float *cs, *sn;
-} acts;
+#define ORC_MAX_TTT 16
 
-static void acts_free(acts* a) {
-  float** ptrs[] = {&a->F,   &a->E_rows, &a->g,   &a->U,   &a->rstd_a,   &a->rstd_b, &a->qkv,
-                    &a->o,   &a->lse_attn, &a->r, &a->z,   &a->rstd_post, &a->gu,    &a->act,
-                    &a->h,   &a->nrm,    &a->rstd_fin, &a->lse, &a->dlog, &a->cs,     &a->sn};
-  for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) {
-    free(*ptrs[i]);
-    *ptrs[i] = NULL;
+/* activations of one unroll step of the decoder layer (+ its LM head) */
+typedef struct step_acts {
+  float *E_rows, *U, *rstd_a, *rstd_b, *qkv, *o, *lse_attn, *r, *z, *rstd_post, *gu, *act, *h,
+      *nrm, *rstd_fin, *lse, *dlog;
+  int32_t* argmax;
+} step_acts;
+
+typedef struct model {
+  const orc_shape* s;
+  int K;
+  float decay;
+  int64_t T, H, Q, KV, NQ, I, V, W3;
+  float *F, *g0;  /* step-0 features and fc output g = W_fc f */
+  float *cs, *sn; /* RoPE tables, positions [0, S + K - 1) */
+  step_acts st[ORC_MAX_TTT];
+} model;
+
+static void model_free(model* M) {
+  free(M->F);
+  free(M->g0);
+  free(M->cs);
+  free(M->sn);
+  for (int j = 0; j < M->K; ++j) {
+    step_acts* a = &M->st[j];
+    float** ptrs[] = {&a->E_rows, &a->U,   &a->rstd_a,   &a->rstd_b, &a->qkv, &a->o,
+                      &a->lse_attn, &a->r, &a->z,        &a->rstd_post, &a->gu, &a->act,
+                      &a->h,      &a->nrm, &a->rstd_fin, &a->lse,    &a->dlog};
+    for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) {
+      free(*ptrs[i]);
+      *ptrs[i] = NULL;
+    }
+    free(a->argmax);
   }
-  free(a->argmax);
 }
 
 static float* wcopy(const float* p, int64_t n, int round) {
@@ -291,18 +317,79 @@ static float* wcopy(const float* p, int64_t n, int round) {
   return w;
 }
 
-/* Forward through the LM-head logits; fills dlog with logits [T, V]. */
-static void forward_core(const orc_shape* s, const float* P, const int64_t* off,
-                         const uint16_t* E, const uint16_t* F16, const int32_t* u, int rnd,
-                         acts* a, float** Wb /* bf16-rounded GEMM weights by param index */) {
-  const int64_t T = (int64_t)s->B * s->S, H = s->H, Q = (int64_t)s->nh * s->hd,
-                KV = (int64_t)s->nkv * s->hd, I = s->I, V = s->V, W3 = (int64_t)s->layers * H;
-  a->T = T; a->H = H; a->Q = Q; a->KV = KV; a->NQKV = Q + 2 * KV; a->I = I; a->V = V; a->W3 = W3;
-  a->F = falloc(T * W3);
-  for (int64_t i = 0; i < T * W3; ++i) a->F[i] = orc_bf16_to_f32(F16[i]);
-  a->g = falloc(T * H);
-  mm_nt(T, H, W3, a->F, W3, Wb[ORC_FC], W3, a->g, H, 0);
-  round_vec(a->g, T * H, rnd);
+/* input of unroll step j: g = W_fc f at step 0, the previous step's output h after */
+static const float* step_input(const model* M, int j) { return j == 0 ? M->g0 : M->st[j - 1].h; }
+
+/* RoPE (forward or inverse) on the q and k heads of a [T, NQ] buffer; row t
+ * is position t % S + j (unroll step j) */
+static void rope_rows(const model* M, float* qkv, int j, int inverse) {
+  const orc_shape* s = M->s;
+  const int64_t half = s->hd / 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < M->T; ++t) {
+    const int64_t pos = t % s->S + j;
+    float* row = qkv + t * M->NQ;
+    rope_row(row, s->nh, s->hd, M->cs + pos * half, M->sn + pos * half, inverse);
+    rope_row(row + M->Q, s->nkv, s->hd, M->cs + pos * half, M->sn + pos * half, inverse);
+  }
+}
+
+/* Causal GQA attention of unroll step j: query row t of step j sees step 0's
+ * keys s <= t of its sample plus, for i = 1..j, step i's key at row t
+ * (EAGLE-3 training-time-test cache, SpecForge's shifted-diagonal mask). */
+static void attention_fwd(model* M, int j) {
+  const orc_shape* s = M->s;
+  const int64_t NQ = M->NQ, Q = M->Q, KV = M->KV;
+  step_acts* A = &M->st[j];
+  const float scale = 1.0f / sqrtf((float)s->hd);
+  const int grp = s->nh / s->nkv;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+  for (int b = 0; b < s->B; ++b)
+    for (int h = 0; h < s->nh; ++h) {
+      const int kvh = h / grp;
+      float* p = (float*)malloc(sizeof(float) * (s->S + ORC_MAX_TTT));
+      for (int i = 0; i < s->S; ++i) {
+        const int64_t ti = (int64_t)b * s->S + i;
+        const float* q = A->qkv + ti * NQ + (int64_t)h * s->hd;
+        float mx = -INFINITY;
+        for (int c0 = 0; c0 <= i + j; ++c0) {
+          /* c0 <= i: step-0 key c0; c0 = i + d (d = 1..j): step d's key at row i */
+          const float* k = c0 <= i
+                               ? M->st[0].qkv + ((int64_t)b * s->S + c0) * NQ + Q + (int64_t)kvh * s->hd
+                               : M->st[c0 - i].qkv + ti * NQ + Q + (int64_t)kvh * s->hd;
+          float d = 0.f;
+          for (int c = 0; c < s->hd; ++c) d += q[c] * k[c];
+          p[c0] = d * scale;
+          if (p[c0] > mx) mx = p[c0];
+        }
+        double sum = 0.0;
+        for (int c0 = 0; c0 <= i + j; ++c0) {
+          p[c0] = expf(p[c0] - mx);
+          sum += p[c0];
+        }
+        A->lse_attn[ti * s->nh + h] = mx + (float)log(sum);
+        const float inv = (float)(1.0 / sum);
+        float* out = A->o + ti * Q + (int64_t)h * s->hd;
+        for (int c = 0; c < s->hd; ++c) out[c] = 0.f;
+        for (int c0 = 0; c0 <= i + j; ++c0) {
+          const float* vv = c0 <= i ? M->st[0].qkv + ((int64_t)b * s->S + c0) * NQ + Q + KV +
+                                          (int64_t)kvh * s->hd
+                                    : M->st[c0 - i].qkv + ti * NQ + Q + KV + (int64_t)kvh * s->hd;
+          const float pj = p[c0] * inv;
+          for (int c = 0; c < s->hd; ++c) out[c] += pj * vv[c];
+        }
+      }
+      free(p);
+    }
+}
+
+/* Decoder layer + final norm + LM-head logits (into dlog) of unroll step j. */
+static void decoder_fwd(model* M, int j, const float* P, const int64_t* off, const uint16_t* E,
+                        const int32_t* u, int rnd, float** Wb) {
+  const orc_shape* s = M->s;
+  const int64_t T = M->T, H = M->H, Q = M->Q, KV = M->KV, NQ = M->NQ, I = M->I, V = M->V;
+  step_acts* a = &M->st[j];
+  const float* g = step_input(M, j);
   a->E_rows = falloc(T * H);
   for (int64_t t = 0; t < T; ++t)
     for (int64_t i = 0; i < H; ++i) a->E_rows[t * H + i] = orc_bf16_to_f32(E[(int64_t)u[t] * H + i]);
@@ -310,66 +397,21 @@ static void forward_core(const orc_shape* s, const float* P, const int64_t* off,
   a->rstd_a = falloc(T);
   a->rstd_b = falloc(T);
   rmsnorm_fwd(T, H, a->E_rows, H, P + off[ORC_W_IN], s->eps, a->U, 2 * H, a->rstd_a);
-  rmsnorm_fwd(T, H, a->g, H, P + off[ORC_W_HID], s->eps, a->U + H, 2 * H, a->rstd_b);
+  rmsnorm_fwd(T, H, g, H, P + off[ORC_W_HID], s->eps, a->U + H, 2 * H, a->rstd_b);
   round_vec(a->U, T * 2 * H, rnd);
-  const int64_t NQ = a->NQKV;
   a->qkv = falloc(T * NQ);
   mm_nt(T, NQ, 2 * H, a->U, 2 * H, Wb[ORC_QKV], 2 * H, a->qkv, NQ, 0);
   round_vec(a->qkv, T * NQ, rnd);
-  a->cs = falloc((int64_t)s->S * s->hd / 2);
-  a->sn = falloc((int64_t)s->S * s->hd / 2);
-  rope_tables(s->S, s->hd, s->theta, a->cs, a->sn);
-#pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < T; ++t) {
-    const int pos = (int)(t % s->S);
-    float* row = a->qkv + t * NQ;
-    rope_row(row, s->nh, s->hd, a->cs + (int64_t)pos * s->hd / 2, a->sn + (int64_t)pos * s->hd / 2, 0);
-    rope_row(row + Q, s->nkv, s->hd, a->cs + (int64_t)pos * s->hd / 2,
-             a->sn + (int64_t)pos * s->hd / 2, 0);
-    if (rnd)
-      for (int64_t i = 0; i < Q + KV; ++i) row[i] = rb(row[i]);
-  }
-  /* causal GQA attention within each sample */
+  rope_rows(M, a->qkv, j, 0);
+  if (rnd)
+    for (int64_t t = 0; t < T; ++t)
+      for (int64_t i = 0; i < Q + KV; ++i) a->qkv[t * NQ + i] = rb(a->qkv[t * NQ + i]);
   a->o = falloc(T * Q);
   a->lse_attn = falloc(T * s->nh);
-  const float scale = 1.0f / sqrtf((float)s->hd);
-  const int grp = s->nh / s->nkv;
-#pragma omp parallel for collapse(2) schedule(dynamic, 1)
-  for (int b = 0; b < s->B; ++b)
-    for (int h = 0; h < s->nh; ++h) {
-      const int kvh = h / grp;
-      float* p = (float*)malloc(sizeof(float) * s->S);
-      for (int i = 0; i < s->S; ++i) {
-        const int64_t ti = (int64_t)b * s->S + i;
-        const float* q = a->qkv + ti * NQ + (int64_t)h * s->hd;
-        float mx = -INFINITY;
-        for (int j = 0; j <= i; ++j) {
-          const float* k = a->qkv + ((int64_t)b * s->S + j) * NQ + Q + (int64_t)kvh * s->hd;
-          float d = 0.f;
-          for (int c = 0; c < s->hd; ++c) d += q[c] * k[c];
-          p[j] = d * scale;
-          if (p[j] > mx) mx = p[j];
-        }
-        double sum = 0.0;
-        for (int j = 0; j <= i; ++j) {
-          p[j] = expf(p[j] - mx);
-          sum += p[j];
-        }
-        a->lse_attn[ti * s->nh + h] = mx + (float)log(sum);
-        const float inv = (float)(1.0 / sum);
-        float* out = a->o + ti * Q + (int64_t)h * s->hd;
-        for (int c = 0; c < s->hd; ++c) out[c] = 0.f;
-        for (int j = 0; j <= i; ++j) {
-          const float* vv = a->qkv + ((int64_t)b * s->S + j) * NQ + Q + KV + (int64_t)kvh * s->hd;
-          const float pj = p[j] * inv;
-          for (int c = 0; c < s->hd; ++c) out[c] += pj * vv[c];
-        }
-      }
-      free(p);
-    }
+  attention_fwd(M, j);
   round_vec(a->o, T * Q, rnd);
   a->r = falloc(T * H);
-  memcpy(a->r, a->g, sizeof(float) * T * H);
+  memcpy(a->r, g, sizeof(float) * T * H);
   mm_nt(T, H, Q, a->o, Q, Wb[ORC_O], Q, a->r, H, 1);
   round_vec(a->r, T * H, rnd);
   a->z = falloc(T * H);
@@ -399,40 +441,84 @@ static void forward_core(const orc_shape* s, const float* P, const int64_t* off,
   mm_nt(T, V, H, a->nrm, H, Wb[ORC_LM], H, a->dlog, V, 0);
 }
 
-/* lse / loss / top-1 from the logits in a->dlog */
-static void ce_stats(const orc_shape* s, acts* a, const int32_t* y, const int32_t* mask,
-                     int64_t global_valid, orc_step_out* out) {
-  const int64_t T = a->T, V = a->V;
-  a->lse = falloc(T);
-  a->argmax = (int32_t*)calloc((size_t)T, sizeof(int32_t));
-  double loss = 0.0;
-  int64_t valid = 0, top1 = 0;
-#pragma omp parallel for schedule(static) reduction(+ : loss, valid, top1)
-  for (int64_t t = 0; t < T; ++t) {
-    const float* l = a->dlog + t * V;
-    float mx = -INFINITY;
-    int32_t am = 0;
-    for (int64_t v = 0; v < V; ++v)
-      if (l[v] > mx) {
-        mx = l[v];
-        am = (int32_t)v;
+/* Full forward: fc, then the K unroll steps (each feeding its output h to the
+ * next), logits of every step in st[j].dlog. */
+static void model_fwd(model* M, const orc_shape* s, const float* P, const int64_t* off,
+                      const uint16_t* E, const uint16_t* F16, const int32_t* u, int rnd,
+                      float** Wb) {
+  memset(M, 0, sizeof(*M));
+  M->s = s;
+  M->K = ttt_of(s);
+  M->decay = decay_of(s);
+  M->T = (int64_t)s->B * s->S;
+  M->H = s->H;
+  M->Q = (int64_t)s->nh * s->hd;
+  M->KV = (int64_t)s->nkv * s->hd;
+  M->NQ = M->Q + 2 * M->KV;
+  M->I = s->I;
+  M->V = s->V;
+  M->W3 = (int64_t)s->layers * s->H;
+  const int64_t T = M->T, H = M->H, W3 = M->W3;
+  M->F = falloc(T * W3);
+  for (int64_t i = 0; i < T * W3; ++i) M->F[i] = orc_bf16_to_f32(F16[i]);
+  M->g0 = falloc(T * H);
+  mm_nt(T, H, W3, M->F, W3, Wb[ORC_FC], W3, M->g0, H, 0);
+  round_vec(M->g0, T * H, rnd);
+  const int npos = s->S + M->K - 1;
+  M->cs = falloc((int64_t)npos * s->hd / 2);
+  M->sn = falloc((int64_t)npos * s->hd / 2);
+  rope_tables(npos, s->hd, s->theta, M->cs, M->sn);
+  for (int j = 0; j < M->K; ++j) decoder_fwd(M, j, P, off, E, u + (int64_t)j * T, rnd, Wb);
+}
+
+/* loss weight of unroll step j: decay^j (fp32, as the library's table) */
+static float step_weight(const model* M, int j) { return (float)pow((double)M->decay, (double)j); }
+
+/* lse / loss / top-1 from the logits in st[j].dlog: loss = sum_j decay^j
+ * sum_t m_j (lse - l_y) / denom; valid / top1 over unroll step 0. */
+static void ce_stats(model* M, const int32_t* y, const int32_t* mask, int64_t global_valid,
+                     orc_step_out* out) {
+  const int64_t T = M->T, V = M->V;
+  int64_t valid0 = 0;
+  for (int64_t t = 0; t < T; ++t) valid0 += mask[t] ? 1 : 0;
+  const double denom =
+      global_valid > 0 ? (double)global_valid : (double)(valid0 > 0 ? valid0 : 1);
+  double total = 0.0;
+  out->valid = valid0;
+  out->top1 = 0;
+  for (int j = 0; j < M->K; ++j) {
+    const float w = step_weight(M, j);
+    step_acts* a = &M->st[j];
+    const int32_t* yj = y + (int64_t)j * T;
+    const int32_t* mj = mask + (int64_t)j * T;
+    a->lse = falloc(T);
+    a->argmax = (int32_t*)calloc((size_t)T, sizeof(int32_t));
+    double loss = 0.0;
+    int64_t top1 = 0;
+#pragma omp parallel for schedule(static) reduction(+ : loss, top1)
+    for (int64_t t = 0; t < T; ++t) {
+      const float* l = a->dlog + t * V;
+      float mx = -INFINITY;
+      int32_t am = 0;
+      for (int64_t v = 0; v < V; ++v)
+        if (l[v] > mx) {
+          mx = l[v];
+          am = (int32_t)v;
+        }
+      double sum = 0.0;
+      for (int64_t v = 0; v < V; ++v) sum += exp((double)l[v] - mx);
+      const float lse = mx + (float)log(sum);
+      a->lse[t] = lse;
+      a->argmax[t] = am;
+      if (mj[t]) {
+        loss += (double)lse - l[yj[t]];
+        top1 += (am == yj[t]);
       }
-    double sum = 0.0;
-    for (int64_t v = 0; v < V; ++v) sum += exp((double)l[v] - mx);
-    const float lse = mx + (float)log(sum);
-    a->lse[t] = lse;
-    a->argmax[t] = am;
-    if (mask[t]) {
-      loss += (double)lse - l[y[t]];
-      valid += 1;
-      top1 += (am == y[t]);
     }
+    total += w * (loss / denom);
+    if (j == 0) out->top1 = top1;
   }
-  const double denom = global_valid > 0 ? (double)global_valid : (double)(valid > 0 ? valid : 1);
-  out->loss = loss / denom;
-  out->valid = valid;
-  out->top1 = top1;
-  (void)s;
+  out->loss = total;
 }
 
 /* bf16-rounded GEMM weights: one persistent buffer (re-used across steps, so
@@ -454,20 +540,26 @@ static void weights_bf16(const orc_shape* s, const float* P, const int64_t* off,
   for (int p = 0; p < ORC_NPARAMS; ++p) Wb[p] = wb_cache + off[p];
 }
 
+static int shape_ok(const orc_shape* s) {
+  return s->nh % s->nkv == 0 && s->hd % 2 == 0 && ttt_of(s) <= ORC_MAX_TTT;
+}
+
 int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, const uint16_t* F,
                 const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
                 int round_bf16, orc_step_out* out, float* lse_out, int32_t* argmax_out) {
+  if (!shape_ok(s)) return 1;
   int64_t off[ORC_NPARAMS];
   orc_param_layout(s, NULL, NULL, NULL, off);
   float* Wb[ORC_NPARAMS];
   weights_bf16(s, params, off, round_bf16, Wb);
-  acts a;
-  memset(&a, 0, sizeof(a));
-  forward_core(s, params, off, E, F, u, round_bf16, &a, Wb);
-  ce_stats(s, &a, y, mask, global_valid, out);
-  if (lse_out) memcpy(lse_out, a.lse, sizeof(float) * a.T);
-  if (argmax_out) memcpy(argmax_out, a.argmax, sizeof(int32_t) * a.T);
-  acts_free(&a);
+  model M;
+  model_fwd(&M, s, params, off, E, F, u, round_bf16, Wb);
+  ce_stats(&M, y, mask, global_valid, out);
+  for (int j = 0; j < M.K; ++j) {
+    if (lse_out) memcpy(lse_out + (int64_t)j * M.T, M.st[j].lse, sizeof(float) * M.T);
+    if (argmax_out) memcpy(argmax_out + (int64_t)j * M.T, M.st[j].argmax, sizeof(int32_t) * M.T);
+  }
+  model_free(&M);
   return 0;
 }
 
@@ -493,129 +585,57 @@ void orc_adamw(int64_t n, float* p, float* m, float* v, const float* g, const fl
   }
 }
 
-int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, float* params,
-                   float* mst, float* vst, float* grads, const uint16_t* E, const uint16_t* F16,
-                   const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
-                   int rnd, int do_update, orc_step_out* out) {
-  if (s->nh % s->nkv != 0 || s->hd % 2 != 0) return 1;
-  int64_t off[ORC_NPARAMS], rows[ORC_NPARAMS], cols[ORC_NPARAMS];
-  const int64_t total = orc_param_layout(s, NULL, rows, cols, off);
-  float* Wb[ORC_NPARAMS];
-  prof(NULL);
-  weights_bf16(s, params, off, rnd, Wb);
-  prof("bf16 weight copies");
-  acts a;
-  memset(&a, 0, sizeof(a));
-  forward_core(s, params, off, E, F16, u, rnd, &a, Wb);
-  prof("forward (incl. LM head)");
-  ce_stats(s, &a, y, mask, global_valid, out);
-  prof("CE stats");
-  const int64_t T = a.T, H = a.H, Q = a.Q, KV = a.KV, NQ = a.NQKV, I = a.I, V = a.V, W3 = a.W3;
-  int64_t nvalid = 0;
-  for (int64_t t = 0; t < T; ++t) nvalid += mask[t] ? 1 : 0;
-  const double denom = global_valid > 0 ? (double)global_valid : (double)(nvalid > 0 ? nvalid : 1);
-  memset(grads, 0, sizeof(float) * total);
-
-  /* ---- LM head + CE backward: dlogits = (softmax - onehot) * m / N */
-#pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < T; ++t) {
-    float* l = a.dlog + t * V;
-    const float coef = mask[t] ? (float)(1.0 / denom) : 0.f;
-    for (int64_t v = 0; v < V; ++v) {
-      const float p = expf(l[v] - a.lse[t]);
-      float gval = (p - (v == y[t] ? 1.f : 0.f)) * coef;
-      l[v] = rnd ? rb(gval) : gval;
-    }
-  }
-  prof("CE backward (softmax grad)");
-  float* dn = falloc(T * H);
-  mm_nn(T, H, V, a.dlog, V, Wb[ORC_LM], H, dn, H, 0);
-  prof("LM head dX");
-  mm_tn(V, H, T, a.dlog, V, a.nrm, H, grads + off[ORC_LM], H);
-  prof("LM head dW");
-
-  /* ---- final norm */
-  float* dh = falloc(T * H);
-  rmsnorm_bwd(T, H, dn, H, a.h, H, params + off[ORC_W_FIN], a.rstd_fin, dh, H, 0,
-              grads + off[ORC_W_FIN]);
-  float* dh_b = wcopy(dh, T * H, rnd);
-
-  /* ---- MLP */
-  float* dact = falloc(T * I);
-  mm_nn(T, I, H, dh_b, H, Wb[ORC_DOWN], I, dact, I, 0);
-  round_vec(dact, T * I, rnd);
-  mm_tn(H, I, T, dh_b, H, a.act, I, grads + off[ORC_DOWN], I);
-  float* dgu = falloc(T * 2 * I);
-#pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < T; ++t)
-    for (int64_t i = 0; i < I; ++i) {
-      const float gt = a.gu[t * 2 * I + i], up = a.gu[t * 2 * I + I + i];
-      const float sg = 1.0f / (1.0f + expf(-gt));
-      const float d = dact[t * I + i];
-      dgu[t * 2 * I + i] = d * up * sg * (1.0f + gt * (1.0f - sg));
-      dgu[t * 2 * I + I + i] = d * gt * sg;
-    }
-  round_vec(dgu, T * 2 * I, rnd);
-  float* dz = falloc(T * H);
-  mm_nn(T, H, 2 * I, dgu, 2 * I, Wb[ORC_GATE_UP], H, dz, H, 0);
-  mm_tn(2 * I, H, T, dgu, 2 * I, a.z, H, grads + off[ORC_GATE_UP], H);
-
-  /* ---- post-attention norm; residual */
-  float* dr = falloc(T * H);
-  memcpy(dr, dh, sizeof(float) * T * H);
-  rmsnorm_bwd(T, H, dz, H, a.r, H, params + off[ORC_W_POST], a.rstd_post, dr, H, 1,
-              grads + off[ORC_W_POST]);
-  float* dr_b = wcopy(dr, T * H, rnd);
-
-  /* ---- o projection */
-  float* dO = falloc(T * Q);
-  mm_nn(T, Q, H, dr_b, H, Wb[ORC_O], Q, dO, Q, 0);
-  round_vec(dO, T * Q, rnd);
-  mm_tn(H, Q, T, dr_b, H, a.o, Q, grads + off[ORC_O], Q);
-
-  /* ---- attention backward */
-  float* dqkv = falloc(T * NQ);
+/* Attention backward of unroll step j.  dq [T, Q] receives step j's query
+ * gradient; dK / dV [K][T, KV] accumulate the key / value gradients of every
+ * step (rotated space): step 0's from the causal part of all steps, step i's
+ * (i >= 1) from the diagonal entries of steps j >= i. */
+static void attention_bwd(model* M, int j, const float* dO, float* dq, float** dK, float** dV) {
+  const orc_shape* s = M->s;
+  const int64_t NQ = M->NQ, Q = M->Q, KV = M->KV;
+  const step_acts* A = &M->st[j];
   const float scale = 1.0f / sqrtf((float)s->hd);
   const int grp = s->nh / s->nkv;
-  /* dq per (b, h) rows; dk/dv accumulated per (b, kv head) over the group */
+  /* (b, kv head) partitions: every dK / dV row it touches belongs to it */
 #pragma omp parallel for collapse(2) schedule(dynamic, 1)
   for (int b = 0; b < s->B; ++b)
     for (int kvh = 0; kvh < s->nkv; ++kvh) {
-      float* p = (float*)malloc(sizeof(float) * s->S);
-      float* dp = (float*)malloc(sizeof(float) * s->S);
+      float* p = (float*)malloc(sizeof(float) * (s->S + ORC_MAX_TTT));
+      float* dp = (float*)malloc(sizeof(float) * (s->S + ORC_MAX_TTT));
       for (int hh = 0; hh < grp; ++hh) {
         const int h = kvh * grp + hh;
         for (int i = 0; i < s->S; ++i) {
           const int64_t ti = (int64_t)b * s->S + i;
-          const float* q = a.qkv + ti * NQ + (int64_t)h * s->hd;
+          const float* q = A->qkv + ti * NQ + (int64_t)h * s->hd;
           const float* dout = dO + ti * Q + (int64_t)h * s->hd;
-          const float* oo = a.o + ti * Q + (int64_t)h * s->hd;
-          const float lse = a.lse_attn[ti * s->nh + h];
+          const float* oo = A->o + ti * Q + (int64_t)h * s->hd;
+          const float lse = A->lse_attn[ti * s->nh + h];
           float Di = 0.f;
           for (int c = 0; c < s->hd; ++c) Di += dout[c] * oo[c];
-          for (int j = 0; j <= i; ++j) {
-            const int64_t tj = (int64_t)b * s->S + j;
-            const float* k = a.qkv + tj * NQ + Q + (int64_t)kvh * s->hd;
-            const float* vv = a.qkv + tj * NQ + Q + KV + (int64_t)kvh * s->hd;
+          for (int c0 = 0; c0 <= i + j; ++c0) {
+            const int st = c0 <= i ? 0 : c0 - i;
+            const int64_t row = c0 <= i ? (int64_t)b * s->S + c0 : ti;
+            const float* k = M->st[st].qkv + row * NQ + Q + (int64_t)kvh * s->hd;
+            const float* vv = k + KV;
             float d = 0.f, e = 0.f;
             for (int c = 0; c < s->hd; ++c) {
               d += q[c] * k[c];
               e += dout[c] * vv[c];
             }
-            p[j] = expf(d * scale - lse);
-            dp[j] = e;
+            p[c0] = expf(d * scale - lse);
+            dp[c0] = e;
           }
-          float* dq = dqkv + ti * NQ + (int64_t)h * s->hd;
-          for (int j = 0; j <= i; ++j) {
-            const int64_t tj = (int64_t)b * s->S + j;
-            const float* k = a.qkv + tj * NQ + Q + (int64_t)kvh * s->hd;
-            float* dk = dqkv + tj * NQ + Q + (int64_t)kvh * s->hd;
-            float* dv = dqkv + tj * NQ + Q + KV + (int64_t)kvh * s->hd;
-            const float ds = p[j] * (dp[j] - Di) * scale;
+          float* dqr = dq + ti * Q + (int64_t)h * s->hd;
+          for (int c0 = 0; c0 <= i + j; ++c0) {
+            const int st = c0 <= i ? 0 : c0 - i;
+            const int64_t row = c0 <= i ? (int64_t)b * s->S + c0 : ti;
+            const float* k = M->st[st].qkv + row * NQ + Q + (int64_t)kvh * s->hd;
+            float* dk = dK[st] + row * KV + (int64_t)kvh * s->hd;
+            float* dv = dV[st] + row * KV + (int64_t)kvh * s->hd;
+            const float ds = p[c0] * (dp[c0] - Di) * scale;
             for (int c = 0; c < s->hd; ++c) {
-              dq[c] += ds * k[c];
+              dqr[c] += ds * k[c];
               dk[c] += ds * q[c];
-              dv[c] += p[j] * dout[c];
+              dv[c] += p[c0] * dout[c];
             }
           }
         }
@@ -623,39 +643,152 @@ int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, floa
       free(p);
       free(dp);
     }
-  /* RoPE backward on dq, dk; round to bf16 (GEMM operand) */
-#pragma omp parallel for schedule(static)
-  for (int64_t t = 0; t < T; ++t) {
-    const int pos = (int)(t % s->S);
-    float* row = dqkv + t * NQ;
-    if (rnd)
-      for (int64_t i = 0; i < NQ; ++i) row[i] = rb(row[i]);
-    rope_row(row, s->nh, s->hd, a.cs + (int64_t)pos * s->hd / 2, a.sn + (int64_t)pos * s->hd / 2, 1);
-    rope_row(row + Q, s->nkv, s->hd, a.cs + (int64_t)pos * s->hd / 2,
-             a.sn + (int64_t)pos * s->hd / 2, 1);
-    if (rnd)
-      for (int64_t i = 0; i < Q + KV; ++i) row[i] = rb(row[i]);
+}
+
+int orc_train_step(const orc_shape* s, const float* adamw5, int64_t step_k, float* params,
+                   float* mst, float* vst, float* grads, const uint16_t* E, const uint16_t* F16,
+                   const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
+                   int rnd, int do_update, orc_step_out* out) {
+  if (!shape_ok(s)) return 1;
+  int64_t off[ORC_NPARAMS], rows[ORC_NPARAMS], cols[ORC_NPARAMS];
+  const int64_t total = orc_param_layout(s, NULL, rows, cols, off);
+  float* Wb[ORC_NPARAMS];
+  prof(NULL);
+  weights_bf16(s, params, off, rnd, Wb);
+  prof("bf16 weight copies");
+  model M;
+  model_fwd(&M, s, params, off, E, F16, u, rnd, Wb);
+  prof("forward (incl. LM head)");
+  ce_stats(&M, y, mask, global_valid, out);
+  prof("CE stats");
+  const int64_t T = M.T, H = M.H, Q = M.Q, KV = M.KV, NQ = M.NQ, I = M.I, V = M.V, W3 = M.W3;
+  const int K = M.K;
+  const double denom = global_valid > 0 ? (double)global_valid
+                                        : (double)(out->valid > 0 ? out->valid : 1);
+  memset(grads, 0, sizeof(float) * total);
+  float *dK[ORC_MAX_TTT], *dV[ORC_MAX_TTT];
+  for (int j = 0; j < K; ++j) {
+    dK[j] = falloc(T * KV);
+    dV[j] = falloc(T * KV);
   }
+  float* dn = falloc(T * H);
+  float* dh = falloc(T * H);
+  float* dact = falloc(T * I);
+  float* dgu = falloc(T * 2 * I);
+  float* dz = falloc(T * H);
+  float* dr = falloc(T * H);
+  float* dO = falloc(T * Q);
+  float* dq = falloc(T * Q);
+  float* dqkv = falloc(T * NQ);
   float* dU = falloc(T * 2 * H);
-  mm_nn(T, 2 * H, NQ, dqkv, NQ, Wb[ORC_QKV], 2 * H, dU, 2 * H, 0);
-  mm_tn(NQ, 2 * H, T, dqkv, NQ, a.U, 2 * H, grads + off[ORC_QKV], 2 * H);
+  float* dg_next = NULL; /* gradient w.r.t. h_j arriving from step j + 1's input */
+  /* unroll steps in reverse: step j's input gradient feeds step j - 1's output */
+  for (int j = K - 1; j >= 0; --j) {
+    step_acts* a = &M.st[j];
+    const int32_t* yj = y + (int64_t)j * T;
+    const int32_t* mj = mask + (int64_t)j * T;
+    const float* g = step_input(&M, j);
+    const float wj = step_weight(&M, j);
 
-  /* ---- input norms (embedding frozen: only dw_in) */
-  rmsnorm_bwd(T, H, dU, 2 * H, a.E_rows, H, params + off[ORC_W_IN], a.rstd_a, NULL, 0, 0,
-              grads + off[ORC_W_IN]);
-  float* dg = dr; /* residual path: dg = dr + d(hidden norm) */
-  rmsnorm_bwd(T, H, dU + H, 2 * H, a.g, H, params + off[ORC_W_HID], a.rstd_b, dg, H, 1,
-              grads + off[ORC_W_HID]);
-  round_vec(dg, T * H, rnd);
-  mm_tn(H, W3, T, dg, H, a.F, W3, grads + off[ORC_FC], W3);
+    /* ---- LM head + CE backward: dlogits = (softmax - onehot) * m * decay^j / N */
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < T; ++t) {
+      float* l = a->dlog + t * V;
+      const float coef = mj[t] ? (float)(1.0 / denom) * wj : 0.f;
+      for (int64_t v = 0; v < V; ++v) {
+        const float p = expf(l[v] - a->lse[t]);
+        float gval = (p - (v == yj[t] ? 1.f : 0.f)) * coef;
+        l[v] = rnd ? rb(gval) : gval;
+      }
+    }
+    mm_nn(T, H, V, a->dlog, V, Wb[ORC_LM], H, dn, H, 0);
+    mm_tn(V, H, T, a->dlog, V, a->nrm, H, grads + off[ORC_LM], H, 1);
+    prof("LM head backward");
 
-  prof("decoder backward");
+    /* ---- final norm (+ the gradient arriving through the next step's input) */
+    if (dg_next)
+      memcpy(dh, dg_next, sizeof(float) * T * H);
+    rmsnorm_bwd(T, H, dn, H, a->h, H, params + off[ORC_W_FIN], a->rstd_fin, dh, H,
+                dg_next != NULL, grads + off[ORC_W_FIN], 1);
+    float* dh_b = wcopy(dh, T * H, rnd);
+
+    /* ---- MLP */
+    mm_nn(T, I, H, dh_b, H, Wb[ORC_DOWN], I, dact, I, 0);
+    round_vec(dact, T * I, rnd);
+    mm_tn(H, I, T, dh_b, H, a->act, I, grads + off[ORC_DOWN], I, 1);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < T; ++t)
+      for (int64_t i = 0; i < I; ++i) {
+        const float gt = a->gu[t * 2 * I + i], up = a->gu[t * 2 * I + I + i];
+        const float sg = 1.0f / (1.0f + expf(-gt));
+        const float d = dact[t * I + i];
+        dgu[t * 2 * I + i] = d * up * sg * (1.0f + gt * (1.0f - sg));
+        dgu[t * 2 * I + I + i] = d * gt * sg;
+      }
+    round_vec(dgu, T * 2 * I, rnd);
+    mm_nn(T, H, 2 * I, dgu, 2 * I, Wb[ORC_GATE_UP], H, dz, H, 0);
+    mm_tn(2 * I, H, T, dgu, 2 * I, a->z, H, grads + off[ORC_GATE_UP], H, 1);
+
+    /* ---- post-attention norm; residual */
+    memcpy(dr, dh, sizeof(float) * T * H);
+    rmsnorm_bwd(T, H, dz, H, a->r, H, params + off[ORC_W_POST], a->rstd_post, dr, H, 1,
+                grads + off[ORC_W_POST], 1);
+    float* dr_b = wcopy(dr, T * H, rnd);
+
+    /* ---- o projection */
+    mm_nn(T, Q, H, dr_b, H, Wb[ORC_O], Q, dO, Q, 0);
+    round_vec(dO, T * Q, rnd);
+    mm_tn(H, Q, T, dr_b, H, a->o, Q, grads + off[ORC_O], Q, 1);
+
+    /* ---- attention: dq of this step; dK / dV of this step are complete now
+     * (every step >= j has contributed) */
+    memset(dq, 0, sizeof(float) * T * Q);
+    attention_bwd(&M, j, dO, dq, dK, dV);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < T; ++t) {
+      float* row = dqkv + t * NQ;
+      memcpy(row, dq + t * Q, sizeof(float) * Q);
+      memcpy(row + Q, dK[j] + t * KV, sizeof(float) * KV);
+      memcpy(row + Q + KV, dV[j] + t * KV, sizeof(float) * KV);
+    }
+    /* round, RoPE backward on dq / dk (position t % S + j), round: GEMM operand */
+    round_vec(dqkv, T * NQ, rnd);
+    rope_rows(&M, dqkv, j, 1);
+    if (rnd)
+      for (int64_t t = 0; t < T; ++t)
+        for (int64_t i = 0; i < Q + KV; ++i) dqkv[t * NQ + i] = rb(dqkv[t * NQ + i]);
+    mm_nn(T, 2 * H, NQ, dqkv, NQ, Wb[ORC_QKV], 2 * H, dU, 2 * H, 0);
+    mm_tn(NQ, 2 * H, T, dqkv, NQ, a->U, 2 * H, grads + off[ORC_QKV], 2 * H, 1);
+
+    /* ---- input norms (embedding frozen: only dw_in) */
+    rmsnorm_bwd(T, H, dU, 2 * H, a->E_rows, H, params + off[ORC_W_IN], a->rstd_a, NULL, 0, 0,
+                grads + off[ORC_W_IN], 1);
+    float* dg = dr; /* residual path: dg = dr + d(hidden norm) */
+    rmsnorm_bwd(T, H, dU + H, 2 * H, g, H, params + off[ORC_W_HID], a->rstd_b, dg, H, 1,
+                grads + off[ORC_W_HID], 1);
+    if (j > 0) {
+      /* fp32 gradient w.r.t. h_{j-1} (the previous step's output) */
+      if (!dg_next) dg_next = falloc(T * H);
+      memcpy(dg_next, dg, sizeof(float) * T * H);
+    } else {
+      round_vec(dg, T * H, rnd);
+      mm_tn(H, W3, T, dg, H, M.F, W3, grads + off[ORC_FC], W3, 0);
+    }
+    free(dh_b);
+    free(dr_b);
+    prof("decoder backward");
+  }
   if (do_update) orc_adamw(total, params, mst, vst, grads, adamw5, step_k);
   prof("AdamW");
 
-  free(dn); free(dh); free(dh_b); free(dact); free(dgu); free(dz); free(dr); free(dr_b);
-  free(dO); free(dqkv); free(dU);
-  acts_free(&a);
+  for (int j = 0; j < K; ++j) {
+    free(dK[j]);
+    free(dV[j]);
+  }
+  free(dg_next);
+  free(dn); free(dh); free(dact); free(dgu); free(dz); free(dr); free(dO); free(dq); free(dqkv);
+  free(dU);
+  model_free(&M);
   (void)rows; (void)cols;
   return 0;
 }

@@ -101,3 +101,55 @@ def test_bf16_rounding_mode_is_close():
                                  round_bf16=True, update=False)
     assert abs(o16.loss - o32.loss) < 2e-3 * o32.loss
     assert np.linalg.norm(g16 - g32) / np.linalg.norm(g32) < 3e-2
+
+
+@pytest.mark.parametrize("sh,K", [(SHAPES[0], 3), (SHAPES[1], 2)])
+def test_ttt_step_matches_torch(sh, K):
+    """Training-time-test unroll (K steps): C oracle (fp32) vs torch autograd of
+    the SpecForge-layout restatement (tests/torch_ref.forward_loss_ttt)."""
+    from torch_ref import forward_loss_ttt
+    sh = dict(sh, ttt=K)
+    # one full-length sample, one whose shifted masks run out at different steps
+    lens = [sh["S"] + 2 + K] * (sh["B"] - 1) + [sh["S"] // 2 + 1]
+    shp, P, E, F, u, y, m = build(sh, 13, lens)
+    assert u.size == K * sh["B"] * sh["S"]
+    hp = [1e-3, 0.9, 0.95, 1e-8, 0.01]
+    z = np.zeros_like(P)
+    out, grads = oracle.train_step(shp, hp, 1, P.copy(), z.copy(), z.copy(), E, F, u, y, m,
+                                   round_bf16=False, update=False)
+    W, layout = torch_params(shp, P)
+    Et = torch.from_numpy(oracle.bf16_to_f32(E).reshape(shp.V, shp.H))
+    Ft = torch.from_numpy(oracle.bf16_to_f32(F).reshape(F.shape))
+    loss, logits = forward_loss_ttt(shp, W, Et, Ft, torch.from_numpy(u).long(),
+                                    torch.from_numpy(y), torch.from_numpy(m), 0, K)
+    loss.backward()
+    T = sh["B"] * sh["S"]
+    assert out.valid == int(m[:T].sum())
+    assert abs(out.loss - loss.item()) <= 1e-5 * abs(loss.item()), (out.loss, loss.item())
+    for name, r, c, off in layout:
+        gt = W[name].grad.numpy().reshape(-1)
+        go = grads[off:off + r * c]
+        rel = np.linalg.norm(go - gt) / max(np.linalg.norm(gt), 1e-30)
+        assert rel < 2e-4, (name, rel)
+    o2, lse, am = oracle.forward(shp, P, E, F, u, y, m, round_bf16=False)
+    np.testing.assert_allclose(lse, torch.logsumexp(logits, -1).detach().numpy(), rtol=1e-5,
+                               atol=1e-5)
+    assert abs(o2.loss - out.loss) <= 1e-9 * abs(out.loss)
+
+
+def test_ttt_gather_shifts():
+    """Slice j of u / y / m is the step-0 rule shifted by j tokens (bit-exact)."""
+    sh = dict(SHAPES[1], ttt=3)
+    shp = oracle.make_shape(**sh)
+    L = [sh["S"] + 4, 7, 0]
+    samples = [(np.arange(100, 100 + n, dtype=np.int32), np.zeros((n, 3 * sh["H"]), np.uint16))
+               for n in L]
+    F, u, y, m = oracle.gather_batch(shp, samples)
+    S, T = sh["S"], sh["B"] * sh["S"]
+    for j in range(3):
+        for b, n in enumerate(L):
+            for t in range(S):
+                r = j * T + b * S + t
+                assert m[r] == (t + 2 + j < n)
+                assert y[r] == (100 + t + 2 + j if t + 2 + j < n else 0)
+                assert u[r] == (100 + t + 1 + j if t + 1 + j < n else 0)
