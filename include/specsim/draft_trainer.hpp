@@ -137,6 +137,10 @@ struct DraftShape {
       layers_tapped = 3, micro_batch = 1;
   float rms_eps = 1e-5f;
   double rope_theta = 10000.0;
+  // EAGLE-3 training-time-test unroll: K decoder passes per step, step j's
+  // loss weighted ttt_decay^j (see specsim_draft_shape)
+  int ttt_steps = 1;
+  float ttt_decay = 0.8f;
   void validate() const;  // collects every problem, throws std::invalid_argument
 };
 

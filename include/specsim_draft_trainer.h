@@ -216,6 +216,17 @@ typedef struct specsim_draft_shape {
   int32_t micro_batch;   /* B samples per rank per step             */
   float rms_eps;
   double rope_theta;
+  /* EAGLE-3 training-time-test unroll (SpecForge
+   * convention, not in the reference): K = ttt_steps decoder passes per step
+   * (0 reads as 1, max 16; K > 1 needs seq_len % 128 == 0).  Pass j >= 1
+   * takes the previous pass's output h in place of g, tokens shifted by j
+   * (u = x[t+1+j], y = x[t+2+j], m = [t+2+j < L]), RoPE positions t + j, and
+   * its attention row t also sees the keys / values of passes 1..j at row t.
+   * loss = sum_j ttt_decay^j CE_j / N (N = valid count of pass 0; decay 0
+   * reads as 0.8); valid_tokens / top1_correct / alpha_eval are pass 0's;
+   * eval runs pass 0 only. */
+  int32_t ttt_steps;
+  float ttt_decay;
 } specsim_draft_shape;
 
 /* PyTorch AdamW semantics. */

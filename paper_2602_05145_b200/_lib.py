@@ -47,7 +47,8 @@ class DraftShape(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("vocab", C.c_int32), ("seq_len", C.c_int32),
                 ("n_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("ffn", C.c_int32), ("layers_tapped", C.c_int32), ("micro_batch", C.c_int32),
-                ("rms_eps", C.c_float), ("rope_theta", C.c_double)]
+                ("rms_eps", C.c_float), ("rope_theta", C.c_double), ("ttt_steps", C.c_int32),
+                ("ttt_decay", C.c_float)]
 
 
 class AdamW(C.Structure):

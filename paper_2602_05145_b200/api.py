@@ -31,19 +31,25 @@ CONFIGS = {
 
 
 def gemm_flops_per_token(c: dict) -> dict:
-    """Algorithmic FLOPs per processed token (SURVEY §8(d) convention)."""
+    """Algorithmic FLOPs per processed token (SURVEY §8(d) convention).  With a
+    training-time-test unroll of K passes the decoder layer and the LM head
+    run K times (fc once) and pass j's attention adds 4Q FLOPs per cache
+    entry (j of them) to the forward."""
     H, V, S = c["hidden"], c["vocab"], c["seq_len"]
     Q = c["n_heads"] * c["head_dim"]
     KV = c["n_kv_heads"] * c["head_dim"]
     I = c["ffn"]
     L = c.get("layers_tapped", 3)
-    gemm_fwd = 2 * (L * H * H + 2 * H * (Q + 2 * KV) + Q * H + 3 * H * I + H * V)
-    attn_fwd = 2 * Q * (S + 1)
+    K = c.get("ttt_steps", 1)
+    fc = 2 * L * H * H
+    per_pass = 2 * (2 * H * (Q + 2 * KV) + Q * H + 3 * H * I + H * V)
+    gemm_fwd = fc + K * per_pass
+    attn_fwd = K * 2 * Q * (S + 1) + sum(4 * Q * j for j in range(K))
     fwd = gemm_fwd + attn_fwd
-    bwd = 2 * gemm_fwd - 2 * (L * H * H) + 2 * attn_fwd
-    lm = 2 * H * V
-    return dict(total=fwd + bwd, gemm=3 * gemm_fwd - 2 * L * H * H, attn=3 * attn_fwd,
-                lm=3 * lm, decoder_gemm=3 * gemm_fwd - 2 * L * H * H - 3 * lm)
+    bwd = 2 * gemm_fwd - fc + 2 * attn_fwd
+    lm = K * 2 * H * V
+    return dict(total=fwd + bwd, gemm=3 * gemm_fwd - fc, attn=3 * attn_fwd,
+                lm=3 * lm, decoder_gemm=3 * gemm_fwd - fc - 3 * lm)
 
 
 # ------------------------------------------------------------ bookkeeping
@@ -296,7 +302,8 @@ class DraftTrainer:
         s = _lib.DraftShape(shape["hidden"], shape["vocab"], shape["seq_len"], shape["n_heads"],
                             shape["n_kv_heads"], shape["head_dim"], shape["ffn"],
                             shape.get("layers_tapped", 3), shape["micro_batch"],
-                            shape.get("rms_eps", 1e-5), shape.get("rope_theta", 10000.0))
+                            shape.get("rms_eps", 1e-5), shape.get("rope_theta", 10000.0),
+                            shape.get("ttt_steps", 1), shape.get("ttt_decay", 0.8))
         a = _lib.AdamW(lr, betas[0], betas[1], eps, weight_decay)
         self.h = C.c_void_p()
         nid = None

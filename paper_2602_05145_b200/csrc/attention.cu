@@ -633,10 +633,16 @@ void prepare(int hd) {
 
 void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims& d, int hd,
              cudaStream_t s) {
-  if (use_tc(d)) {
-    // tcgen05 / TMEM / TMA path (attention_tc.cu)
-    const CUtensorMap tm = gemm::make_tensor_map(qkv, static_cast<long long>(d.B) * d.S, d.NQ,
-                                                 d.NQ, 64, 128);
+  const bool ttt = d.q_row_off != 0 || d.n_diag != 0;
+  if (ttt && d.S % 128 != 0)
+    throw std::invalid_argument("training-time-test attention needs seq_len % 128 == 0");
+  if (ttt && (d.n_diag < 0 || d.n_diag > kMaxDiag || (d.n_diag > 0 && !d.diag_qkv)))
+    throw std::invalid_argument("training-time-test attention: bad n_diag / diag_qkv");
+  if (ttt || use_tc(d)) {
+    // tcgen05 / TMEM / TMA path (attention_tc.cu); the map spans every unroll
+    // step's rows up to this one
+    const CUtensorMap tm = gemm::make_tensor_map(
+        qkv, d.q_row_off + static_cast<long long>(d.B) * d.S, d.NQ, d.NQ, 64, 128);
     forward_tc(qkv, o, lse, d, hd, tm, s);
     return;
   }
@@ -644,6 +650,14 @@ void forward(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Dims&
     fwd_t<128>(qkv, o, lse, d, s);
   else
     fwd_t<64>(qkv, o, lse, d, s);
+}
+
+void bwd_dot(const __nv_bfloat16* dout, const __nv_bfloat16* o, float* D, const Dims& d, int hd,
+             cudaStream_t s) {
+  const long long T = static_cast<long long>(d.B) * d.S;
+  count_launches();
+  attn_bwd_dot_kernel<<<static_cast<unsigned>((T * d.nh * 32 + 255) / 256), 256, 0, s>>>(
+      dout, o, D, d, hd);
 }
 
 bool backward(const __nv_bfloat16* qkv, const __nv_bfloat16* o, const __nv_bfloat16* dout,

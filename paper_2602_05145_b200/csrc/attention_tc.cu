@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(192, 1)
       constexpr int A = L::ATOMS;
       ptx::mbar_arrive_expect_tx(q_full, L::Q);
       for (int a = 0; a < A; ++a)
-        ptx::tma_load_2d(&tm, q_full, sQ + a * TILE, h * HD + 64 * a, row0 + qb * BQ);
+        ptx::tma_load_2d(&tm, q_full, sQ + a * TILE, h * HD + 64 * a,
+                         static_cast<int>(d.q_row_off) + row0 + qb * BQ);
       for (int j = 0; j < nkv; ++j) {
         const int s = j & 1;
         const uint32_t ph = (j >> 1) & 1;
@@ -264,6 +265,40 @@ __global__ void __launch_bounds__(192, 1)
     }
     ptx::mbar_wait(pv_done, (nkv - 1) & 1);
     ptx::tc_fence_after();
+    const long long T = static_cast<long long>(d.B) * d.S;
+    // Training-time-test cache entries (unroll step n_diag >= 1): one extra
+    // score per earlier step i at this row, q . k_i (q from the swizzled smem
+    // tile, k_i from HBM), merged into the running max / sum; their values
+    // are added to O row-wise in the store loop below.
+    const int nd = d.n_diag;
+    float pd[kMaxDiag];
+    float corr = 1.f;
+    if (nd > 0) {
+      float mnew = m_run;
+#pragma unroll 1
+      for (int i = 0; i < nd; ++i) {
+        const uint4* kr = reinterpret_cast<const uint4*>(
+            d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + g * HD);
+        float dot = 0.f;
+#pragma unroll
+        for (int c8 = 0; c8 < HD / 8; ++c8) {
+          const uint4 qv = *reinterpret_cast<const uint4*>(
+              sQ + (c8 >> 3) * TILE + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
+          const uint4 kv = __ldg(kr + c8);
+          dot += ptx::dot_bf16x8(qv, kv);
+        }
+        pd[i] = dot * sl2;
+        mnew = fmaxf(mnew, pd[i]);
+      }
+      corr = exp2f(m_run - mnew);
+      l_run *= corr;
+#pragma unroll 1
+      for (int i = 0; i < nd; ++i) {
+        pd[i] = exp2f(pd[i] - mnew);
+        l_run += pd[i];
+      }
+      m_run = mnew;
+    }
     const float inv = 1.f / l_run;
     __nv_bfloat16* orow = out + static_cast<long long>(row0 + q) * d.Q + h * HD;
 #pragma unroll
@@ -271,15 +306,29 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t o[32];
       ptx::tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
       ptx::tmem_ld_wait();
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * corr;
+#pragma unroll 1
+      for (int i = 0; i < nd; ++i) {
+        const uint4* vr = reinterpret_cast<const uint4*>(
+            d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + d.KV +
+            g * HD + c * 32);
+#pragma unroll
+        for (int v8 = 0; v8 < 4; ++v8) {
+          float vf[8];
+          ptx::unpack_bf16x8(__ldg(vr + v8), vf);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[v8 * 8 + e] += pd[i] * vf[e];
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 32; i += 8)
-        ptx::st_global_v4(orow + c * 32 + i,
-                          ptx::pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv),
-                          ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv),
-                          ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv),
-                          ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv));
+        ptx::st_global_v4(orow + c * 32 + i, ptx::pack_bf16x2(acc[i] * inv, acc[i + 1] * inv),
+                          ptx::pack_bf16x2(acc[i + 2] * inv, acc[i + 3] * inv),
+                          ptx::pack_bf16x2(acc[i + 4] * inv, acc[i + 5] * inv),
+                          ptx::pack_bf16x2(acc[i + 6] * inv, acc[i + 7] * inv));
     }
-    const long long T = static_cast<long long>(d.B) * d.S;
     lse[h * T + row0 + q] = (m_run + log2f(l_run)) * kLn2;
   }
   ptx::tc_fence_before();
@@ -305,10 +354,14 @@ __global__ void __launch_bounds__(192, 1)
 // sc as bf16.  With RoPE tables the row is first rounded to bf16 (the value
 // the unfused path stores) and then inverse-rotated in registers:
 // x1' = x1 c + x2 s, x2' = x2 c - x1 s.
+// add (nullable): an fp32 row in the same (rotated, scaled) units, added
+// before rounding (the training-time-test cache part of dq).
 template <int HD>
 __device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, float sc,
-                                               const Dims& d, int pos) {
+                                               const Dims& d, int pos,
+                                               const float* __restrict__ add = nullptr) {
   constexpr int HALF = HD / 2;
+  const long long L = d.rope_len > 0 ? d.rope_len : d.S;
   // rotation partners (i, i + HD/2) sit in chunks p and p + HD/64: process one
   // such pair of 32-column chunks at a time (64 live registers)
 #pragma unroll
@@ -317,20 +370,28 @@ __device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, 
     ptx::tmem_ld_32x32b_x32(tm + p * 32, a);
     ptx::tmem_ld_32x32b_x32(tm + HALF + p * 32, b);
     ptx::tmem_ld_wait();
-    float s = sc;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float x1 = __uint_as_float(a[i]) * sc, x2 = __uint_as_float(b[i]) * sc;
+      if (add != nullptr) {
+        x1 += __ldg(add + p * 32 + i);
+        x2 += __ldg(add + HALF + p * 32 + i);
+      }
+      a[i] = __float_as_uint(x1);
+      b[i] = __float_as_uint(x2);
+    }
     if (d.rope_cos != nullptr) {
-      const float* cs = d.rope_cos + static_cast<long long>(p * 32) * d.S + pos;
-      const float* sn = d.rope_sin + static_cast<long long>(p * 32) * d.S + pos;
+      const float* cs = d.rope_cos + static_cast<long long>(p * 32) * L + pos;
+      const float* sn = d.rope_sin + static_cast<long long>(p * 32) * L + pos;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float cv = __ldg(cs + static_cast<long long>(i) * d.S);
-        const float sv = __ldg(sn + static_cast<long long>(i) * d.S);
-        const float x1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(a[i]) * sc));
-        const float x2 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(b[i]) * sc));
+        const float cv = __ldg(cs + static_cast<long long>(i) * L);
+        const float sv = __ldg(sn + static_cast<long long>(i) * L);
+        const float x1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(a[i])));
+        const float x2 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(b[i])));
         a[i] = __float_as_uint(x1 * cv + x2 * sv);
         b[i] = __float_as_uint(x2 * cv - x1 * sv);
       }
-      s = 1.f;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -339,10 +400,10 @@ __device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, 
 #pragma unroll
       for (int i = 0; i < 32; i += 8)
         ptx::st_global_v4(
-            out + i, ptx::pack_bf16x2(__uint_as_float(o[i]) * s, __uint_as_float(o[i + 1]) * s),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 2]) * s, __uint_as_float(o[i + 3]) * s),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 4]) * s, __uint_as_float(o[i + 5]) * s),
-            ptx::pack_bf16x2(__uint_as_float(o[i + 6]) * s, __uint_as_float(o[i + 7]) * s));
+            out + i, ptx::pack_bf16x2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 2]), __uint_as_float(o[i + 3])),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 4]), __uint_as_float(o[i + 5])),
+            ptx::pack_bf16x2(__uint_as_float(o[i + 6]), __uint_as_float(o[i + 7])));
     }
   }
 }
@@ -379,7 +440,7 @@ __global__ void __launch_bounds__(192, 1)
                           const __grid_constant__ CUtensorMap tm_q,   // qkv, box {64,64}
                           const __grid_constant__ CUtensorMap tm_do,  // dO,  box {64,64}
                           const float* __restrict__ lse, const float* __restrict__ Dv,
-                          __nv_bfloat16* __restrict__ dqkv, Dims d) {
+                          __nv_bfloat16* __restrict__ dqkv, Dims d, int n_steps) {
   using L = KvSmem<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -404,7 +465,8 @@ __global__ void __launch_bounds__(192, 1)
   const long long T = static_cast<long long>(d.B) * d.S;
   const int qb0 = kb * (BKV / BQB), nqb = d.S / BQB;
   const int per_head = nqb - qb0;
-  const int n_it = rep * per_head;
+  const int per_step = rep * per_head;  // (query head, 64-query block) pairs of one unroll step
+  const int n_it = n_steps * per_step;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tm_kv);
@@ -444,18 +506,21 @@ __global__ void __launch_bounds__(192, 1)
       }
       for (int it = 0; it < n_it; ++it) {
         const int st = it & 1;
-        const int h = g * rep + it / per_head;
-        const int q0 = (qb0 + it % per_head) * BQB;
+        const int step = it / per_step, rem = it % per_step;
+        const int h = g * rep + rem / per_head;
+        const int q0 = (qb0 + rem % per_head) * BQB;
+        const int qrow = static_cast<int>(step * T) + row0 + q0;
+        const long long li = (static_cast<long long>(step) * d.nh + h) * T + row0 + q0;
         ptx::mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * L::QT + 2 * BQB * 4);
         for (int a = 0; a < A; ++a) {
           ptx::tma_load_2d(&tm_q, &qd_full[st], smem + L::OFF_Q + st * L::QT + a * TILE64,
-                           h * HD + 64 * a, row0 + q0);
+                           h * HD + 64 * a, qrow);
           ptx::tma_load_2d(&tm_do, &qd_full[st], smem + L::OFF_DO + st * L::QT + a * TILE64,
-                           h * HD + 64 * a, row0 + q0);
+                           h * HD + 64 * a, qrow);
         }
-        ptx::bulk_load(sLD + st * 2 * BQB, lse + h * T + row0 + q0, BQB * 4, &qd_full[st]);
-        ptx::bulk_load(sLD + st * 2 * BQB + BQB, Dv + h * T + row0 + q0, BQB * 4, &qd_full[st]);
+        ptx::bulk_load(sLD + st * 2 * BQB, lse + li, BQB * 4, &qd_full[st]);
+        ptx::bulk_load(sLD + st * 2 * BQB + BQB, Dv + li, BQB * 4, &qd_full[st]);
       }
     }
   } else if (warp == 1) {
@@ -508,7 +573,7 @@ __global__ void __launch_bounds__(192, 1)
     const float sl2 = d.scale * kLog2e;
     for (int it = 0; it < n_it; ++it) {
       const int st = it & 1;
-      const int q0 = (qb0 + it % per_head) * BQB;
+      const int q0 = (qb0 + (it % per_step) % per_head) * BQB;
       ptx::mbar_wait(&s_full[st], (it >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t sv[2][32], pv[2][32];
@@ -577,7 +642,7 @@ __global__ void __launch_bounds__(192, 1)
                           ptx::pack_bf16x2(__uint_as_float(o[i + 4]), __uint_as_float(o[i + 5])),
                           ptx::pack_bf16x2(__uint_as_float(o[i + 6]), __uint_as_float(o[i + 7])));
     }
-    store_grad_row<HD>(tdK + lane_off, kp, d.scale, d, (row0 + key) % d.S);
+    store_grad_row<HD>(tdK + lane_off, kp, d.scale, d, (row0 + key) % d.S + d.pos_off);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -609,7 +674,8 @@ __global__ void __launch_bounds__(192, 1)
     attn_bwd_q_tc_kernel(const __grid_constant__ CUtensorMap tm_kv,  // qkv, box {64,128}
                          const __grid_constant__ CUtensorMap tm_do,  // dO,  box {64,128}
                          const float* __restrict__ lse, const float* __restrict__ Dv,
-                         __nv_bfloat16* __restrict__ dqkv, Dims d) {
+                         const float* __restrict__ dq_add, __nv_bfloat16* __restrict__ dqkv,
+                         Dims d) {
   using L = QSmem<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -661,7 +727,7 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_arrive_expect_tx(q_full, 2 * L::T128);
       for (int a = 0; a < A; ++a) {
         ptx::tma_load_2d(&tm_kv, q_full, smem + L::OFF_Q + a * TILE, h * HD + 64 * a,
-                         row0 + qb * BQ);
+                         static_cast<int>(d.q_row_off) + row0 + qb * BQ);
         ptx::tma_load_2d(&tm_do, q_full, smem + L::OFF_DO + a * TILE, h * HD + 64 * a,
                          row0 + qb * BQ);
       }
@@ -757,7 +823,9 @@ __global__ void __launch_bounds__(192, 1)
     ptx::mbar_wait(all_done, 0);
     ptx::tc_fence_after();
     __nv_bfloat16* qp = dqkv + static_cast<long long>(row0 + q) * d.NQ + h * HD;
-    store_grad_row<HD>(tdQ + lane_off, qp, d.scale, d, (row0 + q) % d.S);
+    const float* addp =
+        dq_add ? dq_add + static_cast<long long>(row0 + q) * d.Q + h * HD : nullptr;
+    store_grad_row<HD>(tdQ + lane_off, qp, d.scale, d, (row0 + q) % d.S + d.pos_off, addp);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -793,27 +861,167 @@ void forward_tc(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const Di
     forward_tc_t<64>(qkv, o, lse, d, tm, s);
 }
 
+namespace {
+// ---------------------------------------------------------------------------
+// Training-time-test cache entries of the backward (unroll step j >= 1), on
+// CUDA cores: one warp per (row t, KV head g), lanes hold HD/32 consecutive
+// columns.  For each query head of the group and each earlier step i <= j:
+// p = exp(q.k_i*scale - lse), ds = p (dO.v_i - D) scale; dq += ds k_i,
+// dk_i += ds q, dv_i += p dO (fp32 accumulators, fixed order: deterministic).
 template <int HD>
-void backward_tc_t(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
-                   const float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, cudaStream_t s) {
+__global__ void __launch_bounds__(256) attn_bwd_diag_kernel(
+    const __nv_bfloat16* __restrict__ qkv_all, const __nv_bfloat16* __restrict__ dout,
+    const float* __restrict__ lse, const float* __restrict__ Dv, float* __restrict__ dq_add,
+    float* __restrict__ dkv_acc, __nv_bfloat16* __restrict__ dqkv_step, Dims d) {
+  constexpr int E = HD / 32;
   const long long T = static_cast<long long>(d.B) * d.S;
-  const CUtensorMap kv = gemm::make_tensor_map(qkv, T, d.NQ, d.NQ, 64, 128);
-  const CUtensorMap q64 = gemm::make_tensor_map(qkv, T, d.NQ, d.NQ, 64, 64);
-  const CUtensorMap do64 = gemm::make_tensor_map(dout, T, d.Q, d.Q, 64, 64);
+  const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= T * d.nkv) return;
+  const long long t = w / d.nkv;
+  const int g = static_cast<int>(w % d.nkv);
+  const int rep = d.nh / d.nkv, j = d.n_diag;
+  const int c0 = lane * E;
+  const long long KV2 = 2ll * d.KV;
+  auto ld = [](const __nv_bfloat16* p, float (&f)[E]) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) f[e] = __bfloat162float(p[e]);
+  };
+  auto wsum = [](float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  for (int hh = 0; hh < rep; ++hh) {
+    const int h = g * rep + hh;
+    float q[E], dO[E], dq[E];
+    ld(qkv_all + (static_cast<long long>(j) * T + t) * d.NQ + h * HD + c0, q);
+    ld(dout + t * d.Q + h * HD + c0, dO);
+    const float l = lse[h * T + t], Dh = Dv[h * T + t];
+#pragma unroll
+    for (int e = 0; e < E; ++e) dq[e] = 0.f;
+    for (int i = 1; i <= j; ++i) {
+      const __nv_bfloat16* kr = qkv_all + (static_cast<long long>(i) * T + t) * d.NQ + d.Q + g * HD;
+      float k[E], v[E];
+      ld(kr + c0, k);
+      ld(kr + d.KV + c0, v);
+      float sd = 0.f, sp = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        sd += q[e] * k[e];
+        sp += dO[e] * v[e];
+      }
+      sd = wsum(sd);
+      sp = wsum(sp);
+      const float p = __expf(sd * d.scale - l);
+      const float ds = p * (sp - Dh) * d.scale;
+      float* acc = dkv_acc + (static_cast<long long>(i) * T + t) * KV2 + g * HD + c0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        dq[e] += ds * k[e];
+        acc[e] += ds * q[e];
+        acc[d.KV + e] += p * dO[e];
+      }
+    }
+    float* dqa = dq_add + t * d.Q + h * HD + c0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dqa[e] = dq[e];
+  }
+  // step j's k / v receive no further contributions: round, inverse-rotate
+  // k (position t % S + j; partner column c +- HD/2 lives 16 lanes away),
+  // round, store into the GEMM operand
+  const float* acc = dkv_acc + (static_cast<long long>(j) * T + t) * KV2 + g * HD + c0;
+  __nv_bfloat16* kd = dqkv_step + t * d.NQ + d.Q + g * HD + c0;
+  const long long L = d.rope_len > 0 ? d.rope_len : d.S;
+  const int pos = static_cast<int>(t % d.S) + j;
+  const bool lo = lane < 16;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const float x = __bfloat162float(__float2bfloat16_rn(acc[e]));
+    const float y = __shfl_xor_sync(0xffffffffu, x, 16);
+    float r = x;
+    if (d.rope_cos != nullptr) {
+      const int i = (lane & 15) * E + e;  // rotation index in [0, HD/2)
+      const float cv = __ldg(d.rope_cos + i * L + pos), sv = __ldg(d.rope_sin + i * L + pos);
+      r = lo ? x * cv + y * sv : x * cv - y * sv;  // lo: x1' = x1 c + x2 s; hi: x2' = x2 c - x1 s
+    }
+    kd[e] = __float2bfloat16_rn(r);
+    kd[d.KV + e] = __float2bfloat16_rn(acc[d.KV + e]);
+  }
+}
+
+}  // namespace
+
+template <int HD>
+void bwd_dq_t(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const float* lse,
+              const float* D, const float* dq_add, __nv_bfloat16* dqkv_step, const Dims& d,
+              cudaStream_t s) {
+  const long long T = static_cast<long long>(d.B) * d.S;
+  const CUtensorMap kv = gemm::make_tensor_map(qkv_all, d.q_row_off + T, d.NQ, d.NQ, 64, 128);
   const CUtensorMap do128 = gemm::make_tensor_map(dout, T, d.Q, d.Q, 64, 128);
-  count_launches(2);
-  attn_bwd_kv_tc_kernel<HD><<<dim3(d.S / BKV, d.nkv, d.B), 192, KvSmem<HD>::BYTES, s>>>(
-      kv, q64, do64, lse, Dbuf, dqkv, d);
+  count_launches();
   attn_bwd_q_tc_kernel<HD><<<dim3(d.S / BQ, d.nh, d.B), 192, QSmem<HD>::BYTES, s>>>(
-      kv, do128, lse, Dbuf, dqkv, d);
+      kv, do128, lse, D, dq_add, dqkv_step, d);
+}
+
+template <int HD>
+void bwd_dkdv_t(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout_all, const float* lse_all,
+                const float* D_all, __nv_bfloat16* dqkv0, const Dims& d, int n_steps,
+                cudaStream_t s) {
+  const long long T = static_cast<long long>(d.B) * d.S;
+  const CUtensorMap kv = gemm::make_tensor_map(qkv_all, T, d.NQ, d.NQ, 64, 128);
+  const CUtensorMap q64 = gemm::make_tensor_map(qkv_all, n_steps * T, d.NQ, d.NQ, 64, 64);
+  const CUtensorMap do64 = gemm::make_tensor_map(dout_all, n_steps * T, d.Q, d.Q, 64, 64);
+  count_launches();
+  attn_bwd_kv_tc_kernel<HD><<<dim3(d.S / BKV, d.nkv, d.B), 192, KvSmem<HD>::BYTES, s>>>(
+      kv, q64, do64, lse_all, D_all, dqkv0, d, n_steps);
 }
 
 void backward_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
                  const float* Dbuf, __nv_bfloat16* dqkv, const Dims& d, int hd, cudaStream_t s) {
+  if (hd == 128) {
+    bwd_dkdv_t<128>(qkv, dout, lse, Dbuf, dqkv, d, 1, s);
+    bwd_dq_t<128>(qkv, dout, lse, Dbuf, nullptr, dqkv, d, s);
+  } else {
+    bwd_dkdv_t<64>(qkv, dout, lse, Dbuf, dqkv, d, 1, s);
+    bwd_dq_t<64>(qkv, dout, lse, Dbuf, nullptr, dqkv, d, s);
+  }
+}
+
+void bwd_diag(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const float* lse,
+              const float* D, float* dq_add, float* dkv_acc, __nv_bfloat16* dqkv_step,
+              const Dims& d, int hd, cudaStream_t s) {
+  if (d.n_diag < 1 || d.n_diag > kMaxDiag)
+    throw std::invalid_argument("bwd_diag: n_diag must be in [1, 15]");
+  const long long warps = static_cast<long long>(d.B) * d.S * d.nkv;
+  const unsigned blocks = static_cast<unsigned>((warps * 32 + 255) / 256);
+  count_launches();
   if (hd == 128)
-    backward_tc_t<128>(qkv, dout, lse, Dbuf, dqkv, d, s);
+    attn_bwd_diag_kernel<128><<<blocks, 256, 0, s>>>(qkv_all, dout, lse, D, dq_add, dkv_acc,
+                                                     dqkv_step, d);
   else
-    backward_tc_t<64>(qkv, dout, lse, Dbuf, dqkv, d, s);
+    attn_bwd_diag_kernel<64><<<blocks, 256, 0, s>>>(qkv_all, dout, lse, D, dq_add, dkv_acc,
+                                                    dqkv_step, d);
+}
+
+void bwd_dq(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const float* lse,
+            const float* D, const float* dq_add, __nv_bfloat16* dqkv_step, const Dims& d, int hd,
+            cudaStream_t s) {
+  if (d.S % BQ) throw std::invalid_argument("bwd_dq: seq_len must be a multiple of 128");
+  if (hd == 128)
+    bwd_dq_t<128>(qkv_all, dout, lse, D, dq_add, dqkv_step, d, s);
+  else
+    bwd_dq_t<64>(qkv_all, dout, lse, D, dq_add, dqkv_step, d, s);
+}
+
+void bwd_dkdv(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout_all, const float* lse_all,
+              const float* D_all, __nv_bfloat16* dqkv0, const Dims& d, int hd, int n_steps,
+              cudaStream_t s) {
+  if (d.S % BKV) throw std::invalid_argument("bwd_dkdv: seq_len must be a multiple of 128");
+  if (hd == 128)
+    bwd_dkdv_t<128>(qkv_all, dout_all, lse_all, D_all, dqkv0, d, n_steps, s);
+  else
+    bwd_dkdv_t<64>(qkv_all, dout_all, lse_all, D_all, dqkv0, d, n_steps, s);
 }
 
 template <int HD>

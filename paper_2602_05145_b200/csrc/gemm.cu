@@ -208,8 +208,12 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   }
   if (epi == EPI_BF16_ROPE) {
     if (!p.args.rope_cos || !p.args.rope_sin || p.args.rope_S <= 0 ||
-        (p.args.rope_hd != 64 && p.args.rope_hd != 128) || p.args.rope_cols % p.args.rope_hd)
+        (p.args.rope_hd != 64 && p.args.rope_hd != 128) || p.args.rope_cols % p.args.rope_hd ||
+        p.args.rope_pos_off < 0)
       throw std::invalid_argument("gemm: bad RoPE epilogue arguments");
+    if (p.args.rope_ld == 0) p.args.rope_ld = p.args.rope_S;
+    if (p.args.rope_ld < p.args.rope_S + p.args.rope_pos_off)
+      throw std::invalid_argument("gemm: RoPE table shorter than rope_S + rope_pos_off");
   }
   if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
       epi == EPI_F32_ACC || epi == EPI_BF16_ROPE) {

@@ -334,15 +334,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_ld_wait();
         const int colh = n0 + c_begin;  // first column of this half tile
         if (row_ok && colh < args.N) {
-          const int pos = row % args.rope_S;
+          const int pos = row % args.rope_S + args.rope_pos_off;
           auto rot = [&](float& a, float& b, float cs, float sn) {
             const float x1 = __bfloat162float(__float2bfloat16_rn(a));
             const float x2 = __bfloat162float(__float2bfloat16_rn(b));
             a = x1 * cs - x2 * sn;
             b = x2 * cs + x1 * sn;
           };
-          const long long S = args.rope_S;
-          // tables [hd/2, S]: lanes hold consecutive rows, so each load is coalesced
+          const long long S = args.rope_ld;
+          // tables [hd/2, rope_ld]: lanes hold consecutive rows, so each load is coalesced
           if (args.rope_hd == 128) {
             if (colh < args.rope_cols) {
 #pragma unroll

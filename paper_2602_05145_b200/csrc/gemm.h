@@ -63,10 +63,12 @@ struct Args {
   __nv_bfloat16* opt_p16;
   float* opt_g;  // optional gradient store (nullable)
   const AdamDev* opt_hp;
-  // RoPE epilogue: row r is position r % rope_S; tables transposed [rope_hd / 2, rope_S]
+  // RoPE epilogue: row r is position r % rope_S + rope_pos_off (training-time-test
+  // unroll step); tables transposed [rope_hd / 2, rope_ld] (rope_ld 0 -> rope_S)
   const float* rope_cos;
   const float* rope_sin;
   int rope_S, rope_cols, rope_hd;
+  int rope_pos_off, rope_ld;
 };
 
 // A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).

@@ -37,7 +37,7 @@ unsigned blocks_for(long long n, int per_block) {
 // ------------------------------------------------------------ batch gather
 __global__ void gather_batch_kernel(const uint4* __restrict__ ring_feat,
                                     const int32_t* __restrict__ ring_ids, long long cap, int W8,
-                                    const BatchSpec* __restrict__ specp, int S,
+                                    const BatchSpec* __restrict__ specp, int S, int K,
                                     uint4* __restrict__ F, int32_t* __restrict__ u,
                                     int32_t* __restrict__ y, int32_t* __restrict__ m) {
   const long long row = blockIdx.x;
@@ -53,11 +53,13 @@ __global__ void gather_batch_kernel(const uint4* __restrict__ ring_feat,
     const uint4 z = make_uint4(0, 0, 0, 0);
     for (int i = threadIdx.x; i < W8; i += blockDim.x) dst[i] = z;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < K) {
+    const int j = threadIdx.x;
     const long long base = b < spec.n ? spec.start[b] : 0;
-    u[row] = (t + 1 < L) ? ring_ids[(base + t + 1) % cap] : 0;
-    y[row] = (t + 2 < L) ? ring_ids[(base + t + 2) % cap] : 0;
-    m[row] = (t + 2 < L) ? 1 : 0;
+    const long long r = static_cast<long long>(j) * gridDim.x + row;
+    u[r] = (t + 1 + j < L) ? ring_ids[(base + t + 1 + j) % cap] : 0;
+    y[r] = (t + 2 + j < L) ? ring_ids[(base + t + 2 + j) % cap] : 0;
+    m[r] = (t + 2 + j < L) ? 1 : 0;
   }
 }
 
@@ -82,11 +84,11 @@ __global__ void select_count_kernel(const long long* __restrict__ o, const long 
 }
 
 __global__ void ce_coef_kernel(const int32_t* __restrict__ m, const long long* __restrict__ n,
-                               float* __restrict__ coef, long long T) {
+                               float* __restrict__ coef, StepWeights sw) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= T) return;
+  if (i >= sw.K * sw.T) return;
   const long long N = *n > 0 ? *n : 1;
-  coef[i] = m[i] ? static_cast<float>(1.0 / static_cast<double>(N)) : 0.f;
+  coef[i] = m[i] ? static_cast<float>(1.0 / static_cast<double>(N)) * sw.w[i / sw.T] : 0.f;
 }
 
 // ------------------------------------------------------------ RMSNorm fwd
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
       }
     }
   }
+  if (!dw_part) return;
   float4* dp = reinterpret_cast<float4*>(dw_part + static_cast<long long>(blockIdx.x) * H);
 #pragma unroll
   for (int k = 0; k < kMaxChunks; ++k) {
@@ -376,40 +379,54 @@ __global__ void __launch_bounds__(256) ce_reduce_kernel(
 __global__ void ce_finalize_kernel(const float* __restrict__ row_loss,
                                    const int32_t* __restrict__ argmax,
                                    const int32_t* __restrict__ y, const int32_t* __restrict__ m,
-                                   const long long* __restrict__ n_global, long long T,
+                                   const long long* __restrict__ n_global, StepWeights sw,
                                    double* __restrict__ stats) {
   __shared__ double sl[32], sv[32], sc[32];
-  double l = 0.0, v = 0.0, c = 0.0;
-  for (long long i = threadIdx.x; i < T; i += blockDim.x) {
-    l += row_loss[i];
-    if (m[i]) {
-      v += 1.0;
-      c += (argmax[i] == y[i]) ? 1.0 : 0.0;
+  __shared__ double step_loss[kMaxTtt];
+  const long long T = sw.T;
+  for (int j = 0; j < sw.K; ++j) {
+    double l = 0.0, v = 0.0, c = 0.0;
+    const long long r0 = static_cast<long long>(j) * T;
+    for (long long i = threadIdx.x; i < T; i += blockDim.x) {
+      l += row_loss[r0 + i];
+      if (j == 0 && m[i]) {
+        v += 1.0;
+        c += (argmax[i] == y[i]) ? 1.0 : 0.0;
+      }
     }
-  }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    l += __shfl_xor_sync(0xffffffff, l, o);
-    v += __shfl_xor_sync(0xffffffff, v, o);
-    c += __shfl_xor_sync(0xffffffff, c, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    sl[threadIdx.x >> 5] = l;
-    sv[threadIdx.x >> 5] = v;
-    sc[threadIdx.x >> 5] = c;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double L = 0, V = 0, Cc = 0;
-    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
-      L += sl[i];
-      V += sv[i];
-      Cc += sc[i];
+    for (int o = 16; o; o >>= 1) {
+      l += __shfl_xor_sync(0xffffffff, l, o);
+      v += __shfl_xor_sync(0xffffffff, v, o);
+      c += __shfl_xor_sync(0xffffffff, c, o);
     }
+    if ((threadIdx.x & 31) == 0) {
+      sl[threadIdx.x >> 5] = l;
+      sv[threadIdx.x >> 5] = v;
+      sc[threadIdx.x >> 5] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double L = 0, V = 0, Cc = 0;
+      for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+        L += sl[i];
+        V += sv[i];
+        Cc += sc[i];
+      }
+      step_loss[j] = L;
+      if (j == 0) {
+        stats[1] = V;
+        stats[2] = Cc;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double V = stats[1];
     const double N = *n_global > 0 ? static_cast<double>(*n_global) : (V > 0 ? V : 1.0);
-    stats[0] = L / N;
-    stats[1] = V;
-    stats[2] = Cc;
+    double total = 0.0;
+    for (int j = 0; j < sw.K; ++j) total += static_cast<double>(sw.w[j]) * (step_loss[j] / N);
+    stats[0] = total;
   }
 }
 
@@ -503,12 +520,12 @@ __global__ void ce_grad_kernel(const float* __restrict__ logits, long long ldl,
 
 // ============================================================== launchers
 void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long long cap, int W,
-                  const BatchSpec* spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
-                  int32_t* m, cudaStream_t s) {
+                  const BatchSpec* spec, int B, int S, int K, __nv_bfloat16* F, int32_t* u,
+                  int32_t* y, int32_t* m, cudaStream_t s) {
   const long long T = static_cast<long long>(B) * S;
   count_launches();
   gather_batch_kernel<<<static_cast<unsigned>(T), 256, 0, s>>>(
-      reinterpret_cast<const uint4*>(ring_feat), ring_ids, cap, W / 8, spec, S,
+      reinterpret_cast<const uint4*>(ring_feat), ring_ids, cap, W / 8, spec, S, K,
       reinterpret_cast<uint4*>(F), u, y, m);
 }
 
@@ -523,10 +540,10 @@ void select_count(const long long* override_n, const long long* counted, long lo
   select_count_kernel<<<1, 1, 0, s>>>(override_n, counted, n_global);
 }
 
-void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T,
+void ce_coef(const int32_t* m, const long long* n_global, float* coef, const StepWeights& sw,
              cudaStream_t s) {
   count_launches();
-  ce_coef_kernel<<<blocks_for(T, 256), 256, 0, s>>>(m, n_global, coef, T);
+  ce_coef_kernel<<<blocks_for(sw.K * sw.T, 256), 256, 0, s>>>(m, n_global, coef, sw);
 }
 
 void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, const float* w,
@@ -555,7 +572,8 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
   const unsigned g = static_cast<unsigned>(nb);
 #define SPECSIM_RMS_BWD(C)                                                                     \
   rmsnorm_bwd_kernel<C><<<g, kNormThreads, 0, s>>>(dy, lddy, x, ldx, gather, w, rstd, resid, \
-                                                   out_f32, out_bf16, ldo, dw_partial, T, H)
+                                                   out_f32, out_bf16, ldo,                   \
+                                                   dw ? dw_partial : nullptr, T, H)
   if (H <= 1024)
     SPECSIM_RMS_BWD(1);
   else if (H <= 2048)
@@ -565,6 +583,7 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
   else
     SPECSIM_RMS_BWD(8);
 #undef SPECSIM_RMS_BWD
+  if (!dw) return;
   count_launches();
   colsum_kernel<<<blocks_for(H, 32), 256, 0, s>>>(dw_partial, nb, H, dw);
 }
@@ -605,9 +624,9 @@ void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const i
 }
 
 void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,
-                 const long long* n_global, long long T, double* stats, cudaStream_t s) {
+                 const long long* n_global, const StepWeights& sw, double* stats, cudaStream_t s) {
   count_launches();
-  ce_finalize_kernel<<<1, 1024, 0, s>>>(row_loss, argmax, y, m, n_global, T, stats);
+  ce_finalize_kernel<<<1, 1024, 0, s>>>(row_loss, argmax, y, m, n_global, sw, stats);
 }
 
 void adamw(long long n, float* p, float* m, float* v, const float* g, __nv_bfloat16* p16,

@@ -15,6 +15,14 @@ namespace specsim {
 namespace kern {
 
 constexpr int kMaxBatch = 64;
+constexpr int kMaxTtt = 16;  // training-time-test unroll steps
+
+// Rows of K unroll steps are stacked [K][T]; step j's loss weight is w[j] = decay^j.
+struct StepWeights {
+  float w[kMaxTtt];
+  int K;
+  long long T;  // rows per step
+};
 
 // One micro-batch: sample b's tokens live at ring rows (start[b] + t) % cap.
 struct BatchSpec {
@@ -23,14 +31,18 @@ struct BatchSpec {
   int len[kMaxBatch];          // L (tokens)
 };
 
-// F[T, W] bf16, u/y int32, mask int32 (SURVEY A.2 alignment).
+// F[T, W] bf16, u/y int32, mask int32 (SURVEY A.2 alignment).  u / y / m hold
+// K slices of T rows: slice j is the rule shifted by j tokens (training-time
+// test), u = x[t+1+j], y = x[t+2+j], m = [t+2+j < L].
 // spec lives in device memory (so the launch can sit in a CUDA graph)
 void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long long cap, int W,
-                  const BatchSpec* spec, int B, int S, __nv_bfloat16* F, int32_t* u, int32_t* y,
-                  int32_t* m, cudaStream_t s);
+                  const BatchSpec* spec, int B, int S, int K, __nv_bfloat16* F, int32_t* u,
+                  int32_t* y, int32_t* m, cudaStream_t s);
 
-// coef[t] = m[t] / n_global ; n_global read from device scalar (int64)
-void ce_coef(const int32_t* m, const long long* n_global, float* coef, long long T, cudaStream_t s);
+// coef[r] = m[r] / n_global * w[r / T] over K*T rows; n_global read from a
+// device scalar (int64)
+void ce_coef(const int32_t* m, const long long* n_global, float* coef, const StepWeights& sw,
+             cudaStream_t s);
 // count of mask (int64 device scalar)
 void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s);
 // n_global = override > 0 ? override : counted
@@ -45,7 +57,7 @@ void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, c
 // dx = rstd*(dy*w) - x*rstd^3*mean(dy*w*x);  out_f32 = resid + dx (resid nullable),
 // out_bf16 = bf16(out_f32) (nullable); dx skipped entirely when both outputs null.
 // dw[i] = sum_t dy*x*rstd (deterministic two-pass; dw_partial scratch
-// [ceil(T/rows_per_block), H]).  x may be gathered (embedding rows).
+// [ceil(T/rows_per_block), H]); dw nullable.  x may be gathered (embedding rows).
 void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long long ldx,
                  const int32_t* gather, const float* w, const float* rstd, const float* resid,
                  float* out_f32, __nv_bfloat16* out_bf16, long long ldo, float* dw,
@@ -71,10 +83,11 @@ void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const i
 void ce_grad(const float* logits, long long ldl, const float* lse, const float* coef,
              const int32_t* y, int v0, long long T, int vn, __nv_bfloat16* dlog, long long ldd,
              cudaStream_t s);
-// stats[0] = sum row_loss / n_global (double), stats[1] = valid (as double),
-// stats[2] = top-1 correct.  Single block, fixed order.
+// stats[0] = sum_j w[j] * (sum of step j's row_loss / n_global) (double),
+// stats[1] = valid (as double), stats[2] = top-1 correct, both of step 0.
+// Single block, fixed order.
 void ce_finalize(const float* row_loss, const int32_t* argmax, const int32_t* y, const int32_t* m,
-                 const long long* n_global, long long T, double* stats, cudaStream_t s);
+                 const long long* n_global, const StepWeights& sw, double* stats, cudaStream_t s);
 
 // PyTorch AdamW on flat fp32 state; writes the bf16 working copy.
 struct AdamHyper {

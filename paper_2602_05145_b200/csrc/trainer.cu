@@ -97,6 +97,10 @@ void DraftShape::validate() const {
   p.check(micro_batch >= 1 && micro_batch <= kern::kMaxBatch, "micro_batch must be in [1, 64]");
   p.check(rms_eps > 0.f, "rms_eps must be > 0");
   p.check(rope_theta > 0.0, "rope_theta must be > 0");
+  p.check(ttt_steps >= 1 && ttt_steps <= kern::kMaxTtt, "ttt_steps must be in [1, 16]");
+  p.check(ttt_steps == 1 || seq_len % 128 == 0,
+          "ttt_steps > 1 needs seq_len % 128 == 0 (tcgen05 attention)");
+  p.check(ttt_decay > 0.f && ttt_decay <= 1.f, "ttt_decay must be in (0, 1]");
   p.throw_if_any();
 }
 
@@ -113,6 +117,11 @@ class DraftTrainerImpl {
   int rank, world, device;
   long long T, H, Q, KV, NQ, I, V, W3, Vc;
   int n_chunks;
+  // training-time-test unroll: K decoder passes; per-pass buffers are stacked
+  // [K][T]; sw = loss weights over the K*T logit rows, sw1 = pass 0 only (eval)
+  int K = 1;
+  long long KT = 0;
+  kern::StepWeights sw{}, sw1{};
   std::vector<Param> params;
   long long total = 0;
   int64_t step_count = 0;
@@ -139,7 +148,8 @@ class DraftTrainerImpl {
   __nv_bfloat16* E = nullptr;  // frozen embedding [V, H]
   float *cos_t = nullptr, *sin_t = nullptr;    // [S, hd/2] (standalone RoPE kernel)
   float *cos_tr = nullptr, *sin_tr = nullptr;  // [hd/2, S] (fused epilogues: lane = position)
-  // activations
+  // activations ([K][T] stacked per unroll pass; g is [K+1][T, H]: g[0] =
+  // W_fc f, g[j+1] = h_j = the input of pass j+1, so h = g + T*H)
   __nv_bfloat16 *F, *g, *U, *qkv, *o, *r, *z, *gu, *act, *h, *nrm;
   int32_t *u, *y, *m, *argmax;
   float *coef, *rstd_a, *rstd_b, *lse_attn, *rstd_post, *rstd_fin, *lse, *row_loss;
@@ -151,6 +161,9 @@ class DraftTrainerImpl {
   bool keep_logits = false;
   __nv_bfloat16 *dlog, *dh_b, *dact, *dgu, *dr_b, *dO, *dqkv, *dg_b;
   float *dn, *dh, *dz, *dr, *dU, *Dattn, *dw_part;
+  // K > 1: fp32 gradient w.r.t. the pass input (flows into the previous pass's
+  // output), the cache part of dq, and the k | v accumulators of passes >= 1
+  float *dg_in = nullptr, *dq_add = nullptr, *dkv_acc = nullptr;
   // pinned host scalars
   long long* h_nglobal = nullptr;
   double* h_stats = nullptr;
@@ -171,10 +184,13 @@ class DraftTrainerImpl {
   gemm::AdamDev* adam_dev = nullptr;  // = &d_in->hp
   bool keep_grads = false;            // materialise fp32 grads in the fused-AdamW path
 
-  // GEMM plans
-  gemm::GemmPlan p_fc, p_qkv, p_o, p_gu, p_down, p_ce_fwd;
+  // GEMM plans (vectors: one per unroll pass; LM head and weight gradients
+  // span all K*T rows)
+  gemm::GemmPlan p_fc, p_ce_fwd, p_ce_fwd_eval;
+  std::vector<gemm::GemmPlan> p_qkv, p_o, p_gu, p_down;
   std::vector<gemm::GemmPlan> p_ce_bwd, p_lm_dx, p_lm_dw;
-  gemm::GemmPlan p_dact, p_dw_down, p_dz, p_dw_gu, p_dO, p_dw_o, p_dU, p_dw_qkv, p_dw_fc;
+  std::vector<gemm::GemmPlan> p_dact, p_dz, p_dO, p_dU;
+  gemm::GemmPlan p_dw_down, p_dw_gu, p_dw_o, p_dw_qkv, p_dw_fc;
   // weight-gradient GEMMs with the AdamW update fused into the epilogue
   // (single-replica path: no all-reduce between gradient and update)
   std::vector<gemm::GemmPlan> f_lm_dw;
@@ -246,6 +262,14 @@ class DraftTrainerImpl {
     I = sh.ffn;
     V = sh.vocab;
     W3 = static_cast<long long>(sh.layers_tapped) * H;
+    K = sh.ttt_steps;
+    KT = K * T;
+    sw.K = K;
+    sw.T = T;
+    for (int j = 0; j < K; ++j)
+      sw.w[j] = static_cast<float>(std::pow(static_cast<double>(sh.ttt_decay), j));
+    sw1 = sw;
+    sw1.K = 1;
     // vocabulary chunk for the backward: multiple of the GEMM N tile, ~32k
     Vc = std::min<long long>(V, 32768);
     Vc = (Vc + gemm::BN - 1) / gemm::BN * gemm::BN;
@@ -278,60 +302,65 @@ class DraftTrainerImpl {
     arena.reserve(&E, V * H);
     arena.reserve(&cos_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
     arena.reserve(&sin_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
-    arena.reserve(&cos_tr, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
-    arena.reserve(&sin_tr, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
+    arena.reserve(&cos_tr, rope_len() * sh.head_dim / 2);
+    arena.reserve(&sin_tr, rope_len() * sh.head_dim / 2);
     arena.reserve(&F, T * W3);
-    arena.reserve(&g, T * H);
-    arena.reserve(&U, T * 2 * H);
-    arena.reserve(&qkv, T * NQ);
-    arena.reserve(&o, T * Q);
-    arena.reserve(&r, T * H);
-    arena.reserve(&z, T * H);
-    arena.reserve(&gu, T * 2 * I);
-    arena.reserve(&act, T * I);
-    arena.reserve(&h, T * H);
-    arena.reserve(&nrm, T * H);
-    arena.reserve(&u, T);
-    arena.reserve(&y, T);
-    arena.reserve(&m, T);
-    arena.reserve(&argmax, T);
-    arena.reserve(&coef, T);
-    arena.reserve(&rstd_a, T);
-    arena.reserve(&rstd_b, T);
-    arena.reserve(&lse_attn, T * sh.n_heads);
-    arena.reserve(&rstd_post, T);
-    arena.reserve(&rstd_fin, T);
-    arena.reserve(&lse, T);
-    arena.reserve(&row_loss, T);
-    arena.reserve(&partials, 2 * nb_ce * T);
+    arena.reserve(&g, (K + 1) * T * H);
+    arena.reserve(&U, KT * 2 * H);
+    arena.reserve(&qkv, KT * NQ);
+    arena.reserve(&o, KT * Q);
+    arena.reserve(&r, KT * H);
+    arena.reserve(&z, KT * H);
+    arena.reserve(&gu, KT * 2 * I);
+    arena.reserve(&act, KT * I);
+    arena.reserve(&nrm, KT * H);
+    arena.reserve(&u, KT);
+    arena.reserve(&y, KT);
+    arena.reserve(&m, KT);
+    arena.reserve(&argmax, KT);
+    arena.reserve(&coef, KT);
+    arena.reserve(&rstd_a, KT);
+    arena.reserve(&rstd_b, KT);
+    arena.reserve(&lse_attn, KT * sh.n_heads);
+    arena.reserve(&rstd_post, KT);
+    arena.reserve(&rstd_fin, KT);
+    arena.reserve(&lse, KT);
+    arena.reserve(&row_loss, KT);
+    arena.reserve(&partials, 2 * nb_ce * KT);
     arena.reserve(&n_global, 2);
     arena.reserve(&stats, 4);
-    arena.reserve(&dlog, T * Vc);
+    arena.reserve(&dlog, KT * Vc);
     // fp32 logits [T, V] kept from the forward so the backward needs no logit
     // recompute (4.2 GB at C2); SPECSIM_CE_RECOMPUTE=1 or a > 32 GB table
     // selects the recompute path instead
     {
       const char* e = std::getenv("SPECSIM_CE_RECOMPUTE");
-      keep_logits = !(e && e[0] == '1') && T * V * 4 <= (32ll << 30);
-      if (keep_logits) arena.reserve(&logits, T * V);
+      keep_logits = !(e && e[0] == '1') && KT * V * 4 <= (32ll << 30);
+      if (keep_logits) arena.reserve(&logits, KT * V);
     }
-    arena.reserve(&dh_b, T * H);
+    arena.reserve(&dh_b, KT * H);
     arena.reserve(&dact, T * I);
-    arena.reserve(&dgu, T * 2 * I);
-    arena.reserve(&dr_b, T * H);
-    arena.reserve(&dO, T * Q);
-    arena.reserve(&dqkv, T * NQ);
+    arena.reserve(&dgu, KT * 2 * I);
+    arena.reserve(&dr_b, KT * H);
+    arena.reserve(&dO, KT * Q);
+    arena.reserve(&dqkv, KT * NQ);
     arena.reserve(&dg_b, T * H);
-    arena.reserve(&dn, T * H);
+    arena.reserve(&dn, KT * H);
     arena.reserve(&dh, T * H);
-    arena.reserve(&dz, T * H);
+    arena.reserve(&dz, KT * H);
     arena.reserve(&dr, T * H);
-    arena.reserve(&dU, T * 2 * H);
-    arena.reserve(&Dattn, T * sh.n_heads);
-    arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(T) * H);
+    arena.reserve(&dU, KT * 2 * H);
+    arena.reserve(&Dattn, KT * sh.n_heads);
+    arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(KT) * H);
+    if (K > 1) {
+      arena.reserve(&dg_in, T * H);
+      arena.reserve(&dq_add, T * Q);
+      arena.reserve(&dkv_acc, KT * 2 * KV);
+    }
     arena.reserve(&d_in, 1);
     arena.reserve(&n_counted, 1);
     arena.commit();
+    h = g + T * H;
     adam_dev = &d_in->hp;
     SPECSIM_CUDA(cudaMallocHost(&h_in, 2 * sizeof(StepInputs)));
     std::memset(h_in, 0, 2 * sizeof(StepInputs));
@@ -442,24 +471,30 @@ class DraftTrainerImpl {
     SPECSIM_CHECK_LAUNCH();
   }
 
+  // positions covered by the RoPE tables: pass j rotates row t at t % S + j
+  long long rope_len() const { return static_cast<long long>(sh.seq_len) + K - 1; }
+
   void init_rope() {
     // NeoX rotate-half tables, angle = pos * theta^(-2i/hd) in double
     const int half = sh.head_dim / 2;
-    std::vector<float> c(static_cast<size_t>(sh.seq_len) * half), s(c.size());
-    for (int pos = 0; pos < sh.seq_len; ++pos)
+    const int npos = static_cast<int>(rope_len());
+    std::vector<float> c(static_cast<size_t>(npos) * half), s(c.size());
+    for (int pos = 0; pos < npos; ++pos)
       for (int i = 0; i < half; ++i) {
         const double inv = std::pow(sh.rope_theta, -2.0 * i / sh.head_dim);
         const double ang = static_cast<double>(pos) * inv;
         c[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::cos(ang));
         s[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::sin(ang));
       }
-    SPECSIM_CUDA(cudaMemcpy(cos_t, c.data(), sizeof(float) * c.size(), cudaMemcpyHostToDevice));
-    SPECSIM_CUDA(cudaMemcpy(sin_t, s.data(), sizeof(float) * s.size(), cudaMemcpyHostToDevice));
+    // [S, hd/2] (standalone kernel, single pass only): the first S positions
+    const size_t n_std = static_cast<size_t>(sh.seq_len) * half;
+    SPECSIM_CUDA(cudaMemcpy(cos_t, c.data(), sizeof(float) * n_std, cudaMemcpyHostToDevice));
+    SPECSIM_CUDA(cudaMemcpy(sin_t, s.data(), sizeof(float) * n_std, cudaMemcpyHostToDevice));
     std::vector<float> ct(c.size()), st(c.size());
-    for (int pos = 0; pos < sh.seq_len; ++pos)
+    for (int pos = 0; pos < npos; ++pos)
       for (int i = 0; i < half; ++i) {
-        ct[static_cast<size_t>(i) * sh.seq_len + pos] = c[static_cast<size_t>(pos) * half + i];
-        st[static_cast<size_t>(i) * sh.seq_len + pos] = s[static_cast<size_t>(pos) * half + i];
+        ct[static_cast<size_t>(i) * npos + pos] = c[static_cast<size_t>(pos) * half + i];
+        st[static_cast<size_t>(i) * npos + pos] = s[static_cast<size_t>(pos) * half + i];
       }
     SPECSIM_CUDA(cudaMemcpy(cos_tr, ct.data(), sizeof(float) * ct.size(), cudaMemcpyHostToDevice));
     SPECSIM_CUDA(cudaMemcpy(sin_tr, st.data(), sizeof(float) * st.size(), cudaMemcpyHostToDevice));
@@ -481,31 +516,43 @@ class DraftTrainerImpl {
     using namespace gemm;
     // forward: Y = X W^T (both K-major)
     p_fc = make_plan({F, W3, false}, {pb("fc"), W3, false}, T, H, W3, EPI_BF16, out_args(g, H));
-    // q / k heads rotated in the epilogue (NeoX RoPE); v columns stored as is
-    Args qa = out_args(qkv, NQ);
-    qa.rope_cos = cos_tr;
-    qa.rope_sin = sin_tr;
-    qa.rope_S = sh.seq_len;
-    qa.rope_cols = static_cast<int>(Q + KV);
-    qa.rope_hd = sh.head_dim;
-    p_qkv = make_plan({U, 2 * H, false}, {pb("qkv"), 2 * H, false}, T, NQ, 2 * H, EPI_BF16_ROPE,
-                      qa);
-    p_o = make_plan({o, Q, false}, {pb("o"), Q, false}, T, H, Q, EPI_BF16_RESID,
-                    out_args(r, H, g, H));
-    p_gu = make_plan({z, H, false}, {pb("gate_up"), H, false}, T, 2 * I, H, EPI_BF16,
-                     out_args(gu, 2 * I));
-    p_down = make_plan({act, I, false}, {pb("down"), I, false}, T, H, I, EPI_BF16_RESID,
-                       out_args(h, H, r, H));
-    Args ce{};
-    ce.targets = y;
-    ce.partials = partials;
-    if (keep_logits) {
-      ce.C = logits;
-      ce.ldc = V;
+    for (int j = 0; j < K; ++j) {
+      const long long R = j * T;  // first row of pass j in the stacked buffers
+      // q / k heads rotated in the epilogue (NeoX RoPE at t % S + j); v as is
+      Args qa = out_args(qkv + R * NQ, NQ);
+      qa.rope_cos = cos_tr;
+      qa.rope_sin = sin_tr;
+      qa.rope_S = sh.seq_len;
+      qa.rope_cols = static_cast<int>(Q + KV);
+      qa.rope_hd = sh.head_dim;
+      qa.rope_pos_off = j;
+      qa.rope_ld = static_cast<int>(rope_len());
+      p_qkv.push_back(make_plan({U + R * 2 * H, 2 * H, false}, {pb("qkv"), 2 * H, false}, T, NQ,
+                                2 * H, EPI_BF16_ROPE, qa));
+      // r_j = g_j + o_j W_o^T ; h_j (= g_{j+1}) = r_j + act_j W_d^T
+      p_o.push_back(make_plan({o + R * Q, Q, false}, {pb("o"), Q, false}, T, H, Q, EPI_BF16_RESID,
+                              out_args(r + R * H, H, g + R * H, H)));
+      p_gu.push_back(make_plan({z + R * H, H, false}, {pb("gate_up"), H, false}, T, 2 * I, H,
+                               EPI_BF16, out_args(gu + R * 2 * I, 2 * I)));
+      p_down.push_back(make_plan({act + R * I, I, false}, {pb("down"), I, false}, T, H, I,
+                                 EPI_BF16_RESID, out_args(h + R * H, H, r + R * H, H)));
     }
-    if (const char* e = std::getenv("SPECSIM_CE_L2_MB")) ce.l2_budget_mb = std::atoi(e);
-    p_ce_fwd = make_plan({nrm, H, false}, {pb("lm_head"), H, false}, T, V, H, EPI_CE_FWD, ce);
-    // LM head backward, vocabulary chunks
+    auto ce_fwd = [&](long long rows) {
+      Args ce{};
+      ce.targets = y;
+      ce.partials = partials;
+      if (keep_logits) {
+        ce.C = logits;
+        ce.ldc = V;
+      }
+      if (const char* e = std::getenv("SPECSIM_CE_L2_MB")) ce.l2_budget_mb = std::atoi(e);
+      return make_plan({nrm, H, false}, {pb("lm_head"), H, false}, static_cast<int>(rows), V, H,
+                       EPI_CE_FWD, ce);
+    };
+    // LM head + CE over every pass's rows at once; eval runs pass 0 only
+    p_ce_fwd = ce_fwd(KT);
+    if (K > 1) p_ce_fwd_eval = ce_fwd(T);
+    // LM head backward, vocabulary chunks, all K*T rows
     for (int c = 0; c < n_chunks; ++c) {
       const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
       Args cb = out_args(dlog, Vc);
@@ -513,33 +560,37 @@ class DraftTrainerImpl {
       cb.lse = lse;
       cb.coef = coef;
       cb.vocab_offset = static_cast<int>(v0);
-      p_ce_bwd.push_back(make_plan({nrm, H, false}, {pb("lm_head") + v0 * H, H, false}, T, vn, H,
-                                   EPI_CE_BWD, cb));
+      p_ce_bwd.push_back(make_plan({nrm, H, false}, {pb("lm_head") + v0 * H, H, false}, KT, vn,
+                                   H, EPI_CE_BWD, cb));
       // dn (+)= dlog_c . W_c     (B = W_c stored [vn, H] -> MN-major)
-      p_lm_dx.push_back(make_plan({dlog, Vc, false}, {pb("lm_head") + v0 * H, H, true}, T, H, vn,
+      p_lm_dx.push_back(make_plan({dlog, Vc, false}, {pb("lm_head") + v0 * H, H, true}, KT, H, vn,
                                   c == 0 ? EPI_F32 : EPI_F32_ACC, out_args(dn, H)));
-      // dW_c = dlog_c^T . nrm    (A = dlog stored [T, vn] -> MN-major)
-      p_lm_dw.push_back(make_plan({dlog, Vc, true}, {nrm, H, true}, vn, H, T, EPI_F32,
+      // dW_c = dlog_c^T . nrm    (A = dlog stored [KT, vn] -> MN-major)
+      p_lm_dw.push_back(make_plan({dlog, Vc, true}, {nrm, H, true}, vn, H, KT, EPI_F32,
                                   out_args(gf("lm_head") + v0 * H, H)));
     }
-    // MLP
-    p_dact = make_plan({dh_b, H, false}, {pb("down"), I, true}, T, I, H, EPI_BF16,
-                       out_args(dact, I));
-    p_dw_down = make_plan({dh_b, H, true}, {act, I, true}, H, I, T, EPI_F32,
+    // data gradients, per pass
+    for (int j = 0; j < K; ++j) {
+      const long long R = j * T;
+      p_dact.push_back(make_plan({dh_b + R * H, H, false}, {pb("down"), I, true}, T, I, H,
+                                 EPI_BF16, out_args(dact, I)));
+      p_dz.push_back(make_plan({dgu + R * 2 * I, 2 * I, false}, {pb("gate_up"), H, true}, T, H,
+                               2 * I, EPI_F32, out_args(dz + R * H, H)));
+      p_dO.push_back(make_plan({dr_b + R * H, H, false}, {pb("o"), Q, true}, T, Q, H, EPI_BF16,
+                               out_args(dO + R * Q, Q)));
+      p_dU.push_back(make_plan({dqkv + R * NQ, NQ, false}, {pb("qkv"), 2 * H, true}, T, 2 * H, NQ,
+                               EPI_F32, out_args(dU + R * 2 * H, 2 * H)));
+    }
+    // weight gradients: one GEMM over every pass's rows (the sum over passes
+    // is the reduction over K*T)
+    p_dw_down = make_plan({dh_b, H, true}, {act, I, true}, H, I, KT, EPI_F32,
                           out_args(gf("down"), I));
-    p_dz = make_plan({dgu, 2 * I, false}, {pb("gate_up"), H, true}, T, H, 2 * I, EPI_F32,
-                     out_args(dz, H));
-    p_dw_gu = make_plan({dgu, 2 * I, true}, {z, H, true}, 2 * I, H, T, EPI_F32,
+    p_dw_gu = make_plan({dgu, 2 * I, true}, {z, H, true}, 2 * I, H, KT, EPI_F32,
                         out_args(gf("gate_up"), H));
-    // attention output projection
-    p_dO = make_plan({dr_b, H, false}, {pb("o"), Q, true}, T, Q, H, EPI_BF16, out_args(dO, Q));
-    p_dw_o = make_plan({dr_b, H, true}, {o, Q, true}, H, Q, T, EPI_F32, out_args(gf("o"), Q));
-    // qkv
-    p_dU = make_plan({dqkv, NQ, false}, {pb("qkv"), 2 * H, true}, T, 2 * H, NQ, EPI_F32,
-                     out_args(dU, 2 * H));
-    p_dw_qkv = make_plan({dqkv, NQ, true}, {U, 2 * H, true}, NQ, 2 * H, T, EPI_F32,
+    p_dw_o = make_plan({dr_b, H, true}, {o, Q, true}, H, Q, KT, EPI_F32, out_args(gf("o"), Q));
+    p_dw_qkv = make_plan({dqkv, NQ, true}, {U, 2 * H, true}, NQ, 2 * H, KT, EPI_F32,
                          out_args(gf("qkv"), 2 * H));
-    // fc (no dF: captured features are inputs)
+    // fc (pass 0 only; no dF: captured features are inputs)
     p_dw_fc = make_plan({dg_b, H, true}, {F, W3, true}, H, W3, T, EPI_F32,
                         out_args(gf("fc"), W3));
     // fused-AdamW twins of every weight-gradient GEMM
@@ -627,15 +678,17 @@ class DraftTrainerImpl {
   double* hist_buf = nullptr;  // pinned per-step stats of train()
   size_t hist_cap = 0;
 
-  // Device work of the forward.  Everything that varies per step is read from
+  // Device work of the forward over `passes` unroll passes (K for a training
+  // step, 1 for eval).  Everything that varies per step is read from
   // d_in (filled by stage() before the launch), so the whole step can be
   // captured once into a CUDA graph and replayed.
-  void forward(HiddenStateBuffer& buf) {
+  void forward(HiddenStateBuffer& buf, int passes) {
     const int S = sh.seq_len;
+    const kern::StepWeights& w = passes == K ? sw : sw1;
     timed(PH_INGEST, 0, [&] {
       kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
-                         buf.capacity(), static_cast<int>(W3), &d_in->spec, sh.micro_batch, S, F,
-                         u, y, m, stream);
+                         buf.capacity(), static_cast<int>(W3), &d_in->spec, sh.micro_batch, S,
+                         passes, F, u, y, m, stream);
       kern::mask_count(m, T, n_counted, stream);
     });
     if (use_nccl)
@@ -645,38 +698,53 @@ class DraftTrainerImpl {
     timed(PH_ELEM, 0, [&] {
       // caller-provided global count wins over the counted one
       kern::select_count(&d_in->nglobal, n_counted, n_global, stream);
-      kern::ce_coef(m, n_global, coef, T, stream);
+      kern::ce_coef(m, n_global, coef, w, stream);
     });
     run(p_fc);
+    for (int j = 0; j < passes; ++j) {
+      const long long R = j * T;
+      timed(PH_ELEM, 0, [&] {
+        kern::rmsnorm_fwd(E, H, u + R, pf("w_in"), sh.rms_eps, U + R * 2 * H, 2 * H, rstd_a + R,
+                          T, sh.hidden, stream);
+        kern::rmsnorm_fwd(g + R * H, H, nullptr, pf("w_hid"), sh.rms_eps, U + R * 2 * H + H, 2 * H,
+                          rstd_b + R, T, sh.hidden, stream);
+      });
+      run(p_qkv[j]);  // RoPE fused into the epilogue
+      const attn::Dims ad = attn_dims(j);
+      timed(PH_ATTN, attn_flops(j, false), [&] {
+        attn::forward(qkv, o + R * Q, lse_attn + R * sh.n_heads, ad, sh.head_dim, stream);
+      });
+      run(p_o[j]);
+      timed(PH_ELEM, 0, [&] {
+        kern::rmsnorm_fwd(r + R * H, H, nullptr, pf("w_post"), sh.rms_eps, z + R * H, H,
+                          rstd_post + R, T, sh.hidden, stream);
+      });
+      run(p_gu[j]);
+      timed(PH_ELEM, 0, [&] { kern::swiglu_fwd(gu + R * 2 * I, act + R * I, T, sh.ffn, stream); });
+      run(p_down[j]);
+    }
+    const long long rows = passes * T;
     timed(PH_ELEM, 0, [&] {
-      kern::rmsnorm_fwd(E, H, u, pf("w_in"), sh.rms_eps, U, 2 * H, rstd_a, T, sh.hidden, stream);
-      kern::rmsnorm_fwd(g, H, nullptr, pf("w_hid"), sh.rms_eps, U + H, 2 * H, rstd_b, T,
-                        sh.hidden, stream);
-    });
-    run(p_qkv);  // RoPE fused into the epilogue
-    const attn::Dims ad = attn_dims();
-    timed(PH_ATTN, 2.0 * Q * (S + 1) * T, [&] { attn::forward(qkv, o, lse_attn, ad, sh.head_dim, stream); });
-    run(p_o);
-    timed(PH_ELEM, 0, [&] {
-      kern::rmsnorm_fwd(r, H, nullptr, pf("w_post"), sh.rms_eps, z, H, rstd_post, T, sh.hidden,
+      kern::rmsnorm_fwd(h, H, nullptr, pf("w_fin"), sh.rms_eps, nrm, H, rstd_fin, rows, sh.hidden,
                         stream);
     });
-    run(p_gu);
-    timed(PH_ELEM, 0, [&] { kern::swiglu_fwd(gu, act, T, sh.ffn, stream); });
-    run(p_down);
+    const gemm::GemmPlan& ce = passes == K ? p_ce_fwd : p_ce_fwd_eval;
+    run(ce, PH_LM);
     timed(PH_ELEM, 0, [&] {
-      kern::rmsnorm_fwd(h, H, nullptr, pf("w_fin"), sh.rms_eps, nrm, H, rstd_fin, T, sh.hidden,
-                        stream);
-    });
-    run(p_ce_fwd, PH_LM);
-    timed(PH_ELEM, 0, [&] {
-      kern::ce_reduce(partials, 2 * p_ce_fwd.args.num_n_blocks, T, y, m, lse, row_loss, argmax,
+      kern::ce_reduce(partials, 2 * ce.args.num_n_blocks, rows, y, m, lse, row_loss, argmax,
                       stream);
-      kern::ce_finalize(row_loss, argmax, y, m, n_global, T, stats, stream);
+      kern::ce_finalize(row_loss, argmax, y, m, n_global, w, stats, stream);
     });
   }
 
-  attn::Dims attn_dims() const {
+  // algorithmic attention FLOPs of pass j (causal 2Q(S+1) per token forward,
+  // plus 4Q per cache entry; backward twice that)
+  double attn_flops(int j, bool bwd) const {
+    const double f = (2.0 * Q * (sh.seq_len + 1) + 4.0 * Q * j) * T;
+    return bwd ? 2.0 * f : f;
+  }
+
+  attn::Dims attn_dims(int j = 0) const {
     attn::Dims d;
     d.B = sh.micro_batch;
     d.S = sh.seq_len;
@@ -686,6 +754,13 @@ class DraftTrainerImpl {
     d.Q = static_cast<int>(Q);
     d.KV = static_cast<int>(KV);
     d.scale = 1.0f / std::sqrt(static_cast<float>(sh.head_dim));
+    d.rope_len = static_cast<int>(rope_len());
+    // pass j: queries at rows j*T of the stacked qkv, RoPE positions t % S + j,
+    // cache entries of passes 1..j
+    d.q_row_off = j * T;
+    d.pos_off = j;
+    d.n_diag = j;
+    d.diag_qkv = j > 0 ? qkv : nullptr;
     return d;
   }
 
@@ -709,6 +784,28 @@ class DraftTrainerImpl {
                                        comm, comm_stream));
   }
 
+  // Attention backward of pass j (K > 1): D_j, the cache entries (j >= 1),
+  // dQ_j against step 0's keys; dK / dV of pass 0's keys from every pass's
+  // queries once the last pass (j == 0) is reached.
+  void attn_backward_pass(int j) {
+    const long long R = j * T;
+    attn::Dims ad = attn_dims(j);
+    ad.rope_cos = cos_tr;
+    ad.rope_sin = sin_tr;
+    float* D = Dattn + R * sh.n_heads;
+    const float* l = lse_attn + R * sh.n_heads;
+    timed(PH_ATTN, attn_flops(j, true), [&] {
+      attn::bwd_dot(dO + R * Q, o + R * Q, D, ad, sh.head_dim, stream);
+      if (j > 0)
+        attn::bwd_diag(qkv, dO + R * Q, l, D, dq_add, dkv_acc, dqkv + R * NQ, ad, sh.head_dim,
+                       stream);
+      attn::bwd_dq(qkv, dO + R * Q, l, D, j > 0 ? dq_add : nullptr, dqkv + R * NQ, ad,
+                   sh.head_dim, stream);
+      if (j == 0)
+        attn::bwd_dkdv(qkv, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, K, stream);
+    });
+  }
+
   void backward() {
     const int S = sh.seq_len;
     bucket_next = 0;
@@ -716,7 +813,7 @@ class DraftTrainerImpl {
       const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
       if (keep_logits)
         timed(PH_LM, 0, [&] {
-          kern::ce_grad(logits, V, lse, coef, y, static_cast<int>(v0), T, static_cast<int>(vn),
+          kern::ce_grad(logits, V, lse, coef, y, static_cast<int>(v0), KT, static_cast<int>(vn),
                         dlog, Vc, stream);
         });
       else
@@ -726,47 +823,91 @@ class DraftTrainerImpl {
       // LM-head rows of this chunk are final: their all-reduce overlaps the rest
       bucket_ready("lm_head", "lm_head", vn * H, param("lm_head").off + v0 * H);
     }
-    timed(PH_ELEM, 0, [&] {
-      kern::rmsnorm_bwd(dn, H, h, H, nullptr, pf("w_fin"), rstd_fin, nullptr, dh, dh_b, H,
-                        gf("w_fin"), dw_part, T, sh.hidden, stream);
-    });
-    run(p_dact);
-    run_dw(p_dw_down, f_dw_down);
-    bucket_ready("down", "w_fin");
-    timed(PH_ELEM, 0, [&] { kern::swiglu_bwd(gu, dact, dgu, T, sh.ffn, stream); });
-    run(p_dz);
-    run_dw(p_dw_gu, f_dw_gu);
-    bucket_ready("gate_up", "gate_up");
-    timed(PH_ELEM, 0, [&] {
-      kern::rmsnorm_bwd(dz, H, r, H, nullptr, pf("w_post"), rstd_post, dh, dr, dr_b, H,
-                        gf("w_post"), dw_part, T, sh.hidden, stream);
-    });
-    run(p_dO);
-    run_dw(p_dw_o, f_dw_o);
-    bucket_ready("o", "w_post");
-    attn::Dims ad = attn_dims();
-    ad.rope_cos = cos_tr;
-    ad.rope_sin = sin_tr;
-    bool rope_fused = false;
-    timed(PH_ATTN, 4.0 * Q * (S + 1) * T, [&] {
-      rope_fused = attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
-    });
-    if (!rope_fused)
+    if (K > 1)
       timed(PH_ELEM, 0, [&] {
-        kern::rope(dqkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads, sh.head_dim,
-                   cos_t, sin_t, true, stream);
+        SPECSIM_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * KT * 2 * KV, stream));
       });
-    run(p_dU);
-    run_dw(p_dw_qkv, f_dw_qkv);
-    bucket_ready("qkv", "qkv");
-    timed(PH_ELEM, 0, [&] {
-      // w_in: embedding is frozen, only the weight gradient is needed
-      kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
-                        gf("w_in"), dw_part, T, sh.hidden, stream);
-      // hidden norm: dg = dr + d/dg RMSNorm(g) ; bf16 copy feeds dW_fc
-      kern::rmsnorm_bwd(dU + H, 2 * H, g, H, nullptr, pf("w_hid"), rstd_b, dr, nullptr, dg_b, H,
-                        gf("w_hid"), dw_part, T, sh.hidden, stream);
-    });
+    // One pass: each norm backward produces dx and its weight gradient in one
+    // launch.  K passes: dx per pass (in reverse: pass j's input gradient dg
+    // flows into pass j-1's output h), weight gradients once over all K*T rows.
+    const bool one = K == 1;
+    for (int j = K - 1; j >= 0; --j) {
+      const long long R = j * T;
+      timed(PH_ELEM, 0, [&] {
+        kern::rmsnorm_bwd(dn + R * H, H, h + R * H, H, nullptr, pf("w_fin"), rstd_fin + R,
+                          j < K - 1 ? dg_in : nullptr, dh, dh_b + R * H, H,
+                          one ? gf("w_fin") : nullptr, dw_part, T, sh.hidden, stream);
+        if (j == 0 && !one)
+          kern::rmsnorm_bwd(dn, H, h, H, nullptr, pf("w_fin"), rstd_fin, nullptr, nullptr,
+                            nullptr, H, gf("w_fin"), dw_part, KT, sh.hidden, stream);
+      });
+      run(p_dact[j]);
+      if (j == 0) {
+        run_dw(p_dw_down, f_dw_down);
+        bucket_ready("down", "w_fin");
+      }
+      timed(PH_ELEM, 0, [&] {
+        kern::swiglu_bwd(gu + R * 2 * I, dact, dgu + R * 2 * I, T, sh.ffn, stream);
+      });
+      run(p_dz[j]);
+      if (j == 0) {
+        run_dw(p_dw_gu, f_dw_gu);
+        bucket_ready("gate_up", "gate_up");
+      }
+      timed(PH_ELEM, 0, [&] {
+        kern::rmsnorm_bwd(dz + R * H, H, r + R * H, H, nullptr, pf("w_post"), rstd_post + R, dh,
+                          dr, dr_b + R * H, H, one ? gf("w_post") : nullptr, dw_part, T,
+                          sh.hidden, stream);
+      });
+      run(p_dO[j]);
+      if (j == 0) {
+        if (!one)
+          timed(PH_ELEM, 0, [&] {
+            kern::rmsnorm_bwd(dz, H, r, H, nullptr, pf("w_post"), rstd_post, nullptr, nullptr,
+                              nullptr, H, gf("w_post"), dw_part, KT, sh.hidden, stream);
+          });
+        run_dw(p_dw_o, f_dw_o);
+        bucket_ready("o", "w_post");
+      }
+      if (one) {
+        attn::Dims ad = attn_dims();
+        ad.rope_cos = cos_tr;
+        ad.rope_sin = sin_tr;
+        bool rope_fused = false;
+        timed(PH_ATTN, attn_flops(0, true), [&] {
+          rope_fused = attn::backward(qkv, o, dO, lse_attn, Dattn, dqkv, ad, sh.head_dim, stream);
+        });
+        if (!rope_fused)
+          timed(PH_ELEM, 0, [&] {
+            kern::rope(dqkv, T, S, static_cast<int>(NQ), sh.n_heads + sh.n_kv_heads,
+                       sh.head_dim, cos_t, sin_t, true, stream);
+          });
+      } else {
+        attn_backward_pass(j);
+      }
+      run(p_dU[j]);
+      if (j == 0) {
+        run_dw(p_dw_qkv, f_dw_qkv);
+        bucket_ready("qkv", "qkv");
+      }
+      timed(PH_ELEM, 0, [&] {
+        float* dUj = dU + R * 2 * H;
+        if (one)  // w_in: embedding is frozen, only the weight gradient is needed
+          kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
+                            gf("w_in"), dw_part, T, sh.hidden, stream);
+        // hidden norm: dg = dr + d/dg RMSNorm(g); pass 0's bf16 copy feeds dW_fc,
+        // a later pass's fp32 dg flows into the previous pass's output
+        kern::rmsnorm_bwd(dUj + H, 2 * H, g + R * H, H, nullptr, pf("w_hid"), rstd_b + R, dr,
+                          j > 0 ? dg_in : nullptr, j > 0 ? nullptr : dg_b, H,
+                          one ? gf("w_hid") : nullptr, dw_part, T, sh.hidden, stream);
+        if (j == 0 && !one) {
+          kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
+                            gf("w_in"), dw_part, KT, sh.hidden, stream);
+          kern::rmsnorm_bwd(dU + H, 2 * H, g, H, nullptr, pf("w_hid"), rstd_b, nullptr, nullptr,
+                            nullptr, H, gf("w_hid"), dw_part, KT, sh.hidden, stream);
+        }
+      });
+    }
     run_dw(p_dw_fc, f_dw_fc);
     bucket_ready("fc", "w_hid");
     if (use_nccl) {
@@ -903,7 +1044,7 @@ class DraftTrainerImpl {
 
   // The device work of one step (train) or one forward (eval).
   void enqueue(HiddenStateBuffer& buf, bool train) {
-    forward(buf);
+    forward(buf, train ? K : 1);
     if (train) {
       backward();  // includes the bucketed gradient all-reduce when data-parallel
       optimizer_update();
@@ -1123,6 +1264,8 @@ int specsim_trainer_create(const specsim_draft_shape* shape, const specsim_adamw
     s.micro_batch = shape->micro_batch;
     s.rms_eps = shape->rms_eps;
     s.rope_theta = shape->rope_theta;
+    s.ttt_steps = shape->ttt_steps > 0 ? shape->ttt_steps : 1;
+    s.ttt_decay = shape->ttt_decay > 0.f ? shape->ttt_decay : 0.8f;
     AdamWConfig a;
     if (opt) {
       a.lr = opt->lr;

@@ -1,0 +1,138 @@
+"""EAGLE-3 training-time-test unroll on the B200 vs the CPU
+oracle: K decoder passes per step (pass j: previous pass's output as input,
+tokens shifted by j, RoPE at t + j, attention over step 0's causal keys plus
+the cache entries of passes 1..j), decay-weighted loss.  The oracle's unroll
+is itself pinned against a SpecForge-layout torch autograd restatement
+(tests/test_oracle_vs_torch.py::test_ttt_step_matches_torch).
+
+Tolerances as tests/test_trainer_gpu.py: loss rel <= 2e-3, every gradient
+rel-Frobenius <= 1e-2, AdamW update within 0.05 lr on >= 99% of well-determined
+elements, valid counts exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2602_05145_b200 import api
+
+pytestmark = pytest.mark.gpu
+SEED = 20260217
+HP = [1e-3, 0.9, 0.95, 1e-8, 0.0]
+
+CASES = {
+    "C1_k3": dict(api.CONFIGS["C1"], ttt_steps=3),
+    # head_dim 128, one KV head for four query heads (GQA group 4 in the cache kernel)
+    "gqa128_k2": dict(hidden=256, vocab=2048, seq_len=128, n_heads=4, n_kv_heads=1, head_dim=128,
+                      ffn=512, micro_batch=3, rms_eps=1e-6, rope_theta=500000.0, ttt_steps=2),
+    # several attention blocks per sample, decay other than the default
+    "s256_k4": dict(hidden=256, vocab=2048, seq_len=256, n_heads=4, n_kv_heads=2, head_dim=64,
+                    ffn=512, micro_batch=2, rms_eps=1e-5, rope_theta=10000.0, ttt_steps=4,
+                    ttt_decay=0.7),
+}
+
+
+def oshape(c, ttt=None):
+    return oracle.make_shape(c["hidden"], c["vocab"], c["seq_len"], c["n_heads"], c["n_kv_heads"],
+                             c["head_dim"], c["ffn"], c["micro_batch"], eps=c["rms_eps"],
+                             theta=c["rope_theta"], ttt=c["ttt_steps"] if ttt is None else ttt,
+                             ttt_decay=c.get("ttt_decay", 0.8))
+
+
+def setup(c, lens, n_present):
+    tr = api.DraftTrainer(c, lr=HP[0], betas=(HP[1], HP[2]), eps=HP[3], weight_decay=HP[4],
+                          seed=SEED)
+    tr.keep_grads(True)
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 16)
+    samples = []
+    for i, L in enumerate(lens):
+        cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+        buf.append_packed(100 + i, cap["alpha_s"], cap["features"], cap["ids"])
+        samples.append((cap["ids"], cap["features"]))
+    return tr, buf, samples[:n_present], [100 + i for i in range(n_present)]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_ttt_step_matches_oracle(name):
+    c = CASES[name]
+    S, B, K = c["seq_len"], c["micro_batch"], c["ttt_steps"]
+    # full samples (every pass unmasked), one whose shifted masks run out at
+    # different passes, one much longer than S; the last row is padding
+    lens = [S + 2 + K] * (B - 2) + [S // 2 + 3, S + 40]
+    n = B - 1 if B > 2 else B
+    tr, buf, samples, ids = setup(c, lens, n)
+    shp = oshape(c)
+    F, u, y, m = oracle.gather_batch(shp, samples)
+    layout, total = oracle.param_layout(shp)
+    P = oracle.init_params(shp, SEED)
+    E = oracle.init_embedding(shp, SEED)
+    Mst, Vst = np.zeros_like(P), np.zeros_like(P)
+    T = B * S
+    report = {}
+    for k in (1, 2):
+        P0 = P.copy()
+        out, grads = oracle.train_step(shp, HP, k, P, Mst, Vst, E, F, u, y, m, round_bf16=True)
+        r = tr.step(buf, ids)
+        assert r["valid_tokens"] == int(m[:T].sum()) == out.valid
+        assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
+        assert abs(r["top1_correct"] - out.top1) <= max(2, 0.01 * out.valid)
+        for nm, rr, cc, off in layout:
+            g_gpu = tr.get_grad(nm).reshape(-1)
+            g_cpu = grads[off:off + rr * cc]
+            e = rel(g_gpu, g_cpu)
+            report[(k, nm)] = e
+            assert e <= 1e-2, (k, nm, e)
+            d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
+            d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
+            well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
+            if well.sum() > 0:
+                ok = np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]
+                assert ok.mean() >= 0.99, (k, nm, ok.mean())
+            tr.set_param(nm, P[off:off + rr * cc].reshape(rr, cc))
+    print(name, "grad rel errors:", {f"{k}:{n}": round(v, 5) for (k, n), v in report.items()})
+    tr.close()
+    buf.close()
+
+
+def test_ttt_fused_adamw_and_eval():
+    """Default path (fused AdamW in the weight-gradient epilogues over all K*T
+    rows, no gradient store) gives the oracle's update; eval runs pass 0 only
+    (its loss / top-1 equal the single-pass forward)."""
+    c = CASES["C1_k3"]
+    S, B = c["seq_len"], c["micro_batch"]
+    tr, buf, samples, ids = setup(c, [S + 5] * B, B)
+    tr.keep_grads(False)
+    shp = oshape(c)
+    F, u, y, m = oracle.gather_batch(shp, samples)
+    P = oracle.init_params(shp, SEED)
+    E = oracle.init_embedding(shp, SEED)
+    z = np.zeros_like(P)
+    out, _ = oracle.train_step(shp, HP, 1, P, z.copy(), z.copy(), E, F, u, y, m, round_bf16=True)
+    r = tr.step(buf, ids)
+    assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss)
+    layout, _ = oracle.param_layout(shp)
+    P0 = oracle.init_params(shp, SEED)
+    for nm, rr, cc, off in layout:
+        d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
+        d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
+        assert (np.abs(d_gpu - d_cpu) <= 0.05 * HP[0]).mean() >= 0.99, nm
+    # eval = pass 0 of the updated model
+    shp1 = oshape(c, ttt=1)
+    F1, u1, y1, m1 = oracle.gather_batch(shp1, samples)
+    o1, _, _ = oracle.forward(shp1, P, E, F1, u1, y1, m1, round_bf16=True)
+    e = tr.eval(buf, ids)
+    assert e["valid_tokens"] == o1.valid
+    assert abs(e["loss"] - o1.loss) <= 2e-3 * abs(o1.loss)
+    tr.close()
+    buf.close()
+
+
+def test_ttt_shape_validation():
+    c = dict(CASES["C1_k3"], seq_len=192)  # K > 1 needs the tcgen05 attention (S % 128)
+    with pytest.raises(Exception):
+        api.DraftTrainer(c, seed=SEED)
+    with pytest.raises(Exception):
+        api.DraftTrainer(dict(CASES["C1_k3"], ttt_steps=17), seed=SEED)
