@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=WORKLOAD)
+    ap.add_argument("--ttt", type=int, default=1,
+                    help="EAGLE-3 training-time-test unroll passes per step (1 = the headline "
+                         "single-pass step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seq", type=int, default=256,
@@ -124,12 +127,13 @@ def cpu_sample(cfg, seq, threads_note=True):
     captured sequence of `seq` positions at the workload's model shape."""
     import numpy as np
     import oracle
+    K = cfg.get("ttt_steps", 1)
     shp = oracle.make_shape(cfg["hidden"], cfg["vocab"], seq, cfg["n_heads"], cfg["n_kv_heads"],
                             cfg["head_dim"], cfg["ffn"], 1, eps=cfg["rms_eps"],
-                            theta=cfg["rope_theta"])
+                            theta=cfg["rope_theta"], ttt=K)
     P = oracle.init_params(shp, SEED)
     E = oracle.init_embedding(shp, SEED)
-    cap = oracle.synth_capture(SEED, 0, seq + 2, cfg["vocab"], cfg["hidden"])
+    cap = oracle.synth_capture(SEED, 0, seq + 1 + K, cfg["vocab"], cfg["hidden"])
     F, u, y, m = oracle.gather_batch(shp, [(cap["ids"], cap["features"])])
     Mst, Vst = np.zeros_like(P), np.zeros_like(P)
     return shp, P, E, (F, u, y, m), Mst, Vst
@@ -141,7 +145,7 @@ def run_reference(args):
         return 0
     import oracle
     from paper_2602_05145_b200 import api
-    cfg = api.CONFIGS[args.config]
+    cfg = workload_cfg(args, api)
     seq = args.cpu_sample_seq
     shp, P, E, batch, Mst, Vst = cpu_sample(cfg, seq)
     hp = [1e-4, 0.9, 0.95, 1e-8, 0.0]
@@ -176,11 +180,23 @@ MODEL_SHAPE = {"C1": "tiny draft head", "C2": "Llama-3.1-8B shape", "C4": "Qwen3
                "C5": "Llama-3.3-70B shape"}
 
 
+def workload_cfg(args, api):
+    cfg = dict(api.CONFIGS[args.config])
+    if args.ttt > 1:
+        cfg["ttt_steps"] = args.ttt
+    return cfg
+
+
 def config_block(args, cfg):
-    return dict(workload=f"{args.config}: EAGLE-3-style draft head, "
+    K = cfg.get("ttt_steps", 1)
+    ttt = (f", training-time-test unroll {K} passes (loss weights 0.8^j)" if K > 1 else "")
+    name = args.config + (f"-TTT{K}" if K > 1 else "")
+    extra = dict(ttt_steps=K) if K > 1 else {}
+    return dict(workload=f"{name}: EAGLE-3-style draft head, "
                          f"{MODEL_SHAPE.get(args.config, args.config)} "
                          f"(hidden {cfg['hidden']}, 3-layer feature concat, vocab {cfg['vocab']}, "
-                         f"seq {cfg['seq_len']}), bf16 GEMMs, synthetic captured hidden states",
+                         f"seq {cfg['seq_len']}){ttt}, bf16 GEMMs, synthetic captured hidden states",
+                **extra,
                 hidden=cfg["hidden"], vocab=cfg["vocab"], seq_len=cfg["seq_len"],
                 micro_batch=cfg["micro_batch"], global_batch=cfg["micro_batch"] * args.gpus,
                 tokens_per_rank_step=cfg["micro_batch"] * cfg["seq_len"],
@@ -201,7 +217,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = api.CONFIGS[args.config]
+    cfg = workload_cfg(args, api)
     B, S, H, V = cfg["micro_batch"], cfg["seq_len"], cfg["hidden"], cfg["vocab"]
     T = B * S
     nccl_id = None
@@ -212,7 +228,7 @@ def run_ours(args):
     tr = api.DraftTrainer(cfg, seed=SEED, rank=rank, world=world, nccl_id=nccl_id, device=local)
     geom = api.SignalGeometry(H)
     pool_n = 2 * B
-    L = S + 2
+    L = S + 1 + cfg.get("ttt_steps", 1)  # every unroll pass fully unmasked
     W = 3 * H
     # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps) + slack
     buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + 18 * B) * L, device=local)

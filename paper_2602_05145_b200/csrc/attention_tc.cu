@@ -372,13 +372,25 @@ __device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, 
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      float x1 = __uint_as_float(a[i]) * sc, x2 = __uint_as_float(b[i]) * sc;
-      if (add != nullptr) {
-        x1 += __ldg(add + p * 32 + i);
-        x2 += __ldg(add + HALF + p * 32 + i);
+      a[i] = __float_as_uint(__uint_as_float(a[i]) * sc);
+      b[i] = __float_as_uint(__uint_as_float(b[i]) * sc);
+    }
+    if (add != nullptr) {
+      // 16-byte loads: a thread walks its own row (128 B per chunk)
+      const float4* a4 = reinterpret_cast<const float4*>(add + p * 32);
+      const float4* b4 = reinterpret_cast<const float4*>(add + HALF + p * 32);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+        a[4 * i] = __float_as_uint(__uint_as_float(a[4 * i]) + x.x);
+        a[4 * i + 1] = __float_as_uint(__uint_as_float(a[4 * i + 1]) + x.y);
+        a[4 * i + 2] = __float_as_uint(__uint_as_float(a[4 * i + 2]) + x.z);
+        a[4 * i + 3] = __float_as_uint(__uint_as_float(a[4 * i + 3]) + x.w);
+        b[4 * i] = __float_as_uint(__uint_as_float(b[4 * i]) + y.x);
+        b[4 * i + 1] = __float_as_uint(__uint_as_float(b[4 * i + 1]) + y.y);
+        b[4 * i + 2] = __float_as_uint(__uint_as_float(b[4 * i + 2]) + y.z);
+        b[4 * i + 3] = __float_as_uint(__uint_as_float(b[4 * i + 3]) + y.w);
       }
-      a[i] = __float_as_uint(x1);
-      b[i] = __float_as_uint(x2);
     }
     if (d.rope_cos != nullptr) {
       const float* cs = d.rope_cos + static_cast<long long>(p * 32) * L + pos;
@@ -868,7 +880,7 @@ namespace {
 // columns.  For each query head of the group and each earlier step i <= j:
 // p = exp(q.k_i*scale - lse), ds = p (dO.v_i - D) scale; dq += ds k_i,
 // dk_i += ds q, dv_i += p dO (fp32 accumulators, fixed order: deterministic).
-template <int HD>
+template <int HD, int kMaxRep>
 __global__ void __launch_bounds__(256) attn_bwd_diag_kernel(
     const __nv_bfloat16* __restrict__ qkv_all, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, const float* __restrict__ Dv, float* __restrict__ dq_add,
@@ -892,40 +904,62 @@ __global__ void __launch_bounds__(256) attn_bwd_diag_kernel(
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
-  for (int hh = 0; hh < rep; ++hh) {
-    const int h = g * rep + hh;
-    float q[E], dO[E], dq[E];
-    ld(qkv_all + (static_cast<long long>(j) * T + t) * d.NQ + h * HD + c0, q);
-    ld(dout + t * d.Q + h * HD + c0, dO);
-    const float l = lse[h * T + t], Dh = Dv[h * T + t];
+  // the group's q / dO rows live in registers (rep * 2E floats); every cache
+  // entry i is loaded once and its dk / dv accumulated over the group before
+  // one read-modify-write of the fp32 accumulator (kMaxRep >= rep: the
+  // smallest power of two, so register use follows the GQA group)
+  float q[kMaxRep][E], dO[kMaxRep][E], dq[kMaxRep][E], l[kMaxRep], Dh[kMaxRep];
 #pragma unroll
-    for (int e = 0; e < E; ++e) dq[e] = 0.f;
-    for (int i = 1; i <= j; ++i) {
-      const __nv_bfloat16* kr = qkv_all + (static_cast<long long>(i) * T + t) * d.NQ + d.Q + g * HD;
-      float k[E], v[E];
-      ld(kr + c0, k);
-      ld(kr + d.KV + c0, v);
+  for (int hh = 0; hh < kMaxRep; ++hh) {
+    if (hh >= rep) break;
+    const int h = g * rep + hh;
+    ld(qkv_all + (static_cast<long long>(j) * T + t) * d.NQ + h * HD + c0, q[hh]);
+    ld(dout + t * d.Q + h * HD + c0, dO[hh]);
+    l[hh] = lse[h * T + t];
+    Dh[hh] = Dv[h * T + t];
+#pragma unroll
+    for (int e = 0; e < E; ++e) dq[hh][e] = 0.f;
+  }
+  for (int i = 1; i <= j; ++i) {
+    const __nv_bfloat16* kr = qkv_all + (static_cast<long long>(i) * T + t) * d.NQ + d.Q + g * HD;
+    float k[E], v[E], dk[E], dv[E];
+    ld(kr + c0, k);
+    ld(kr + d.KV + c0, v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) dk[e] = dv[e] = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < kMaxRep; ++hh) {
+      if (hh >= rep) break;
       float sd = 0.f, sp = 0.f;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        sd += q[e] * k[e];
-        sp += dO[e] * v[e];
+        sd += q[hh][e] * k[e];
+        sp += dO[hh][e] * v[e];
       }
       sd = wsum(sd);
       sp = wsum(sp);
-      const float p = __expf(sd * d.scale - l);
-      const float ds = p * (sp - Dh) * d.scale;
-      float* acc = dkv_acc + (static_cast<long long>(i) * T + t) * KV2 + g * HD + c0;
+      const float p = __expf(sd * d.scale - l[hh]);
+      const float ds = p * (sp - Dh[hh]) * d.scale;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        dq[e] += ds * k[e];
-        acc[e] += ds * q[e];
-        acc[d.KV + e] += p * dO[e];
+        dq[hh][e] += ds * k[e];
+        dk[e] += ds * q[hh][e];
+        dv[e] += p * dO[hh][e];
       }
     }
-    float* dqa = dq_add + t * d.Q + h * HD + c0;
+    float* acc = dkv_acc + (static_cast<long long>(i) * T + t) * KV2 + g * HD + c0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) dqa[e] = dq[e];
+    for (int e = 0; e < E; ++e) {
+      acc[e] += dk[e];
+      acc[d.KV + e] += dv[e];
+    }
+  }
+#pragma unroll
+  for (int hh = 0; hh < kMaxRep; ++hh) {
+    if (hh >= rep) break;
+    float* dqa = dq_add + t * d.Q + (g * rep + hh) * HD + c0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dqa[e] = dq[hh][e];
   }
   // step j's k / v receive no further contributions: round, inverse-rotate
   // k (position t % S + j; partner column c +- HD/2 lives 16 lanes away),
@@ -993,15 +1027,32 @@ void bwd_diag(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const flo
               const Dims& d, int hd, cudaStream_t s) {
   if (d.n_diag < 1 || d.n_diag > kMaxDiag)
     throw std::invalid_argument("bwd_diag: n_diag must be in [1, 15]");
+  if (d.nh / d.nkv > 16) throw std::invalid_argument("bwd_diag: GQA group must be <= 16");
   const long long warps = static_cast<long long>(d.B) * d.S * d.nkv;
   const unsigned blocks = static_cast<unsigned>((warps * 32 + 255) / 256);
   count_launches();
-  if (hd == 128)
-    attn_bwd_diag_kernel<128><<<blocks, 256, 0, s>>>(qkv_all, dout, lse, D, dq_add, dkv_acc,
-                                                     dqkv_step, d);
-  else
-    attn_bwd_diag_kernel<64><<<blocks, 256, 0, s>>>(qkv_all, dout, lse, D, dq_add, dkv_acc,
-                                                    dqkv_step, d);
+  const int rep = d.nh / d.nkv;
+#define SPECSIM_DIAG(HD_, R_)                                                                  \
+  attn_bwd_diag_kernel<HD_, R_><<<blocks, 256, 0, s>>>(qkv_all, dout, lse, D, dq_add, dkv_acc, \
+                                                       dqkv_step, d)
+#define SPECSIM_DIAG_HD(HD_)        \
+  if (rep <= 1)                     \
+    SPECSIM_DIAG(HD_, 1);           \
+  else if (rep <= 2)                \
+    SPECSIM_DIAG(HD_, 2);           \
+  else if (rep <= 4)                \
+    SPECSIM_DIAG(HD_, 4);           \
+  else if (rep <= 8)                \
+    SPECSIM_DIAG(HD_, 8);           \
+  else                              \
+    SPECSIM_DIAG(HD_, 16);
+  if (hd == 128) {
+    SPECSIM_DIAG_HD(128)
+  } else {
+    SPECSIM_DIAG_HD(64)
+  }
+#undef SPECSIM_DIAG_HD
+#undef SPECSIM_DIAG
 }
 
 void bwd_dq(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const float* lse,
