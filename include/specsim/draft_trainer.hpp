@@ -148,6 +148,17 @@ struct AdamWConfig {
   float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.f;
 };
 
+// One contiguous range [off, off + n) of the flat gradient vector exchanged as
+// a unit by the data-parallel path (see dp_buckets).
+struct DpBucket {
+  long long off, n;
+};
+// Buckets in the order the backward finalises them (they tile the registry).
+std::vector<DpBucket> dp_buckets(const DraftShape& shape);
+// True when every bucket splits into `world` shards of whole 8-element groups
+// (the ZeRO-1 path; otherwise the trainer all-reduces).
+bool zero_shardable(const std::vector<DpBucket>& buckets, int world);
+
 struct StepResult {
   double loss = 0;
   int64_t valid_tokens = 0, top1_correct = 0, positions = 0;

@@ -229,6 +229,19 @@ typedef struct specsim_draft_shape {
   float ttt_decay;
 } specsim_draft_shape;
 
+/* Gradient buckets of the data-parallel exchange for a draft shape, in the
+ * order the backward finalises them (LM-head vocabulary chunks, then
+ * [down, w_fin], [gate_up], [o, w_post], [qkv], [fc, w_in, w_hid]); they tile
+ * the flat parameter vector.  Writes up to cap (off, n) pairs; *count = total
+ * buckets; *zero_ok = 1 when every bucket splits into `world` shards of whole
+ * 8-element groups, i.e. when world > 1 runs ZeRO-1: each bucket is
+ * reduce-scattered in place (rank r owns [off + r*n/world, off + (r+1)*n/world)),
+ * AdamW updates the owned shard and the bf16 working weights are all-gathered,
+ * all overlapped with the rest of the backward (SPECSIM_DP_MODE=allreduce
+ * selects the replicated all-reduce + AdamW path instead).  Host only. */
+int specsim_dp_buckets(const specsim_draft_shape* shape, int32_t world, int64_t* off, int64_t* n,
+                       int32_t cap, int32_t* count, int32_t* zero_ok);
+
 /* PyTorch AdamW semantics. */
 typedef struct specsim_adamw {
   float lr, beta1, beta2, eps, weight_decay;
@@ -331,7 +344,11 @@ int specsim_controller_events(const specsim_controller* c, int32_t* kinds, int64
                               int64_t cap, int64_t* n);
 
 /* Parameter registry (fp32 master copies; names: fc, w_in, w_hid, qkv, o,
- * w_post, gate_up, down, w_fin, lm_head).  Frozen embedding: "embed". */
+ * w_post, gate_up, down, w_fin, lm_head).  Frozen embedding: "embed".
+ * Under ZeRO-1 (world > 1) each rank's fp32 master is current on its own
+ * shards only: get_param and snapshot first all-gather it, so they are
+ * collective (every rank calls them, in the same order), and get_grad is
+ * the reduced gradient on the rank's own shards only. */
 int specsim_trainer_num_params(const specsim_trainer* t, int32_t* count, int64_t* total_elems);
 int specsim_trainer_param_info(const specsim_trainer* t, int32_t index, const char** name,
                                int64_t* rows, int64_t* cols);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "specsim_alpha_from_accept_length": [F64, I32, PF64],
     "specsim_split_train_eval": [I64, PI64, PI64],
     "specsim_dp_shard": [I64, I32, I32, I32, I64, P, PI32],
+    "specsim_dp_buckets": [C.POINTER(DraftShape), I32, P, P, I32, PI32, PI32],
     "specsim_bytes_per_token": [C.POINTER(SignalGeometry), PI64],
     "specsim_synth_capture": [U64, I64, I32, I32, I32, I32, F64, I32, P, P, P, PI32, PF64],
     "specsim_hsbuf_create": [C.POINTER(SignalGeometry), I64, I64, C.c_int, C.POINTER(P)],

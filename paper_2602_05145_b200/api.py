@@ -116,6 +116,34 @@ def dp_shard(n_items: int, per_rank: int, world: int, rank: int, step: int):
     return idx[: n.value].tolist()
 
 
+def draft_shape(shape: dict):
+    """ctypes specsim_draft_shape from a config dict (api.CONFIGS entry)."""
+    return _lib.DraftShape(shape["hidden"], shape["vocab"], shape["seq_len"], shape["n_heads"],
+                           shape["n_kv_heads"], shape["head_dim"], shape["ffn"],
+                           shape.get("layers_tapped", 3), shape.get("micro_batch", 1),
+                           shape.get("rms_eps", 1e-5), shape.get("rope_theta", 10000.0),
+                           shape.get("ttt_steps", 1), shape.get("ttt_decay", 0.8))
+
+
+def dp_buckets(shape: dict, world: int):
+    """(buckets [(off, n)], zero_ok) of the data-parallel gradient exchange."""
+    s = draft_shape(shape)
+    cnt, ok = C.c_int32(), C.c_int32()
+    call("specsim_dp_buckets", C.byref(s), world, None, None, 0, C.byref(cnt), C.byref(ok))
+    off = np.zeros(cnt.value, np.int64)
+    n = np.zeros(cnt.value, np.int64)
+    call("specsim_dp_buckets", C.byref(s), world, ptr(off), ptr(n), cnt.value, C.byref(cnt),
+         C.byref(ok))
+    return list(zip(off.tolist(), n.tolist())), bool(ok.value)
+
+
+def zero_shard(bucket, world: int, rank: int):
+    """Range [lo, hi) of a bucket owned by `rank` under ZeRO-1."""
+    off, n = bucket
+    c = n // world
+    return off + rank * c, off + (rank + 1) * c
+
+
 def global_job(steps: int, per_rank: int, world: int, id_of):
     """Global train(job) list for data parallelism: slot j of step k belongs to
     rank j % world (the specsim_dp_shard rule) and holds id_of(rank, k, j // world),
@@ -299,11 +327,7 @@ class DraftTrainer:
     def __init__(self, shape: dict, lr=1e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0,
                  seed=20260217, rank=0, world=1, nccl_id: bytes | None = None, device=0):
         self.shape = dict(shape)
-        s = _lib.DraftShape(shape["hidden"], shape["vocab"], shape["seq_len"], shape["n_heads"],
-                            shape["n_kv_heads"], shape["head_dim"], shape["ffn"],
-                            shape.get("layers_tapped", 3), shape["micro_batch"],
-                            shape.get("rms_eps", 1e-5), shape.get("rope_theta", 10000.0),
-                            shape.get("ttt_steps", 1), shape.get("ttt_decay", 0.8))
+        s = draft_shape(shape)
         a = _lib.AdamW(lr, betas[0], betas[1], eps, weight_decay)
         self.h = C.c_void_p()
         nid = None

@@ -1,7 +1,7 @@
 // NCCL resolved at run time (dlopen) instead of at link time, so loading this
 // library never pins a libnccl.so.2 into the process before the host
 // framework (e.g. torch, which ships a newer NCCL) loads its own.  Only the
-// five entry points the data-parallel exchange needs are bound.
+// entry points the data-parallel exchange needs are bound.
 #pragma once
 
 #include <nccl.h>
@@ -13,6 +13,10 @@ struct Api {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*);
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   const char* (*GetErrorString)(ncclResult_t);

@@ -79,7 +79,76 @@ class Arena {
 
 enum Phase { PH_INGEST = 0, PH_GEMM, PH_ATTN, PH_ELEM, PH_LM, PH_ADAM, PH_COMM, PH_N };
 
+struct ParamDesc {
+  std::string name;
+  long long rows, cols, off;
+  bool norm;
+};
+
+// Parameter registry: flat fp32 layout, same order / offsets as the oracle.
+std::vector<ParamDesc> param_registry(const DraftShape& sh, long long* total) {
+  const long long H = sh.hidden, Q = static_cast<long long>(sh.n_heads) * sh.head_dim,
+                  KV = static_cast<long long>(sh.n_kv_heads) * sh.head_dim, I = sh.ffn,
+                  V = sh.vocab, W3 = static_cast<long long>(sh.layers_tapped) * H;
+  std::vector<ParamDesc> ps;
+  long long off = 0;
+  auto add = [&](const char* n, long long r, long long c, bool norm) {
+    ps.push_back({n, r, c, off, norm});
+    off += r * c;
+  };
+  add("fc", H, W3, false);
+  add("w_in", 1, H, true);
+  add("w_hid", 1, H, true);
+  add("qkv", Q + 2 * KV, 2 * H, false);
+  add("o", H, Q, false);
+  add("w_post", 1, H, true);
+  add("gate_up", 2 * I, H, false);
+  add("down", H, I, false);
+  add("w_fin", 1, H, true);
+  add("lm_head", V, H, false);
+  if (total) *total = off;
+  return ps;
+}
+
+// vocabulary chunk of the LM-head backward: multiple of the GEMM N tile, ~32k
+long long vocab_chunk(long long V) {
+  long long vc = std::min<long long>(V, 32768);
+  vc = (vc + gemm::BN - 1) / gemm::BN * gemm::BN;
+  return vc > V ? V : vc;
+}
+
 }  // namespace
+
+// Gradient buckets of the data-parallel exchange, in the order the backward
+// finalises them: LM-head vocabulary chunks, then [down, w_fin], [gate_up],
+// [o, w_post], [qkv], [fc, w_in, w_hid].  Together they tile [0, total).
+std::vector<DpBucket> dp_buckets(const DraftShape& sh) {
+  long long total = 0;
+  const auto ps = param_registry(sh, &total);
+  auto off = [&](const char* n) {
+    for (const auto& p : ps)
+      if (p.name == n) return p.off;
+    throw std::logic_error("registry");
+  };
+  const long long H = sh.hidden, V = sh.vocab, Vc = vocab_chunk(V);
+  std::vector<DpBucket> b;
+  for (long long v0 = 0; v0 < V; v0 += Vc)
+    b.push_back({off("lm_head") + v0 * H, std::min(Vc, V - v0) * H});
+  b.push_back({off("down"), off("lm_head") - off("down")});
+  b.push_back({off("gate_up"), off("down") - off("gate_up")});
+  b.push_back({off("o"), off("gate_up") - off("o")});
+  b.push_back({off("qkv"), off("o") - off("qkv")});
+  b.push_back({0, off("qkv")});
+  return b;
+}
+
+// ZeRO-1 needs every bucket to split into `world` equal shards of whole
+// 8-element (32-byte fp32 / 16-byte bf16) groups.
+bool zero_shardable(const std::vector<DpBucket>& b, int world) {
+  for (const auto& x : b)
+    if (x.n % (8ll * world) != 0) return false;
+  return true;
+}
 
 HiddenStateBuffer* hsbuf_unwrap(struct specsim_hsbuf* b);
 
@@ -106,11 +175,7 @@ void DraftShape::validate() const {
 
 class DraftTrainerImpl {
  public:
-  struct Param {
-    std::string name;
-    long long rows, cols, off;
-    bool norm;
-  };
+  using Param = ParamDesc;
 
   DraftShape sh;
   AdamWConfig opt;
@@ -136,7 +201,12 @@ class DraftTrainerImpl {
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   bool use_nccl = false;              // world > 1, or SPECSIM_FORCE_NCCL=1 (1-rank comm, tests)
-  cudaStream_t comm_stream = nullptr;  // gradient buckets all-reduced behind the backward
+  cudaStream_t comm_stream = nullptr;  // gradient buckets exchanged behind the backward
+  // ZeRO-1 (world > 1 default, SPECSIM_DP_MODE=allreduce to disable): each
+  // bucket is reduce-scattered in place, this rank's shard updated by AdamW on
+  // the comm stream, and the bf16 working weights all-gathered in place
+  bool zero = false;
+  std::vector<DpBucket> buckets;
   std::vector<cudaEvent_t> bucket_events;
   size_t bucket_next = 0;
   cudaEvent_t ev_comm_done = nullptr;
@@ -270,27 +340,10 @@ class DraftTrainerImpl {
       sw.w[j] = static_cast<float>(std::pow(static_cast<double>(sh.ttt_decay), j));
     sw1 = sw;
     sw1.K = 1;
-    // vocabulary chunk for the backward: multiple of the GEMM N tile, ~32k
-    Vc = std::min<long long>(V, 32768);
-    Vc = (Vc + gemm::BN - 1) / gemm::BN * gemm::BN;
-    if (Vc > V) Vc = V;
+    Vc = vocab_chunk(V);
     n_chunks = static_cast<int>((V + Vc - 1) / Vc);
-
-    // registry (same order / layout as the oracle)
-    auto add = [&](const char* n, long long r_, long long c_, bool norm) {
-      params.push_back({n, r_, c_, total, norm});
-      total += r_ * c_;
-    };
-    add("fc", H, W3, false);
-    add("w_in", 1, H, true);
-    add("w_hid", 1, H, true);
-    add("qkv", NQ, 2 * H, false);
-    add("o", H, Q, false);
-    add("w_post", 1, H, true);
-    add("gate_up", 2 * I, H, false);
-    add("down", H, I, false);
-    add("w_fin", 1, H, true);
-    add("lm_head", V, H, false);
+    params = param_registry(sh, &total);
+    buckets = dp_buckets(sh);
 
     SPECSIM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     const long long nb_ce = (V + gemm::BN - 1) / gemm::BN;
@@ -392,6 +445,8 @@ class DraftTrainerImpl {
       SPECSIM_NCCL(nccl::api().CommInitRank(&comm, world, id, rank));
       SPECSIM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
       SPECSIM_CUDA(cudaEventCreateWithFlags(&ev_comm_done, cudaEventDisableTiming));
+      const char* mode = std::getenv("SPECSIM_DP_MODE");
+      zero = !(mode && std::strcmp(mode, "allreduce") == 0) && zero_shardable(buckets, world);
     }
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
   }
@@ -764,14 +819,15 @@ class DraftTrainerImpl {
     return d;
   }
 
-  // Data-parallel exchange: a contiguous range of the flat gradient vector is
-  // final -> all-reduce it on the comm stream while the backward continues.
-  void bucket_ready(const char* first, const char* last, long long elems_override = -1,
-                    long long off_override = -1) {
+  // Data-parallel exchange of bucket i (dp_buckets order): its gradient range
+  // is final.  All-reduce mode: sum it on the comm stream while the backward
+  // continues (AdamW after the join).  ZeRO-1: reduce-scatter in place, AdamW
+  // on this rank's shard and in-place all-gather of the bf16 working weights,
+  // all on the comm stream -- the weights of a finished bucket are not read
+  // again by this step's backward, and the next step joins on ev_comm_done.
+  void bucket_ready(int i) {
     if (!use_nccl) return;
-    const long long off = off_override >= 0 ? off_override : param(first).off;
-    const long long end = param(last).off + param(last).rows * param(last).cols;
-    const long long n = elems_override >= 0 ? elems_override : end - off;
+    const DpBucket& bk = buckets[i];
     if (bucket_next == bucket_events.size()) {
       cudaEvent_t e;
       SPECSIM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -780,8 +836,29 @@ class DraftTrainerImpl {
     cudaEvent_t e = bucket_events[bucket_next++];
     SPECSIM_CUDA(cudaEventRecord(e, stream));
     SPECSIM_CUDA(cudaStreamWaitEvent(comm_stream, e, 0));
-    SPECSIM_NCCL(nccl::api().AllReduce(G + off, G + off, static_cast<size_t>(n), ncclFloat, ncclSum,
-                                       comm, comm_stream));
+    if (!zero) {
+      SPECSIM_NCCL(nccl::api().AllReduce(G + bk.off, G + bk.off, static_cast<size_t>(bk.n),
+                                         ncclFloat, ncclSum, comm, comm_stream));
+      return;
+    }
+    const long long c = bk.n / world, o = bk.off + rank * c;
+    SPECSIM_NCCL(nccl::api().ReduceScatter(G + bk.off, G + o, static_cast<size_t>(c), ncclFloat,
+                                           ncclSum, comm, comm_stream));
+    kern::adamw(c, P + o, Mst + o, Vst + o, G + o, P16 + o, adam_dev, comm_stream);
+    SPECSIM_NCCL(nccl::api().AllGather(P16 + o, P16 + bk.off, static_cast<size_t>(c),
+                                       ncclBfloat16, comm, comm_stream));
+  }
+
+  // ZeRO-1 keeps each rank's fp32 master current on its own shards only:
+  // all-gather them (collective: every rank must call it, same order).
+  void sync_master() {
+    if (!zero || world == 1) return;
+    for (const auto& bk : buckets) {
+      const long long c = bk.n / world, o = bk.off + rank * c;
+      SPECSIM_NCCL(nccl::api().AllGather(P + o, P + bk.off, static_cast<size_t>(c), ncclFloat,
+                                         comm, stream));
+    }
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
   }
 
   // Attention backward of pass j (K > 1): D_j, the cache entries (j >= 1),
@@ -821,7 +898,7 @@ class DraftTrainerImpl {
       run(p_lm_dx[c], PH_LM);
       run_dw(p_lm_dw[c], f_lm_dw[c], PH_LM);
       // LM-head rows of this chunk are final: their all-reduce overlaps the rest
-      bucket_ready("lm_head", "lm_head", vn * H, param("lm_head").off + v0 * H);
+      bucket_ready(c);
     }
     if (K > 1)
       timed(PH_ELEM, 0, [&] {
@@ -844,7 +921,7 @@ class DraftTrainerImpl {
       run(p_dact[j]);
       if (j == 0) {
         run_dw(p_dw_down, f_dw_down);
-        bucket_ready("down", "w_fin");
+        bucket_ready(n_chunks);  // down, w_fin
       }
       timed(PH_ELEM, 0, [&] {
         kern::swiglu_bwd(gu + R * 2 * I, dact, dgu + R * 2 * I, T, sh.ffn, stream);
@@ -852,7 +929,7 @@ class DraftTrainerImpl {
       run(p_dz[j]);
       if (j == 0) {
         run_dw(p_dw_gu, f_dw_gu);
-        bucket_ready("gate_up", "gate_up");
+        bucket_ready(n_chunks + 1);  // gate_up
       }
       timed(PH_ELEM, 0, [&] {
         kern::rmsnorm_bwd(dz + R * H, H, r + R * H, H, nullptr, pf("w_post"), rstd_post + R, dh,
@@ -867,7 +944,7 @@ class DraftTrainerImpl {
                               nullptr, H, gf("w_post"), dw_part, KT, sh.hidden, stream);
           });
         run_dw(p_dw_o, f_dw_o);
-        bucket_ready("o", "w_post");
+        bucket_ready(n_chunks + 2);  // o, w_post
       }
       if (one) {
         attn::Dims ad = attn_dims();
@@ -888,7 +965,7 @@ class DraftTrainerImpl {
       run(p_dU[j]);
       if (j == 0) {
         run_dw(p_dw_qkv, f_dw_qkv);
-        bucket_ready("qkv", "qkv");
+        bucket_ready(n_chunks + 3);  // qkv
       }
       timed(PH_ELEM, 0, [&] {
         float* dUj = dU + R * 2 * H;
@@ -909,7 +986,7 @@ class DraftTrainerImpl {
       });
     }
     run_dw(p_dw_fc, f_dw_fc);
-    bucket_ready("fc", "w_hid");
+    bucket_ready(n_chunks + 4);  // fc, w_in, w_hid
     if (use_nccl) {
       // join: AdamW waits for every bucket
       timed(PH_COMM, 0, [&] {
@@ -921,6 +998,7 @@ class DraftTrainerImpl {
 
   void snapshot() {
     SPECSIM_CUDA(cudaSetDevice(device));
+    sync_master();
     const size_t f = sizeof(float) * static_cast<size_t>(total);
     if (!snap) SPECSIM_CUDA(cudaMalloc(&snap, 3 * f + sizeof(__nv_bfloat16) * total));
     char* s = static_cast<char*>(snap);
@@ -991,6 +1069,7 @@ class DraftTrainerImpl {
   }
 
   void optimizer_update() {
+    if (zero) return;  // every shard was updated on the comm stream (bucket_ready)
     if (!fused_adamw()) {
       timed(PH_ADAM, 0, [&] { kern::adamw(total, P, Mst, Vst, G, P16, adam_dev, stream); });
       return;
@@ -1225,6 +1304,25 @@ DraftTrainerImpl& impl_of(const specsim_trainer* t) {
   if (!t || !t->t) throw std::invalid_argument("null trainer");
   return const_cast<DraftTrainer*>(t->t)->impl();
 }
+DraftShape to_shape(const specsim_draft_shape* shape) {
+  if (!shape) throw std::invalid_argument("null shape");
+  DraftShape s;
+  s.hidden = shape->hidden;
+  s.vocab = shape->vocab;
+  s.seq_len = shape->seq_len;
+  s.n_heads = shape->n_heads;
+  s.n_kv_heads = shape->n_kv_heads;
+  s.head_dim = shape->head_dim;
+  s.ffn = shape->ffn;
+  s.layers_tapped = shape->layers_tapped;
+  s.micro_batch = shape->micro_batch;
+  s.rms_eps = shape->rms_eps;
+  s.rope_theta = shape->rope_theta;
+  s.ttt_steps = shape->ttt_steps > 0 ? shape->ttt_steps : 1;
+  s.ttt_decay = shape->ttt_decay > 0.f ? shape->ttt_decay : 0.8f;
+  return s;
+}
+
 void fill(specsim_step_result* out, const StepResult& r) {
   if (!out) return;
   out->loss = r.loss;
@@ -1252,20 +1350,7 @@ int specsim_trainer_create(const specsim_draft_shape* shape, const specsim_adamw
                            specsim_trainer** out) {
   return guard([&] {
     if (!shape || !out) throw std::invalid_argument("null argument");
-    DraftShape s;
-    s.hidden = shape->hidden;
-    s.vocab = shape->vocab;
-    s.seq_len = shape->seq_len;
-    s.n_heads = shape->n_heads;
-    s.n_kv_heads = shape->n_kv_heads;
-    s.head_dim = shape->head_dim;
-    s.ffn = shape->ffn;
-    s.layers_tapped = shape->layers_tapped;
-    s.micro_batch = shape->micro_batch;
-    s.rms_eps = shape->rms_eps;
-    s.rope_theta = shape->rope_theta;
-    s.ttt_steps = shape->ttt_steps > 0 ? shape->ttt_steps : 1;
-    s.ttt_decay = shape->ttt_decay > 0.f ? shape->ttt_decay : 0.8f;
+    const DraftShape s = to_shape(shape);
     AdamWConfig a;
     if (opt) {
       a.lr = opt->lr;
@@ -1275,6 +1360,27 @@ int specsim_trainer_create(const specsim_draft_shape* shape, const specsim_adamw
       a.weight_decay = opt->weight_decay;
     }
     *out = new specsim_trainer{new DraftTrainer(s, a, seed, rank, world, nccl_id, device)};
+  });
+}
+
+int specsim_dp_buckets(const specsim_draft_shape* shape, int32_t world, int64_t* off, int64_t* n,
+                       int32_t cap, int32_t* count, int32_t* zero_ok) {
+  return guard([&] {
+    const DraftShape s = to_shape(shape);
+    // layout only: the kernel constraints of validate() do not apply here
+    Problems p("invalid draft shape");
+    p.check(s.hidden > 0 && s.vocab > 0 && s.ffn > 0 && s.n_heads > 0 && s.n_kv_heads > 0 &&
+                s.head_dim > 0 && s.layers_tapped > 0,
+            "dimensions must be positive");
+    p.check(world >= 1, "world must be >= 1");
+    p.throw_if_any();
+    const auto b = dp_buckets(s);
+    if (count) *count = static_cast<int32_t>(b.size());
+    for (size_t i = 0; i < b.size() && static_cast<int32_t>(i) < cap; ++i) {
+      if (off) off[i] = b[i].off;
+      if (n) n[i] = b[i].n;
+    }
+    if (zero_ok) *zero_ok = zero_shardable(b, world) ? 1 : 0;
   });
 }
 
@@ -1351,6 +1457,7 @@ int specsim_trainer_get_param(const specsim_trainer* t, const char* name, float*
     const auto& p = im.param(name ? name : "");
     DeviceGuard dg(im.device);
     SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    im.sync_master();
     SPECSIM_CUDA(cudaMemcpy(host_out, im.P + p.off, sizeof(float) * p.rows * p.cols,
                             cudaMemcpyDeviceToHost));
   });

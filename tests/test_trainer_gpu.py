@@ -170,12 +170,16 @@ def test_step_is_deterministic():
     buf.close()
 
 
-def test_fused_adamw_equals_separate_path(monkeypatch):
+@pytest.mark.parametrize("mode", ["zero", "allreduce"])
+def test_fused_adamw_equals_separate_path(monkeypatch, mode):
     """Single replica: AdamW fused into the weight-gradient GEMM epilogue.  The
-    data-parallel path (grads materialised, bucketed NCCL all-reduce on a comm
-    stream, standalone AdamW) is forced with a 1-rank communicator; both must
-    give the same losses and weights over three steps."""
+    data-parallel path is forced with a 1-rank communicator, in both modes:
+    ZeRO-1 (per bucket on the comm stream: in-place reduce-scatter, AdamW on
+    the rank's shard, in-place all-gather of the bf16 weights) and all-reduce
+    (bucketed NCCL all-reduce, standalone AdamW after the join).  All must give
+    the same losses and weights over three steps."""
     c = SHAPES["C1"]
+    monkeypatch.setenv("SPECSIM_DP_MODE", mode)
     buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 16)
     for i in range(8):
         cap = oracle.synth_capture(SEED, i, 130, c["vocab"], c["hidden"])
