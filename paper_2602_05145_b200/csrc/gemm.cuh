@@ -87,8 +87,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int B_STAGE_BYTES = C_::B_STAGE;
   constexpr int STAGE_BYTES = C_::STAGE;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment by offsetting the __shared__ array itself (not via an
+  // integer round-trip), so the compiler keeps the shared address space and
+  // the epilogue's staging accesses compile to LDS / STS, not generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * A_STAGE_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
