@@ -297,3 +297,49 @@ def test_stored_logits_equal_recompute(name, monkeypatch):
     assert abs(l0 - l1) <= 1e-6 * abs(l1)
     for nm in g0:
         assert rel(g0[nm], g1[nm]) <= 1e-5, (nm, rel(g0[nm], g1[nm]))
+
+
+def test_step_matches_oracle_at_bench_model_dims():
+    """Parity at the bench workload's model dimensions (C2: H 4096, 3H concat,
+    V 128256 = 4 vocabulary chunks with a ragged last one, 32 q / 8 kv heads of
+    128, FFN 14336; 818.9 M parameters) on a short batch (S 128, B 2: one full
+    sample and one masked tail) so the CPU oracle finishes in seconds.  The
+    oracle starts from the trainer's own weights (init is bit-exact, tested
+    above at small shapes)."""
+    c = dict(api.CONFIGS["C2"], seq_len=128, micro_batch=2)
+    shp = oshape(c)
+    tr = api.DraftTrainer(c, lr=HP[0], betas=(HP[1], HP[2]), eps=HP[3], weight_decay=HP[4],
+                          seed=SEED)
+    tr.keep_grads(True)
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 12)
+    samples = []
+    for i, L in enumerate([c["seq_len"] + 2, 77]):
+        cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+        samples.append((cap["ids"], cap["features"]))
+    F, u, y, m = oracle.gather_batch(shp, samples)
+    layout, total = oracle.param_layout(shp)
+    P = np.zeros(total, np.float32)
+    for nm, rr, cc, off in layout:
+        P[off:off + rr * cc] = tr.get_param(nm).reshape(-1)
+    E = tr.get_embedding()
+    P0 = P.copy()
+    Mst, Vst = np.zeros_like(P), np.zeros_like(P)
+    out, grads = oracle.train_step(shp, HP, 1, P, Mst, Vst, E, F, u, y, m, round_bf16=True)
+    r = tr.step(buf, [0, 1])
+    assert r["valid_tokens"] == out.valid == int(m.sum())
+    assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
+    errs = {}
+    for nm, rr, cc, off in layout:
+        g_cpu = grads[off:off + rr * cc]
+        e = rel(tr.get_grad(nm).reshape(-1), g_cpu)
+        errs[nm] = round(e, 5)
+        assert e <= 1e-2, (nm, e)
+        d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
+        d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
+        well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
+        ok = np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]
+        assert ok.mean() >= 0.99, (nm, ok.mean())
+    print("C2-dims grad rel errors:", errs)
+    tr.close()
+    buf.close()
