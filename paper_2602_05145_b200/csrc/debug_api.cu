@@ -37,12 +37,12 @@ extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi_cg, int32_t M, int
     Problems pr("specsim_debug_gemm");
     pr.check(M > 0 && N > 0 && K > 0, "M, N, K must be > 0");
     pr.check(A && B && C, "A, B, C must be non-null");
-    pr.check(epi >= 0 && epi <= 3, "epi must be 0..3");
+    pr.check((epi >= 0 && epi <= 3) || epi == 6, "epi must be 0..3 or 6 (fused AdamW)");
     pr.check(epi != 3 || R, "epi 3 needs R");
     pr.throw_if_any();
     const size_t a_elems = static_cast<size_t>(a_mn ? K : M) * lda;
     const size_t b_elems = static_cast<size_t>(b_mn ? K : N) * ldb;
-    const size_t c_esz = (epi == 1 || epi == 2) ? 4 : 2;
+    const size_t c_esz = (epi == 1 || epi == 2 || epi == 6) ? 4 : 2;
     const size_t c_bytes = static_cast<size_t>(M) * ldc * c_esz;
     DevBuf dA(a_elems * 2), dB(b_elems * 2), dC(c_bytes), dR(R ? static_cast<size_t>(M) * ldr * 2 : 0);
     SPECSIM_CUDA(cudaMemcpy(dA.p, A, a_elems * 2, cudaMemcpyHostToDevice));
@@ -54,6 +54,22 @@ extern "C" int specsim_debug_gemm(int a_mn, int b_mn, int epi_cg, int32_t M, int
     args.ldc = ldc;
     args.R = static_cast<const __nv_bfloat16*>(dR.p);
     args.ldr = ldr;
+    // epi 6: AdamW fused into the epilogue over device-resident state laid
+    // out like C (p = C's fp32 contents, m = v = 0, step 1); C receives p
+    const size_t n_state = static_cast<size_t>(M) * ldc;
+    DevBuf dM(epi == 6 ? n_state * 4 : 0), dV(epi == 6 ? n_state * 4 : 0),
+        dP16(epi == 6 ? n_state * 2 : 0), dHp(epi == 6 ? sizeof(gemm::AdamDev) : 0);
+    if (epi == 6) {
+      SPECSIM_CUDA(cudaMemset(dM.p, 0, n_state * 4));
+      SPECSIM_CUDA(cudaMemset(dV.p, 0, n_state * 4));
+      const gemm::AdamDev hp{1e-3f, 0.9f, 0.95f, 1e-8f, 1.f, 1e-3f / 0.1f, std::sqrt(0.05f), 0.f};
+      SPECSIM_CUDA(cudaMemcpy(dHp.p, &hp, sizeof(hp), cudaMemcpyHostToDevice));
+      args.opt_p = static_cast<float*>(dC.p);
+      args.opt_m = static_cast<float*>(dM.p);
+      args.opt_v = static_cast<float*>(dV.p);
+      args.opt_p16 = static_cast<__nv_bfloat16*>(dP16.p);
+      args.opt_hp = static_cast<const gemm::AdamDev*>(dHp.p);
+    }
     gemm::GemmPlan plan = gemm::make_plan({dA.p, lda, a_mn != 0}, {dB.p, ldb, b_mn != 0}, M, N,
                                           K, epi, args, cg);
     cudaStream_t s;

@@ -433,7 +433,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // 8 row groups' DRAM latencies overlap
           // AdamW keeps three state vectors per row group in flight: hoist 4
           // row groups at a time so everything stays in registers
-          constexpr int RG = EPI == EPI_ADAMW ? 4 : 8;
+#ifndef SPECSIM_ADAMW_VARIANT
+#define SPECSIM_ADAMW_VARIANT 0  // probe builds only (scripts/adamw_probe.sh)
+#endif
+          constexpr int RG = EPI == EPI_ADAMW ? (SPECSIM_ADAMW_VARIANT == 4 ? 8 : 4) : 8;
 #pragma unroll
           for (int g0 = 0; g0 < 8; g0 += RG) {
           float4 v[RG], x1[RG], x2[RG], x3[RG];
@@ -462,9 +465,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e_it);
             } else if constexpr (EPI == EPI_ADAMW) {
               if (okm >> it & 1) {  // optimizer state streams once: evict-first
-                x1[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_p + e_it));
-                x2[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_m + e_it));
-                x3[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_v + e_it));
+                if constexpr (SPECSIM_ADAMW_VARIANT == 1) {
+                  x1[it] = make_float4(0.01f, 0.01f, 0.01f, 0.01f);
+                  x2[it] = x3[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else if constexpr (SPECSIM_ADAMW_VARIANT == 3) {
+                  x1[it] = *reinterpret_cast<const float4*>(args.opt_p + e_it);
+                  x2[it] = *reinterpret_cast<const float4*>(args.opt_m + e_it);
+                  x3[it] = *reinterpret_cast<const float4*>(args.opt_v + e_it);
+                } else {
+                  x1[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_p + e_it));
+                  x2[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_m + e_it));
+                  x3[it] = __ldcs(reinterpret_cast<const float4*>(args.opt_v + e_it));
+                }
               }
             } else if constexpr (EPI == EPI_CE_BWD) {
               // row constants: x1 = {lse, coef, target (bits)}
@@ -523,11 +535,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float denom = sqrtf(sa[j]) / hp.bc2_sqrt + hp.eps;
                 pa[j] = pi - hp.step_size * (ma[j] / denom);
               }
-              __stcs(reinterpret_cast<float4*>(args.opt_p + e_it), p);
-              __stcs(reinterpret_cast<float4*>(args.opt_m + e_it), m);
-              __stcs(reinterpret_cast<float4*>(args.opt_v + e_it), s2);
-              __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e_it),
-                     make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w)));
+              if constexpr (SPECSIM_ADAMW_VARIANT == 2) {
+                // probe: only the bf16 working copy is stored
+                __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e_it),
+                       make_uint2(ptx::pack_bf16x2(p.x + m.x + s2.x, p.y + m.y + s2.y),
+                                  ptx::pack_bf16x2(p.z + m.z + s2.z, p.w + m.w + s2.w)));
+              } else if constexpr (SPECSIM_ADAMW_VARIANT == 3) {
+                *reinterpret_cast<float4*>(args.opt_p + e_it) = p;
+                *reinterpret_cast<float4*>(args.opt_m + e_it) = m;
+                *reinterpret_cast<float4*>(args.opt_v + e_it) = s2;
+                *reinterpret_cast<uint2*>(args.opt_p16 + e_it) =
+                    make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w));
+              } else {
+                __stcs(reinterpret_cast<float4*>(args.opt_p + e_it), p);
+                __stcs(reinterpret_cast<float4*>(args.opt_m + e_it), m);
+                __stcs(reinterpret_cast<float4*>(args.opt_v + e_it), s2);
+                __stcs(reinterpret_cast<uint2*>(args.opt_p16 + e_it),
+                       make_uint2(ptx::pack_bf16x2(p.x, p.y), ptx::pack_bf16x2(p.z, p.w)));
+              }
               if (args.opt_g) __stcs(reinterpret_cast<float4*>(args.opt_g + e_it), w);
             }
           }
