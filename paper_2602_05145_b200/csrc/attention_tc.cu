@@ -7,8 +7,10 @@
 //               S buffers, then O += P_j V_j with P_j from shared memory
 //   warps 2..5  softmax: one query row per thread (TMEM lane), so row max /
 //               sum need no shuffles; P_j written to smem in the UMMA K-major
-//               SW128 layout; lazy rescaling (only when the row max grows by
-//               more than 2^8) keeps O read-modify-writes rare
+//               SW128 layout, double-buffered so the softmax of block j+1
+//               overlaps the PV MMA of block j; lazy rescaling (only when the
+//               row max grows by more than 2^8) keeps O read-modify-writes --
+//               the one step that must wait for PV_j -- rare
 // TMEM: S0 | S1 | O  (128 + 128 + HD fp32 columns).
 #include <cuda_bf16.h>
 
@@ -35,8 +37,8 @@ struct FwdSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q;          // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV;     // 2 stages
-  static constexpr int OFF_P = OFF_V + 2 * KV;
-  static constexpr int OFF_BAR = OFF_P + P;
+  static constexpr int OFF_P = OFF_V + 2 * KV;     // 2 buffers
+  static constexpr int OFF_BAR = OFF_P + 2 * P;
   static constexpr int BYTES = 1024 + OFF_BAR + 256;
 };
 
@@ -87,9 +89,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* v_empty = bar + 7;   // [2]
   uint64_t* s_full = bar + 9;    // [2]
   uint64_t* s_free = bar + 11;   // [2]
-  uint64_t* p_full = bar + 13;
-  uint64_t* pv_done = bar + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* p_full = bar + 13;   // [2]
+  uint64_t* pv_done = bar + 15;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
 
   const int qb = gridDim.x - 1 - blockIdx.x;  // most keys first
   const int h = blockIdx.y, b = blockIdx.z;
@@ -108,9 +110,9 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_init(&v_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_free[i], 4);
+      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&pv_done[i], 1);
     }
-    ptx::mbar_init(p_full, 4);
-    ptx::mbar_init(pv_done, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(192, 1)
       // ------------------------------------------------------------ MMA
       constexpr uint32_t idS = ptx::make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idO = ptx::make_idesc_bf16(BQ, HD, false, true);
-      const uint32_t aQ = ptx::smem_u32(sQ), aP = ptx::smem_u32(sP);
+      const uint32_t aQ = ptx::smem_u32(sQ);
       auto issue_s = [&](int j) {
         const int s = j & 1;
         ptx::mbar_wait(&k_full[s], (j >> 1) & 1);
@@ -166,15 +168,16 @@ __global__ void __launch_bounds__(192, 1)
       issue_s(0);
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) issue_s(j + 1);
-        const int s = j & 1;
-        ptx::mbar_wait(p_full, j & 1);
+        const int s = j & 1;  // K / V stage, S buffer and P buffer of block j
+        ptx::mbar_wait(&p_full[s], (j >> 1) & 1);
         ptx::mbar_wait(&v_full[s], (j >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aV = ptx::smem_u32(sV + s * L::KV);
+        const uint32_t aP = ptx::smem_u32(sP + s * L::P);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           ptx::umma_bf16(tO, kdesc(aP, kk), mndesc(aV, kk), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::umma_commit(pv_done);
+        ptx::umma_commit(&pv_done[s]);
         ptx::umma_commit(&v_empty[s]);
       }
     }
@@ -190,32 +193,41 @@ __global__ void __launch_bounds__(192, 1)
       const int s = j & 1;
       ptx::mbar_wait(&s_full[s], (j >> 1) & 1);
       ptx::tc_fence_after();
-      // row max over this block's 128 scores
-      float mx = -INFINITY;
+      // Row max over this block's 128 raw scores.  One softmax warp per SM
+      // sub-partition, so the softmax is issue-bound: 3-input max with 4
+      // independent partials, the scale folded into the exponent's FFMA2
+      // (max(s * c) = c * max(s), c > 0), MUFU ex2 without range fix-up, and
+      // packed fp32x2 row sums -- ~3 instructions per score instead of ~10.
       uint32_t v[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS[s] + lane_off + c * 32, v[c]);
       ptx::tmem_ld_wait();
-      const bool diag = (j == qb);
+      if (j == qb) {  // diagonal block: keys after the query are masked
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > r) v[c][i] = __float_as_uint(-INFINITY);
+      }
+      float mxp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x = __uint_as_float(v[c][i]) * sl2;
-          if (diag && (c * 32 + i) > r) x = -INFINITY;
-          v[c][i] = __float_as_uint(x);
-          mx = fmaxf(mx, x);
+        for (int i = 0; i < 32; i += 8) {
+          mxp[0] = ptx::max3f(mxp[0], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
+          mxp[1] = ptx::max3f(mxp[1], __uint_as_float(v[c][i + 2]), __uint_as_float(v[c][i + 3]));
+          mxp[2] = ptx::max3f(mxp[2], __uint_as_float(v[c][i + 4]), __uint_as_float(v[c][i + 5]));
+          mxp[3] = ptx::max3f(mxp[3], __uint_as_float(v[c][i + 6]), __uint_as_float(v[c][i + 7]));
         }
+      const float mx = ptx::max3f(mxp[0], mxp[1], fmaxf(mxp[2], mxp[3])) * sl2;
       // S buffer consumed: the MMA may overwrite it with S_{j+2}
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&s_free[s]);
-      // O and the P buffer are free once PV_{j-1} has completed
-      if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);
-      ptx::tc_fence_after();
       // lazy rescale: a row moves its reference max only when the max grows by
       // more than 2^8; the O read-modify-write is warp-collective (tcgen05.ld /
       // st are .sync.aligned), so the whole warp does it when any lane needs it
+      // -- and only then waits for every PV so far (PV_{j-1}) to have landed
       const bool need = mx > m_run + 8.f;
       float corr = 1.f;
       if (need) {
@@ -223,7 +235,10 @@ __global__ void __launch_bounds__(192, 1)
         l_run *= corr;
         m_run = mx;
       }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
+      const bool rescale = j > 0 && __any_sync(0xffffffffu, need);
+      if (rescale) {
+        ptx::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
@@ -235,17 +250,29 @@ __global__ void __launch_bounds__(192, 1)
         }
         tmem_st_wait();
       }
-      // P = exp2(s - m) -> bf16, K-major SW128: row r, 16-byte chunk cc of
-      // tile t at t*TILE + r*128 + ((cc ^ (r & 7)) * 16)
+      // P buffer s was last read by PV_{j-2}
+      if (j >= 2) ptx::mbar_wait(&pv_done[s], ((j - 2) >> 1) & 1);
+      uint8_t* sPb = sP + s * L::P;
+      // P = 2^(s * scale * log2e - m) -> bf16, K-major SW128: row r, 16-byte
+      // chunk cc of tile t at t*TILE + r*128 + ((cc ^ (r & 7)) * 16); row
+      // sum in 4 packed fp32x2 partials
+      const uint64_t scale2 = ptx::f32x2(sl2, sl2), negm2 = ptx::f32x2(-m_run, -m_run);
+      uint64_t lp2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           float p[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = exp2f(__uint_as_float(v[c][i + e]) - m_run);
-            l_run += p[e];
+          for (int e = 0; e < 8; e += 2) {
+            const uint64_t x2 = ptx::ffma2(
+                ptx::f32x2(__uint_as_float(v[c][i + e]), __uint_as_float(v[c][i + e + 1])), scale2,
+                negm2);
+            float x0, x1;
+            ptx::f32x2_split(x2, x0, x1);
+            p[e] = ptx::ex2_ftz(x0);
+            p[e + 1] = ptx::ex2_ftz(x1);
+            lp2[e >> 1] = ptx::fadd2(lp2[e >> 1], ptx::f32x2(p[e], p[e + 1]));
           }
           const int key = c * 32 + i;  // 8 keys = one 16-byte chunk
           const int t = key >> 6, cc = (key & 63) >> 3;
@@ -254,15 +281,22 @@ __global__ void __launch_bounds__(192, 1)
           pk.y = ptx::pack_bf16x2(p[2], p[3]);
           pk.z = ptx::pack_bf16x2(p[4], p[5]);
           pk.w = ptx::pack_bf16x2(p[6], p[7]);
-          *reinterpret_cast<uint4*>(sP + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) = pk;
+          *reinterpret_cast<uint4*>(sPb + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) = pk;
         }
+      }
+      {
+        float a0, a1, b0, b1;
+        ptx::f32x2_split(ptx::fadd2(ptx::fadd2(lp2[0], lp2[1]), ptx::fadd2(lp2[2], lp2[3])), a0, a1);
+        (void)b0;
+        (void)b1;
+        l_run += a0 + a1;
       }
       ptx::fence_proxy_async_smem();  // generic-proxy P writes -> tensor-core reads
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(p_full);
+      if (lane == 0) ptx::mbar_arrive(&p_full[s]);
     }
-    ptx::mbar_wait(pv_done, (nkv - 1) & 1);
+    ptx::mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     ptx::tc_fence_after();
     const long long T = static_cast<long long>(d.B) * d.S;
     // Training-time-test cache entries (unroll step n_diag >= 1): one extra
