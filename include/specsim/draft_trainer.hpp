@@ -12,11 +12,29 @@
 #include <deque>
 #include <memory>
 #include <random>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
 namespace specsim {
+
+// ---------------------------------------------------------------- errors
+// The reference's split (proj/include/specsim/errors.hpp:8-13):
+// std::invalid_argument = domain error (CLI exit 1), ConfigError =
+// configuration error (CLI exit 2); device failures have their own types.
+class ConfigError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class NcclError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
 
 // ------------------------------------------------------------------ Rng
 // Seeded mt19937_64 with hand-rolled conversions so a seed reproduces the

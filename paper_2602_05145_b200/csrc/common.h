@@ -14,23 +14,9 @@
 #include <vector>
 
 #include "specsim_draft_trainer.h"
+#include "specsim/draft_trainer.hpp"  // ConfigError / CudaError / NcclError (public)
 
 namespace specsim {
-
-class ConfigError : public std::runtime_error {
- public:
-  using std::runtime_error::runtime_error;
-};
-
-class CudaError : public std::runtime_error {
- public:
-  using std::runtime_error::runtime_error;
-};
-
-class NcclError : public std::runtime_error {
- public:
-  using std::runtime_error::runtime_error;
-};
 
 [[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
   throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
