@@ -640,27 +640,43 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_wait(&p_free[st], ((it >> 1) & 1) ^ 1);
       uint8_t* sP = smem + L::OFF_P + st * TILE;
       uint8_t* sS = smem + L::OFF_DS + st * TILE;
+      // causal mask only where this 64-query block crosses the key block's
+      // diagonal (warp-uniform test); packed fp32x2 arithmetic and ftz ex2:
+      // P = 2^(s * scale * log2e - lse * log2e), dS = P (dP - D)
+      const bool masked = q0 < kb * BKV + BKV;
+      const uint64_t sl2x2 = ptx::f32x2(sl2, sl2), nlog2e = ptx::f32x2(-kLog2e, -kLog2e);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
-          float p[8], ds[8];
+          uint32_t pp[4], dd[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
+          for (int e = 0; e < 8; e += 2) {
             const int qi = c * 32 + i + e;
-            float v = exp2f(__uint_as_float(sv[c][i + e]) * sl2 - l2[qi] * kLog2e);
-            if (q0 + qi < key) v = 0.f;  // causal: query before key
-            p[e] = v;
-            ds[e] = v * (__uint_as_float(pv[c][i + e]) - Dq[qi]);
+            const float2 lq = *reinterpret_cast<const float2*>(l2 + qi);
+            const float2 dq = *reinterpret_cast<const float2*>(Dq + qi);
+            const uint64_t x = ptx::ffma2(
+                ptx::f32x2(__uint_as_float(sv[c][i + e]), __uint_as_float(sv[c][i + e + 1])),
+                sl2x2, ptx::fmul2(ptx::f32x2(lq.x, lq.y), nlog2e));
+            float x0, x1;
+            ptx::f32x2_split(x, x0, x1);
+            float p0 = ptx::ex2_ftz(x0), p1 = ptx::ex2_ftz(x1);
+            if (masked) {  // causal: query before key
+              if (q0 + qi < key) p0 = 0.f;
+              if (q0 + qi + 1 < key) p1 = 0.f;
+            }
+            const uint64_t p2 = ptx::f32x2(p0, p1);
+            const uint64_t ds2 = ptx::fmul2(
+                p2, ptx::fadd2(ptx::f32x2(__uint_as_float(pv[c][i + e]),
+                                          __uint_as_float(pv[c][i + e + 1])),
+                               ptx::f32x2(-dq.x, -dq.y)));
+            pp[e >> 1] = ptx::pack_bf16x2_2(p2);
+            dd[e >> 1] = ptx::pack_bf16x2_2(ds2);
           }
           const int cc = (c * 32 + i) >> 3;  // 16-byte chunk within the 128-byte row
           const int off = r * 128 + ((cc ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(sP + off) =
-              make_uint4(ptx::pack_bf16x2(p[0], p[1]), ptx::pack_bf16x2(p[2], p[3]),
-                         ptx::pack_bf16x2(p[4], p[5]), ptx::pack_bf16x2(p[6], p[7]));
-          *reinterpret_cast<uint4*>(sS + off) =
-              make_uint4(ptx::pack_bf16x2(ds[0], ds[1]), ptx::pack_bf16x2(ds[2], ds[3]),
-                         ptx::pack_bf16x2(ds[4], ds[5]), ptx::pack_bf16x2(ds[6], ds[7]));
+          *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[0], pp[1], pp[2], pp[3]);
+          *reinterpret_cast<uint4*>(sS + off) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
         }
       }
       ptx::fence_proxy_async_smem();
@@ -824,6 +840,8 @@ __global__ void __launch_bounds__(192, 1)
     const float sl2 = d.scale * kLog2e;
     const float l2 = lse[h * T + row0 + q] * kLog2e;
     const float Dr = Dv[h * T + row0 + q];
+    const uint64_t sl2x2 = ptx::f32x2(sl2, sl2), nl2x2 = ptx::f32x2(-l2, -l2),
+                   nD2 = ptx::f32x2(-Dr, -Dr);
     uint8_t* sS = smem + L::OFF_DS;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(s_full, j & 1);
@@ -840,19 +858,30 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
-          float ds[8];
+          uint32_t dd[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
+          for (int e = 0; e < 8; e += 2) {
             const int kcol = c * 32 + i + e;
-            float p = exp2f(__uint_as_float(sv[i + e]) * sl2 - l2);
-            if (diag && kcol > r) p = 0.f;
-            ds[e] = p * (__uint_as_float(pv[i + e]) - Dr);
+            // P = 2^(s * scale * log2e - lse * log2e), dS = P (dP - D): packed fp32x2
+            const uint64_t x = ptx::ffma2(
+                ptx::f32x2(__uint_as_float(sv[i + e]), __uint_as_float(sv[i + e + 1])), sl2x2,
+                nl2x2);
+            float x0, x1;
+            ptx::f32x2_split(x, x0, x1);
+            float p0 = ptx::ex2_ftz(x0), p1 = ptx::ex2_ftz(x1);
+            if (diag) {
+              if (kcol > r) p0 = 0.f;
+              if (kcol + 1 > r) p1 = 0.f;
+            }
+            dd[e >> 1] = ptx::pack_bf16x2_2(ptx::fmul2(
+                ptx::f32x2(p0, p1),
+                ptx::fadd2(ptx::f32x2(__uint_as_float(pv[i + e]), __uint_as_float(pv[i + e + 1])),
+                           nD2)));
           }
           const int key = c * 32 + i;
           const int t = key >> 6, cc = (key & 63) >> 3;
           *reinterpret_cast<uint4*>(sS + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(ptx::pack_bf16x2(ds[0], ds[1]), ptx::pack_bf16x2(ds[2], ds[3]),
-                         ptx::pack_bf16x2(ds[4], ds[5]), ptx::pack_bf16x2(ds[6], ds[7]));
+              make_uint4(dd[0], dd[1], dd[2], dd[3]);
         }
       }
       ptx::tc_fence_before();
