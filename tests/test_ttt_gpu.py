@@ -136,3 +136,30 @@ def test_ttt_shape_validation():
         api.DraftTrainer(c, seed=SEED)
     with pytest.raises(Exception):
         api.DraftTrainer(dict(CASES["C1_k3"], ttt_steps=17), seed=SEED)
+
+
+@pytest.mark.parametrize("mode", ["zero", "allreduce"])
+def test_ttt_data_parallel_path_equals_fused(monkeypatch, mode):
+    """Training-time test through the data-parallel exchange (forced 1-rank
+    NCCL communicator: per-bucket ZeRO-1 reduce-scatter / shard AdamW /
+    all-gather, or all-reduce + AdamW after the join) gives the losses and
+    weights of the fused single-replica path."""
+    c = CASES["C1_k3"]
+    S, B = c["seq_len"], c["micro_batch"]
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 16)
+    for i in range(B):
+        cap = oracle.synth_capture(SEED, i, S + 5, c["vocab"], c["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+    fused = api.DraftTrainer(c, lr=1e-3, seed=SEED)
+    monkeypatch.setenv("SPECSIM_DP_MODE", mode)
+    monkeypatch.setenv("SPECSIM_FORCE_NCCL", "1")
+    dp = api.DraftTrainer(c, lr=1e-3, seed=SEED)
+    monkeypatch.delenv("SPECSIM_FORCE_NCCL")
+    for k in range(2):
+        ids = list(range(B))
+        r1, r2 = fused.step(buf, ids), dp.step(buf, ids)
+        assert abs(r1["loss"] - r2["loss"]) <= 1e-4 * abs(r2["loss"]), (k, r1, r2)
+    for nm in ("fc", "qkv", "o", "gate_up", "down", "lm_head", "w_in", "w_hid", "w_post", "w_fin"):
+        a, b = fused.get_param(nm), dp.get_param(nm)
+        assert np.abs(a - b).max() <= 2e-2 * 1e-3 + 1e-6 * np.abs(b).max(), nm
+    fused.close(); dp.close(); buf.close()
