@@ -163,3 +163,40 @@ def test_ttt_data_parallel_path_equals_fused(monkeypatch, mode):
         a, b = fused.get_param(nm), dp.get_param(nm)
         assert np.abs(a - b).max() <= 2e-2 * 1e-3 + 1e-6 * np.abs(b).max(), nm
     fused.close(); dp.close(); buf.close()
+
+
+def test_ttt_matches_oracle_at_bench_model_dims():
+    """Two-pass training-time test at the bench workload's model dimensions
+    (C2: H 4096, V 128256 in four vocabulary chunks, 32 q / 8 kv heads of 128,
+    FFN 14336) on a short batch the CPU oracle finishes in seconds."""
+    c = dict(api.CONFIGS["C2"], seq_len=128, micro_batch=2, ttt_steps=2)
+    shp = oshape(c)
+    tr = api.DraftTrainer(c, lr=HP[0], betas=(HP[1], HP[2]), eps=HP[3], weight_decay=HP[4],
+                          seed=SEED)
+    tr.keep_grads(True)
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 1 << 12)
+    samples = []
+    for i, L in enumerate([c["seq_len"] + 4, 90]):
+        cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+        samples.append((cap["ids"], cap["features"]))
+    F, u, y, m = oracle.gather_batch(shp, samples)
+    layout, total = oracle.param_layout(shp)
+    P = np.zeros(total, np.float32)
+    for nm, rr, cc, off in layout:
+        P[off:off + rr * cc] = tr.get_param(nm).reshape(-1)
+    E = tr.get_embedding()
+    z = np.zeros_like(P)
+    out, grads = oracle.train_step(shp, HP, 1, P, z.copy(), z.copy(), E, F, u, y, m,
+                                   round_bf16=True, update=False)
+    r = tr.step(buf, [0, 1])
+    assert r["valid_tokens"] == out.valid
+    assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
+    errs = {}
+    for nm, rr, cc, off in layout:
+        e = rel(tr.get_grad(nm).reshape(-1), grads[off:off + rr * cc])
+        errs[nm] = round(e, 5)
+        assert e <= 1e-2, (nm, e)
+    print("C2-dims TTT2 grad rel errors:", errs)
+    tr.close()
+    buf.close()
