@@ -28,6 +28,10 @@ import time
 
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# NCCL prints its version banner on stdout at communicator init when
+# NCCL_DEBUG is VERSION; keep stdout to the one JSON line of the contract
+if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 WORKLOAD = "C2"
 SEED = 20260217
