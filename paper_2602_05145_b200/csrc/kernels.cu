@@ -1,5 +1,7 @@
 // HBM-bound kernels of the draft-training step.  See kernels.h.
 #include "common.h"
+#include <cuda_fp16.h>
+
 #include "kernels.h"
 
 namespace specsim {
@@ -493,24 +495,33 @@ __global__ void pack_packed_kernel(const uint4* __restrict__ src, int W8, int n,
   for (int c = threadIdx.x; c < W8; c += blockDim.x) dst[c] = s[c];
 }
 
-__global__ void ce_grad_kernel(const float* __restrict__ logits, long long ldl,
+__global__ void ce_grad_kernel(const __half* __restrict__ logits, long long ldl,
+                               const gemm::CePartial* __restrict__ part,
                                const float* __restrict__ lse, const float* __restrict__ coef,
-                               const int32_t* __restrict__ y, int v0, int vn,
+                               const int32_t* __restrict__ y, int v0, int vn, long long T,
                                __nv_bfloat16* __restrict__ dlog, long long ldd) {
-  // one row per blockIdx.y; 8 columns per thread (two 16-byte loads, one store)
+  // one row per blockIdx.y; 8 columns per thread (one 16-byte load and store);
+  // the stored value is l - m with m the row max of the 128-column half tile
+  // (the forward's partial), so p = 2^((delta + m - lse) log2 e)
   const long long t = blockIdx.y;
   const int j = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (j >= vn) return;
   const float l2e = 1.4426950408889634f;
-  const float lse_t = lse[t], coef_t = coef[t];
+  const float off = part[static_cast<long long>((v0 + j) >> 7) * T + t].max - lse[t];
+  const float coef_t = coef[t];
   const int tgt = y[t] - v0;
-  const float* src = logits + t * ldl + v0 + j;
-  const float4 a = __ldcs(reinterpret_cast<const float4*>(src));
-  const float4 b = __ldcs(reinterpret_cast<const float4*>(src + 4));
-  float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(logits + t * ldl + v0 + j));
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    x[2 * i] = f.x;
+    x[2 * i + 1] = f.y;
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float p = exp2f((x[i] - lse_t) * l2e);
+    const float p = exp2f((x[i] + off) * l2e);
     x[i] = (p - (j + i == tgt ? 1.f : 0.f)) * coef_t;
   }
   *reinterpret_cast<uint4*>(dlog + t * ldd + j) = pack8(x);
@@ -607,13 +618,13 @@ void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat1
   swiglu_bwd_kernel<<<blocks_for(T * (I / 8), 256), 256, 0, s>>>(gu, dact, dgu, T, I);
 }
 
-void ce_grad(const float* logits, long long ldl, const float* lse, const float* coef,
-             const int32_t* y, int v0, long long T, int vn, __nv_bfloat16* dlog, long long ldd,
-             cudaStream_t s) {
+void ce_grad(const __half* logits, long long ldl, const gemm::CePartial* partials,
+             const float* lse, const float* coef, const int32_t* y, int v0, long long T, int vn,
+             __nv_bfloat16* dlog, long long ldd, cudaStream_t s) {
   if (T == 0) return;
   count_launches();
   ce_grad_kernel<<<dim3(blocks_for(vn / 8, 256), static_cast<unsigned>(T)), 256, 0, s>>>(
-      logits, ldl, lse, coef, y, v0, vn, dlog, ldd);
+      logits, ldl, partials, lse, coef, y, v0, vn, T, dlog, ldd);
 }
 
 void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -77,12 +78,14 @@ void swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat1
 // Combine per-N-tile softmax partials into lse / per-row loss / argmax.
 void ce_reduce(const gemm::CePartial* partials, int num_nb, long long T, const int32_t* y,
                const int32_t* m, float* lse, float* row_loss, int32_t* argmax, cudaStream_t s);
-// CE gradient from stored fp32 logits (same arithmetic as the EPI_CE_BWD
-// recompute epilogue): dlog[t, j] = bf16((exp(l[t, v0 + j] - lse[t]) -
-// [v0 + j == y[t]]) * coef[t]) for j < vn.  vn % 8 == 0.
-void ce_grad(const float* logits, long long ldl, const float* lse, const float* coef,
-             const int32_t* y, int v0, long long T, int vn, __nv_bfloat16* dlog, long long ldd,
-             cudaStream_t s);
+// CE gradient from the logits the forward GEMM stored as fp16 offsets from
+// their 128-column half tile's row max (partials[(v / 128) * T + t].max):
+// dlog[t, j] = bf16((exp(delta + max - lse[t]) - [v0 + j == y[t]]) * coef[t])
+// for j < vn (same arithmetic as the EPI_CE_BWD recompute epilogue up to the
+// fp16 rounding of the offset).  vn % 8 == 0, v0 % 128 == 0.
+void ce_grad(const __half* logits, long long ldl, const gemm::CePartial* partials,
+             const float* lse, const float* coef, const int32_t* y, int v0, long long T, int vn,
+             __nv_bfloat16* dlog, long long ldd, cudaStream_t s);
 // stats[0] = sum_j w[j] * (sum of step j's row_loss / n_global) (double),
 // stats[1] = valid (as double), stats[2] = top-1 correct, both of step 0.
 // Single block, fixed order.

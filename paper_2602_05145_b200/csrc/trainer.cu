@@ -227,7 +227,7 @@ class DraftTrainerImpl {
   long long* n_global;
   double* stats;
   // backward
-  float* logits = nullptr;  // [T, V] fp32 when keep_logits
+  __half* logits = nullptr;  // [KT, V] fp16 offsets from the half-tile row max (keep_logits)
   bool keep_logits = false;
   __nv_bfloat16 *dlog, *dh_b, *dact, *dgu, *dr_b, *dO, *dqkv, *dg_b;
   float *dn, *dh, *dz, *dr, *dU, *Dattn, *dw_part;
@@ -383,12 +383,13 @@ class DraftTrainerImpl {
     arena.reserve(&n_global, 2);
     arena.reserve(&stats, 4);
     arena.reserve(&dlog, KT * Vc);
-    // fp32 logits [T, V] kept from the forward so the backward needs no logit
-    // recompute (4.2 GB at C2); SPECSIM_CE_RECOMPUTE=1 or a > 32 GB table
+    // logits [KT, V] kept from the forward so the backward needs no logit
+    // recompute, as fp16 offsets from the row max of each 128-column half tile
+    // (2.1 GB at C2); SPECSIM_CE_RECOMPUTE=1 or a > 32 GB table
     // selects the recompute path instead
     {
       const char* e = std::getenv("SPECSIM_CE_RECOMPUTE");
-      keep_logits = !(e && e[0] == '1') && KT * V * 4 <= (32ll << 30);
+      keep_logits = !(e && e[0] == '1') && KT * V * 2 <= (32ll << 30);
       if (keep_logits) arena.reserve(&logits, KT * V);
     }
     arena.reserve(&dh_b, KT * H);
@@ -890,8 +891,8 @@ class DraftTrainerImpl {
       const long long v0 = c * Vc, vn = std::min(Vc, V - v0);
       if (keep_logits)
         timed(PH_LM, 0, [&] {
-          kern::ce_grad(logits, V, lse, coef, y, static_cast<int>(v0), KT, static_cast<int>(vn),
-                        dlog, Vc, stream);
+          kern::ce_grad(logits, V, partials, lse, coef, y, static_cast<int>(v0), KT,
+                        static_cast<int>(vn), dlog, Vc, stream);
         });
       else
         run(p_ce_bwd[c], PH_LM, 0.0);  // logit recompute: not algorithmic work

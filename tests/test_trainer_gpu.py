@@ -278,10 +278,12 @@ def test_partial_batch_matches_oracle():
 
 @pytest.mark.parametrize("name", ["bigvocab", "gqa128"])
 def test_stored_logits_equal_recompute(name, monkeypatch):
-    """The default backward reads the fp32 logits the forward GEMM stored; the
-    SPECSIM_CE_RECOMPUTE path recomputes them chunk by chunk (EPI_CE_BWD).
-    Both apply the same softmax-gradient arithmetic to the same accumulator
-    values, so the step's loss and every gradient agree to fp32 noise."""
+    """The default backward reads the logits the forward GEMM stored (fp16
+    offsets from each 128-column half tile's row max); the SPECSIM_CE_RECOMPUTE
+    path recomputes them chunk by chunk (EPI_CE_BWD) in fp32.  The loss comes
+    from the forward's statistics in both (fp32 noise); the gradients differ
+    only where the fp16 offset flips a bf16 rounding of the softmax gradient
+    (|offset error| <= 2^-11 |l - max|), measured <= 1.3e-3 rel."""
     c = SHAPES[name]
     S, B = c["seq_len"], c["micro_batch"]
     lens = [S + 2] * (B - 1) + [S // 2 + 5]
@@ -296,7 +298,8 @@ def test_stored_logits_equal_recompute(name, monkeypatch):
     (l0, g0), (l1, g1) = out["0"], out["1"]
     assert abs(l0 - l1) <= 1e-6 * abs(l1)
     for nm in g0:
-        assert rel(g0[nm], g1[nm]) <= 1e-5, (nm, rel(g0[nm], g1[nm]))
+        assert rel(g0[nm], g1[nm]) <= 3e-3, (nm, rel(g0[nm], g1[nm]))
+    print(name, {nm: rel(g0[nm], g1[nm]) for nm in g0})
 
 
 def test_step_matches_oracle_at_bench_model_dims():
