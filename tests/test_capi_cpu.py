@@ -105,3 +105,22 @@ def test_flop_convention_matches_survey():
     assert abs(f["total"] / 1e9 - 4.8633) < 1e-3
     assert abs(api.gemm_flops_per_token(api.CONFIGS["C1"])["total"] / 1e9 - 0.01398) < 1e-4
     assert abs(api.gemm_flops_per_token(api.CONFIGS["C5"])["total"] / 1e9 - 12.9479) < 1e-3
+
+
+def test_shape_validation_precedes_device_checks():
+    """Invalid draft shapes (incl. the training-time-test fields) are domain
+    errors reported with every problem at once, before any device access;
+    a valid shape on a GPU-less host fails with SPECSIM_ECUDA (no fallback)."""
+    bad = dict(api.CONFIGS["C1"], ttt_steps=17, seq_len=192, head_dim=96)
+    with pytest.raises(_lib.DomainError) as e:
+        api.DraftTrainer(bad)
+    msg = str(e.value)
+    assert "ttt_steps" in msg and "head_dim" in msg and "seq_len" in msg
+    with pytest.raises(_lib.DomainError, match="ttt_decay"):
+        api.DraftTrainer(dict(api.CONFIGS["C1"], ttt_steps=2, ttt_decay=1.5))
+    import torch
+    if torch.cuda.is_available():
+        return
+    with pytest.raises(_lib.SpecsimError) as e:
+        api.DraftTrainer(dict(api.CONFIGS["C1"], ttt_steps=3))
+    assert e.value.status == _lib.ECUDA
