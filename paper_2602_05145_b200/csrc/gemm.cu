@@ -204,7 +204,8 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   if (epi == EPI_ADAMW) {
     if (!p.args.opt_p || !p.args.opt_m || !p.args.opt_v || !p.args.opt_p16 || !p.args.opt_hp)
       throw std::invalid_argument("gemm: AdamW epilogue needs p/m/v/p16/hp");
-    if ((p.args.ldc * 4) % 16 != 0) throw std::invalid_argument("gemm: ldc not 16B aligned");
+    if (p.args.ldc % 8 != 0 || N % 8 != 0)
+      throw std::invalid_argument("gemm: AdamW epilogue needs ldc and N multiples of 8");
   }
   if (epi == EPI_BF16_ROPE) {
     if (!p.args.rope_cos || !p.args.rope_sin || p.args.rope_S <= 0 ||

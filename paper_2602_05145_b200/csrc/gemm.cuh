@@ -26,6 +26,12 @@
 #include "gemm.h"
 #include "ptx.cuh"
 
+#ifndef SPECSIM_ADAMW_VARIANT
+// 0: production fused-AdamW epilogue (256-bit accesses); 1..4: the 128-bit
+// epilogue's probe variants, 5: the 128-bit epilogue (scripts/adamw_probe.sh)
+#define SPECSIM_ADAMW_VARIANT 0
+#endif
+
 namespace specsim {
 namespace gemm {
 
@@ -419,6 +425,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   make_uint2(ptx::pack_bf16x2(w.x, w.y), ptx::pack_bf16x2(w.z, w.w));
           }
         }
+      } else if constexpr (EPI == EPI_ADAMW && SPECSIM_ADAMW_VARIANT == 0) {
+        // Fused AdamW on the gradient tile.  The 32x32 chunk is staged through
+        // smem and walked 4 lanes x 8 columns per row (8 rows per warp
+        // instruction) so every optimizer-state access is one 256-bit
+        // LDG / STG (p, m, v, optional g) and the bf16 copy one 128-bit STG:
+        // half the LSU instructions of 128-bit accesses.  Two row groups are
+        // loaded before any store (their DRAM latencies overlap).
+        const AdamDev hp = *args.opt_hp;
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += 32) {
+          uint32_t r[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(t_row + c, r);
+          ptx::tmem_ld_wait();
+          const int col0 = n0 + c;
+          if (col0 >= args.N) continue;  // warp-uniform
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(stg + lane * 36 + i) =
+                make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                            __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          __syncwarp();
+          const int cl = (lane & 3) * 8;  // this lane's 8 columns
+          const int col = col0 + cl;
+          const bool col_ok = col < args.N;  // N % 8 == 0 (make_plan)
+#pragma unroll
+          for (int g0 = 0; g0 < 4; g0 += 2) {
+            float gv[2][8], pv[2][8], mv[2][8], vv[2][8];
+            bool ok[2];
+            long long e[2];
+#pragma unroll
+            for (int it = 0; it < 2; ++it) {
+              const int rl = (g0 + it) * 8 + (lane >> 2);
+              const int rw = row_base + rl;
+              ok[it] = col_ok && rw < args.M;
+              e[it] = static_cast<long long>(rw) * args.ldc + col;
+              const float4 a = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
+              const float4 b = *reinterpret_cast<const float4*>(stg + rl * 36 + cl + 4);
+              gv[it][0] = a.x; gv[it][1] = a.y; gv[it][2] = a.z; gv[it][3] = a.w;
+              gv[it][4] = b.x; gv[it][5] = b.y; gv[it][6] = b.z; gv[it][7] = b.w;
+              if (ok[it]) {
+                ptx::ld_cs_v8(args.opt_p + e[it], pv[it]);
+                ptx::ld_cs_v8(args.opt_m + e[it], mv[it]);
+                ptx::ld_cs_v8(args.opt_v + e[it], vv[it]);
+              }
+            }
+#pragma unroll
+            for (int it = 0; it < 2; ++it) {
+              if (!ok[it]) continue;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float g = gv[it][j];
+                const float pi = pv[it][j] * hp.decay;
+                mv[it][j] = mv[it][j] + (g - mv[it][j]) * (1.f - hp.beta1);
+                vv[it][j] = vv[it][j] * hp.beta2 + (1.f - hp.beta2) * g * g;
+                const float denom = sqrtf(vv[it][j]) / hp.bc2_sqrt + hp.eps;
+                pv[it][j] = pi - hp.step_size * (mv[it][j] / denom);
+              }
+              ptx::st_cs_v8(args.opt_p + e[it], pv[it]);
+              ptx::st_cs_v8(args.opt_m + e[it], mv[it]);
+              ptx::st_cs_v8(args.opt_v + e[it], vv[it]);
+              __stcs(reinterpret_cast<uint4*>(args.opt_p16 + e[it]),
+                     make_uint4(ptx::pack_bf16x2(pv[it][0], pv[it][1]),
+                                ptx::pack_bf16x2(pv[it][2], pv[it][3]),
+                                ptx::pack_bf16x2(pv[it][4], pv[it][5]),
+                                ptx::pack_bf16x2(pv[it][6], pv[it][7])));
+              if (args.opt_g) ptx::st_cs_v8(args.opt_g + e[it], gv[it]);
+            }
+          }
+        }
       } else {
         // per-row constants, owned by lane (row - row_base); shuffled below
         float lse_r = 0.f, coef_r = 0.f;
@@ -454,9 +530,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // 8 row groups' DRAM latencies overlap
           // AdamW keeps three state vectors per row group in flight: hoist 4
           // row groups at a time so everything stays in registers
-#ifndef SPECSIM_ADAMW_VARIANT
-#define SPECSIM_ADAMW_VARIANT 0  // probe builds only (scripts/adamw_probe.sh)
-#endif
           constexpr int RG = EPI == EPI_ADAMW ? (SPECSIM_ADAMW_VARIANT == 4 ? 8 : 4) : 8;
 #pragma unroll
           for (int g0 = 0; g0 < 8; g0 += RG) {

@@ -294,6 +294,20 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 256-bit global accesses (sm_100: LDG/STG .256), streaming (evict-first)
+// hint; volatile so they keep program order with the neighbouring stores
+__device__ __forceinline__ void ld_cs_v8(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_cs_v8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // ---- softmax arithmetic (sm_100 packed fp32x2 pipes, 3-input max, MUFU ex2)
 // 2^x, flush-to-zero, no range fix-up (softmax weights; subnormals are 0 in
 // bf16 anyway): one MUFU.EX2
