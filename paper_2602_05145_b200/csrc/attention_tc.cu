@@ -19,6 +19,10 @@
 #include "gemm.h"
 #include "ptx.cuh"
 
+#ifndef SPECSIM_ATTN_PROBE
+#define SPECSIM_ATTN_PROBE 0
+#endif
+
 namespace specsim {
 namespace attn {
 namespace {
@@ -456,6 +460,11 @@ __device__ __forceinline__ void store_grad_row(uint32_t tm, __nv_bfloat16* dst, 
 constexpr int BQB = 64;               // query block of the dK/dV kernel
 constexpr int TILE64 = BQB * 64 * 2;  // [64 x 64] bf16 SW128 tile = 8 KB
 
+// Q / dO / (lse, D) stream in a 3-deep ring: the stage of iteration it is
+// refilled only after the dV / dK MMAs of it complete, and the S^T MMA of
+// it + 2 is issued right after those -- with two stages that TMA latency
+// sat on the critical path of every iteration.
+constexpr int KV_QSTAGES = 3;
 template <int HD>
 struct KvSmem {
   static constexpr int ATOMS = HD / 64;
@@ -463,12 +472,12 @@ struct KvSmem {
   static constexpr int QT = ATOMS * TILE64;     // [64 q x HD]
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV;
-  static constexpr int OFF_Q = OFF_V + KV;      // 2 stages
-  static constexpr int OFF_DO = OFF_Q + 2 * QT;  // 2 stages
-  static constexpr int OFF_P = OFF_DO + 2 * QT;  // 2 x [128 keys x 64 q]
+  static constexpr int OFF_Q = OFF_V + KV;                    // KV_QSTAGES stages
+  static constexpr int OFF_DO = OFF_Q + KV_QSTAGES * QT;      // KV_QSTAGES stages
+  static constexpr int OFF_P = OFF_DO + KV_QSTAGES * QT;      // 2 x [128 keys x 64 q]
   static constexpr int OFF_DS = OFF_P + 2 * TILE;
-  static constexpr int OFF_LD = OFF_DS + 2 * TILE;  // 2 stages x (lse[64], D[64]) fp32
-  static constexpr int OFF_BAR = OFF_LD + 2 * 2 * BQB * 4;
+  static constexpr int OFF_LD = OFF_DS + 2 * TILE;  // stages x (lse[64], D[64]) fp32
+  static constexpr int OFF_BAR = OFF_LD + KV_QSTAGES * 2 * BQB * 4;
   static constexpr int BYTES = 1024 + OFF_BAR + 256;
 };
 
@@ -490,15 +499,16 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  constexpr int QS = KV_QSTAGES;
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;   // [2]
-  uint64_t* qd_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_free = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* p_free = bar + 11;   // [2]
-  uint64_t* all_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* qd_full = bar + 1;        // [QS]
+  uint64_t* qd_empty = bar + 1 + QS;  // [QS]
+  uint64_t* s_full = bar + 1 + 2 * QS;   // [2]
+  uint64_t* s_free = bar + 3 + 2 * QS;   // [2]
+  uint64_t* p_full = bar + 5 + 2 * QS;   // [2]
+  uint64_t* p_free = bar + 7 + 2 * QS;   // [2]
+  uint64_t* all_done = bar + 9 + 2 * QS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * QS);
   float* sLD = reinterpret_cast<float*>(smem + L::OFF_LD);
 
   const int kb = blockIdx.x;  // key block; early keys see the most queries
@@ -517,9 +527,11 @@ __global__ void __launch_bounds__(192, 1)
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_do);
     ptx::mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QS; ++i) {
       ptx::mbar_init(&qd_full[i], 1);
       ptx::mbar_init(&qd_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_free[i], 4);
       ptx::mbar_init(&p_full[i], 4);
@@ -549,13 +561,14 @@ __global__ void __launch_bounds__(192, 1)
                          d.Q + d.KV + g * HD + 64 * a, row0 + kb * BKV);
       }
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
+        const int st = it % QS;
+        const uint32_t ph = (it / QS) & 1;
         const int step = it / per_step, rem = it % per_step;
         const int h = g * rep + rem / per_head;
         const int q0 = (qb0 + rem % per_head) * BQB;
         const int qrow = static_cast<int>(step * T) + row0 + q0;
         const long long li = (static_cast<long long>(step) * d.nh + h) * T + row0 + q0;
-        ptx::mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&qd_empty[st], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * L::QT + 2 * BQB * 4);
         for (int a = 0; a < A; ++a) {
           ptx::tma_load_2d(&tm_q, &qd_full[st], smem + L::OFF_Q + st * L::QT + a * TILE64,
@@ -574,37 +587,37 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idG = ptx::make_idesc_bf16(BKV, HD, false, true);
       const uint32_t aK = ptx::smem_u32(smem + L::OFF_K), aV = ptx::smem_u32(smem + L::OFF_V);
       auto issue_s = [&](int it) {
-        const int st = it & 1;
-        ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);
-        ptx::mbar_wait(&s_free[st], ((it >> 1) & 1) ^ 1);
+        const int qs = it % QS, sb = it & 1;  // Q / dO stage, TMEM S^T / dP^T buffer
+        ptx::mbar_wait(&qd_full[qs], (it / QS) & 1);
+        ptx::mbar_wait(&s_free[sb], ((it >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + st * L::QT);
-        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + st * L::QT);
+        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + qs * L::QT);
+        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + qs * L::QT);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          ptx::umma_bf16(tSt[st], kdesc(aK, kk), kdesc64(aQ, kk), idS, kk > 0 ? 1u : 0u);
-          ptx::umma_bf16(tdPt[st], kdesc(aV, kk), kdesc64(adO, kk), idS, kk > 0 ? 1u : 0u);
+          ptx::umma_bf16(tSt[sb], kdesc(aK, kk), kdesc64(aQ, kk), idS, kk > 0 ? 1u : 0u);
+          ptx::umma_bf16(tdPt[sb], kdesc(aV, kk), kdesc64(adO, kk), idS, kk > 0 ? 1u : 0u);
         }
-        ptx::umma_commit(&s_full[st]);
+        ptx::umma_commit(&s_full[sb]);
       };
       ptx::mbar_wait(kv_full, 0);
       issue_s(0);
       for (int it = 0; it < n_it; ++it) {
         if (it + 1 < n_it) issue_s(it + 1);
-        const int st = it & 1;
+        const int st = it & 1, qs = it % QS;  // P / dS buffer, Q / dO stage
         ptx::mbar_wait(&p_full[st], (it >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aP = ptx::smem_u32(smem + L::OFF_P + st * TILE);
         const uint32_t aS = ptx::smem_u32(smem + L::OFF_DS + st * TILE);
-        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + st * L::QT);
-        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + st * L::QT);
+        const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q + qs * L::QT);
+        const uint32_t adO = ptx::smem_u32(smem + L::OFF_DO + qs * L::QT);
 #pragma unroll
         for (int kk = 0; kk < BQB / 16; ++kk) {
           ptx::umma_bf16(tdV, kdesc(aP, kk), mndesc64(adO, kk), idG, (it > 0 || kk > 0) ? 1u : 0u);
           ptx::umma_bf16(tdK, kdesc(aS, kk), mndesc64(aQ, kk), idG, (it > 0 || kk > 0) ? 1u : 0u);
         }
         ptx::umma_commit(&p_free[st]);
-        ptx::umma_commit(&qd_empty[st]);
+        ptx::umma_commit(&qd_empty[qs]);
       }
       ptx::umma_commit(all_done);
     }
@@ -621,20 +634,28 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_wait(&s_full[st], (it >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t sv[2][32], pv[2][32];
+#if SPECSIM_ATTN_PROBE == 2  // probe: no TMEM reads (timing experiments only)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c][i] = pv[c][i] = __float_as_uint(0.01f * i);
+#else
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         ptx::tmem_ld_32x32b_x32(tSt[st] + lane_off + c * 32, sv[c]);
         ptx::tmem_ld_32x32b_x32(tdPt[st] + lane_off + c * 32, pv[c]);
       }
       ptx::tmem_ld_wait();
+#endif
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&s_free[st]);
       // lse / D slices arrived with this stage's TMA bytes: observe that
       // barrier directly (cannot have advanced: the stage is only refilled
       // after the dV/dK MMAs that need this iteration's P / dS)
-      ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);
-      const float* l2 = sLD + st * 2 * BQB;
+      const int qs = it % QS;
+      ptx::mbar_wait(&qd_full[qs], (it / QS) & 1);
+      const float* l2 = sLD + qs * 2 * BQB;
       const float* Dq = l2 + BQB;
       // the P / dS smem buffer of this stage is free once the MMAs of it-2 ran
       ptx::mbar_wait(&p_free[st], ((it >> 1) & 1) ^ 1);
@@ -660,7 +681,11 @@ __global__ void __launch_bounds__(192, 1)
                 sl2x2, ptx::fmul2(ptx::f32x2(lq.x, lq.y), nlog2e));
             float x0, x1;
             ptx::f32x2_split(x, x0, x1);
+#if SPECSIM_ATTN_PROBE == 1  // probe: no MUFU (timing experiments only)
+            float p0 = x0, p1 = x1;
+#else
             float p0 = ptx::ex2_ftz(x0), p1 = ptx::ex2_ftz(x1);
+#endif
             if (masked) {  // causal: query before key
               if (q0 + qi < key) p0 = 0.f;
               if (q0 + qi + 1 < key) p1 = 0.f;
