@@ -109,6 +109,7 @@ void dispatch_epi(const GemmPlan& p, cudaStream_t s, bool a = false) {
     case EPI_CE_BWD: launch_t<A_MN, B_MN, EPI_CE_BWD, CG>(p, s, a); break;
     case EPI_ADAMW: launch_t<A_MN, B_MN, EPI_ADAMW, CG>(p, s, a); break;
     case EPI_BF16_ROPE: launch_t<A_MN, B_MN, EPI_BF16_ROPE, CG>(p, s, a); break;
+    case EPI_SWIGLU_BWD: launch_t<A_MN, B_MN, EPI_SWIGLU_BWD, CG>(p, s, a); break;
     default: throw std::invalid_argument("gemm: bad epilogue");
   }
 }
@@ -216,8 +217,10 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
     if (p.args.rope_ld < p.args.rope_S + p.args.rope_pos_off)
       throw std::invalid_argument("gemm: RoPE table shorter than rope_S + rope_pos_off");
   }
+  if (epi == EPI_SWIGLU_BWD && (!p.args.R || p.args.ldr != p.args.ldc || p.args.ldc < 2ll * N))
+    throw std::invalid_argument("gemm: SwiGLU-backward epilogue needs R = gu and ldc = ldr >= 2N");
   if (epi == EPI_BF16 || epi == EPI_BF16_RESID || epi == EPI_CE_BWD || epi == EPI_F32 ||
-      epi == EPI_F32_ACC || epi == EPI_BF16_ROPE) {
+      epi == EPI_F32_ACC || epi == EPI_BF16_ROPE || epi == EPI_SWIGLU_BWD) {
     if (!p.args.C) throw std::invalid_argument("gemm: missing output");
     if ((p.args.ldc * (epi == EPI_F32 || epi == EPI_F32_ACC ? 4 : 2)) % 16 != 0)
       throw std::invalid_argument("gemm: ldc not 16B aligned");

@@ -554,6 +554,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 x1[it].x = __uint_as_float(q.x);
                 x1[it].y = __uint_as_float(q.y);
               }
+            } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+              if (okm >> it & 1) {  // gate | up of these 4 columns
+                const __nv_bfloat16* gp = args.R + static_cast<long long>(rr) * args.ldr + col;
+                const uint2 qg = *reinterpret_cast<const uint2*>(gp);
+                const uint2 qu = *reinterpret_cast<const uint2*>(gp + args.N);
+                x1[it] = make_float4(__uint_as_float(qg.x), __uint_as_float(qg.y),
+                                     __uint_as_float(qu.x), __uint_as_float(qu.y));
+              }
             } else if constexpr (EPI == EPI_F32_ACC) {
               if (okm >> it & 1)
                 x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e_it);
@@ -586,7 +594,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const long long e_it = SPECSIM_E(it);
             float4 w = v[it];
             float* wa = &w.x;
-            if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
+            if constexpr (EPI == EPI_SWIGLU_BWD) {
+              // d act rounded to bf16 (the operand the unfused path stores),
+              // then silu' with the stored bf16 gate / up, as swiglu_bwd_kernel
+              uint32_t qb[4] = {__float_as_uint(x1[it].x), __float_as_uint(x1[it].y),
+                                __float_as_uint(x1[it].z), __float_as_uint(x1[it].w)};
+              float gv[4], uv[4], dg[4], du[4];
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const float2 gg =
+                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qb[j]));
+                const float2 uu =
+                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qb[2 + j]));
+                gv[2 * j] = gg.x;
+                gv[2 * j + 1] = gg.y;
+                uv[2 * j] = uu.x;
+                uv[2 * j + 1] = uu.y;
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float dv = __bfloat162float(__float2bfloat16_rn(wa[j]));
+                const float sg = 1.f / (1.f + __expf(-gv[j]));
+                dg[j] = dv * uv[j] * sg * (1.f + gv[j] * (1.f - sg));
+                du[j] = dv * gv[j] * sg;
+              }
+              __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(args.C) + e_it;
+              *reinterpret_cast<uint2*>(cp) =
+                  make_uint2(ptx::pack_bf16x2(dg[0], dg[1]), ptx::pack_bf16x2(dg[2], dg[3]));
+              *reinterpret_cast<uint2*>(cp + args.N) =
+                  make_uint2(ptx::pack_bf16x2(du[0], du[1]), ptx::pack_bf16x2(du[2], du[3]));
+            } else if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
               if constexpr (EPI == EPI_BF16_RESID) {
                 uint32_t q0 = __float_as_uint(x1[it].x), q1 = __float_as_uint(x1[it].y);
                 const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q0));

@@ -24,6 +24,8 @@ enum Epi : int {
   EPI_CE_BWD = 5,      // C(bf16) = (exp(acc - lse[row]) - [col == y[row]]) * coef[row]
   EPI_ADAMW = 6,       // acc is a weight gradient: fused PyTorch-AdamW update of p/m/v (+ bf16 p)
   EPI_BF16_ROPE = 7,   // C(bf16) = acc with NeoX RoPE applied to columns < rope_cols (q | k heads)
+  EPI_SWIGLU_BWD = 8,  // acc = d act (N = I columns): with gate | up = R[:, c] | R[:, I + c],
+                       // C[:, c] = d gate, C[:, I + c] = d up (bf16; ldc = ldr = 2I)
 };
 
 // Device-resident AdamW hyper-parameters of the current step (updated per step

@@ -253,6 +253,7 @@ class DraftTrainerImpl {
   int in_slot = 0;
   gemm::AdamDev* adam_dev = nullptr;  // = &d_in->hp
   bool keep_grads = false;            // materialise fp32 grads in the fused-AdamW path
+  bool swiglu_fused = true;           // SwiGLU backward in the d act GEMM epilogue
 
   // GEMM plans (vectors: one per unroll pass; LM head and weight gradients
   // span all K*T rows)
@@ -429,6 +430,10 @@ class DraftTrainerImpl {
 
     init_params(seed);
     init_rope();
+    {
+      const char* e = std::getenv("SPECSIM_SWIGLU_UNFUSED");
+      swiglu_fused = !(e && e[0] == '1');
+    }
     build_plans();
     attn::prepare(sh.head_dim);
     SPECSIM_CUDA(cudaEventCreate(&ev_begin));
@@ -628,8 +633,15 @@ class DraftTrainerImpl {
     // data gradients, per pass
     for (int j = 0; j < K; ++j) {
       const long long R = j * T;
-      p_dact.push_back(make_plan({dh_b + R * H, H, false}, {pb("down"), I, true}, T, I, H,
-                                 EPI_BF16, out_args(dact, I)));
+      // d act = dh W_down; the SwiGLU backward runs in its epilogue (reads the
+      // stored gate | up, writes d gate | d up) unless SPECSIM_SWIGLU_UNFUSED=1
+      if (swiglu_fused)
+        p_dact.push_back(make_plan({dh_b + R * H, H, false}, {pb("down"), I, true}, T, I, H,
+                                   EPI_SWIGLU_BWD,
+                                   out_args(dgu + R * 2 * I, 2 * I, gu + R * 2 * I, 2 * I)));
+      else
+        p_dact.push_back(make_plan({dh_b + R * H, H, false}, {pb("down"), I, true}, T, I, H,
+                                   EPI_BF16, out_args(dact, I)));
       p_dz.push_back(make_plan({dgu + R * 2 * I, 2 * I, false}, {pb("gate_up"), H, true}, T, H,
                                2 * I, EPI_F32, out_args(dz + R * H, H)));
       p_dO.push_back(make_plan({dr_b + R * H, H, false}, {pb("o"), Q, true}, T, Q, H, EPI_BF16,
@@ -924,9 +936,10 @@ class DraftTrainerImpl {
         run_dw(p_dw_down, f_dw_down);
         bucket_ready(n_chunks);  // down, w_fin
       }
-      timed(PH_ELEM, 0, [&] {
-        kern::swiglu_bwd(gu + R * 2 * I, dact, dgu + R * 2 * I, T, sh.ffn, stream);
-      });
+      if (!swiglu_fused)
+        timed(PH_ELEM, 0, [&] {
+          kern::swiglu_bwd(gu + R * 2 * I, dact, dgu + R * 2 * I, T, sh.ffn, stream);
+        });
       run(p_dz[j]);
       if (j == 0) {
         run_dw(p_dw_gu, f_dw_gu);

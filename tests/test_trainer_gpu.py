@@ -346,3 +346,23 @@ def test_step_matches_oracle_at_bench_model_dims():
     print("C2-dims grad rel errors:", errs)
     tr.close()
     buf.close()
+
+
+def test_swiglu_backward_epilogue_equals_unfused(monkeypatch):
+    """The SwiGLU backward fused into the d act GEMM epilogue (reads gate | up,
+    writes d gate | d up) equals the separate kernel over the stored bf16 d act:
+    same rounding point, same formula (FMA contraction may differ: 1e-5)."""
+    c = SHAPES["C1"]
+    lens = [c["seq_len"] + 2] * c["micro_batch"]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SPECSIM_SWIGLU_UNFUSED", mode)
+        c, shp, tr, buf, ids, _ = setup("C1", lens)
+        r = tr.step(buf, ids)
+        out[mode] = (r["loss"], {nm: tr.get_grad(nm).copy() for nm in ("gate_up", "qkv", "fc")})
+        tr.close()
+        buf.close()
+    (l0, g0), (l1, g1) = out["0"], out["1"]
+    assert l0 == l1
+    for nm in g0:
+        assert rel(g0[nm], g1[nm]) <= 1e-5, (nm, rel(g0[nm], g1[nm]))
