@@ -14,6 +14,10 @@
 // TMEM: S0 | S1 | O  (128 + 128 + HD fp32 columns).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 #include "attention.h"
 #include "common.h"
 #include "gemm.h"
@@ -42,7 +46,7 @@ struct FwdSmem {
   static constexpr int OFF_K = OFF_Q + Q;          // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV;     // 2 stages
   static constexpr int OFF_P = OFF_V + 2 * KV;     // 2 buffers
-  static constexpr int OFF_BAR = OFF_P + 2 * P;
+  static constexpr int OFF_BAR = OFF_P + 2 * P;  // 20 mbarriers + the TMEM slot
   static constexpr int BYTES = 1024 + OFF_BAR + 256;
 };
 
@@ -74,6 +78,13 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t base, int kk) {
   return ptx::make_sw128_desc(base + kk * 2048, TILE, 1024);
 }
 
+// Persistent: grid = min(#items, #SMs); CTA c processes work items c, c + grid,
+// ... where item i = (query block, head, sample) in decreasing-work order
+// (most keys first).  Block counters (K / V stages, S and P buffers, their
+// mbarrier phases) run across items; the O accumulator is double-buffered in
+// TMEM (S0 | S1 | O0 | O1) so item i's epilogue overlaps item i+1's first
+// MMAs, and the single Q tile is reloaded as soon as item i's last S MMA ran.
+// A grid of #items reproduces one-item-per-CTA launches (SPECSIM_ATTN_FWD_GRID=items).
 template <int HD>
 __global__ void __launch_bounds__(192, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
@@ -95,18 +106,28 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* s_free = bar + 11;   // [2]
   uint64_t* p_full = bar + 13;   // [2]
   uint64_t* pv_done = bar + 15;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+  uint64_t* q_empty = bar + 17;
+  uint64_t* o_free = bar + 18;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
-  const int qb = gridDim.x - 1 - blockIdx.x;  // most keys first
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int g = h / (d.nh / d.nkv);
+  const int nqb = d.S / BQ;
+  const int n_items = nqb * d.nh * d.B;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = b * d.S;
-  const int nkv = qb + 1;
+  const int nd = d.n_diag;
+  // item -> (query block, head, sample); most keys first
+  auto decode = [&](int idx, int& qb, int& h, int& b) {
+    qb = nqb - 1 - idx / (d.nh * d.B);
+    const int hb = idx % (d.nh * d.B);
+    h = hb % d.nh;
+    b = hb / d.nh;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tm);
     ptx::mbar_init(q_full, 1);
+    // Q is free after the item's last S MMA; with training-time-test cache
+    // entries the softmax epilogue also reads it (4 more arrivals)
+    ptx::mbar_init(q_empty, nd > 0 ? 5 : 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
@@ -116,6 +137,7 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_init(&s_free[i], 4);
       ptx::mbar_init(&p_full[i], 4);
       ptx::mbar_init(&pv_done[i], 1);
+      ptx::mbar_init(&o_free[i], 4);
     }
     ptx::fence_barrier_init();
   }
@@ -125,29 +147,36 @@ __global__ void __launch_bounds__(192, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
+  const uint32_t tO[2] = {tmem + 256, tmem + 384};
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA
       constexpr int A = L::ATOMS;
-      ptx::mbar_arrive_expect_tx(q_full, L::Q);
-      for (int a = 0; a < A; ++a)
-        ptx::tma_load_2d(&tm, q_full, sQ + a * TILE, h * HD + 64 * a,
-                         static_cast<int>(d.q_row_off) + row0 + qb * BQ);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        ptx::mbar_wait(&k_empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&k_full[s], L::KV);
+      int n = 0;  // block counter across items
+      for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+        int qb, h, b;
+        decode(idx, qb, h, b);
+        const int g = h / (d.nh / d.nkv), row0 = b * d.S;
+        ptx::mbar_wait(q_empty, (li & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(q_full, L::Q);
         for (int a = 0; a < A; ++a)
-          ptx::tma_load_2d(&tm, &k_full[s], sK + s * L::KV + a * TILE, d.Q + g * HD + 64 * a,
-                           row0 + j * BKV);
-        ptx::mbar_wait(&v_empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&v_full[s], L::KV);
-        for (int a = 0; a < A; ++a)
-          ptx::tma_load_2d(&tm, &v_full[s], sV + s * L::KV + a * TILE,
-                           d.Q + d.KV + g * HD + 64 * a, row0 + j * BKV);
+          ptx::tma_load_2d(&tm, q_full, sQ + a * TILE, h * HD + 64 * a,
+                           static_cast<int>(d.q_row_off) + row0 + qb * BQ);
+        for (int j = 0; j <= qb; ++j, ++n) {
+          const int s = n & 1;
+          const uint32_t ph = (n >> 1) & 1;
+          ptx::mbar_wait(&k_empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&k_full[s], L::KV);
+          for (int a = 0; a < A; ++a)
+            ptx::tma_load_2d(&tm, &k_full[s], sK + s * L::KV + a * TILE, d.Q + g * HD + 64 * a,
+                             row0 + j * BKV);
+          ptx::mbar_wait(&v_empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[s], L::KV);
+          for (int a = 0; a < A; ++a)
+            ptx::tma_load_2d(&tm, &v_full[s], sV + s * L::KV + a * TILE,
+                             d.Q + d.KV + g * HD + 64 * a, row0 + j * BKV);
+        }
       }
     }
   } else if (warp == 1) {
@@ -156,10 +185,13 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idS = ptx::make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idO = ptx::make_idesc_bf16(BQ, HD, false, true);
       const uint32_t aQ = ptx::smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int s = j & 1;
-        ptx::mbar_wait(&k_full[s], (j >> 1) & 1);
-        ptx::mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
+      // S_n = Q K_n^T for block n (item li, its block j of nkv); the item's
+      // last S releases Q
+      auto issue_s = [&](int n, int li, int j, int nkv) {
+        const int s = n & 1;
+        if (j == 0) ptx::mbar_wait(q_full, li & 1);
+        ptx::mbar_wait(&k_full[s], (n >> 1) & 1);
+        ptx::mbar_wait(&s_free[s], ((n >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t aK = ptx::smem_u32(sK + s * L::KV);
 #pragma unroll
@@ -167,206 +199,239 @@ __global__ void __launch_bounds__(192, 1)
           ptx::umma_bf16(tS[s], kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
         ptx::umma_commit(&s_full[s]);
         ptx::umma_commit(&k_empty[s]);
+        if (j == nkv - 1) ptx::umma_commit(q_empty);
       };
-      ptx::mbar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(j + 1);
-        const int s = j & 1;  // K / V stage, S buffer and P buffer of block j
-        ptx::mbar_wait(&p_full[s], (j >> 1) & 1);
-        ptx::mbar_wait(&v_full[s], (j >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t aV = ptx::smem_u32(sV + s * L::KV);
-        const uint32_t aP = ptx::smem_u32(sP + s * L::P);
+      int n = 0;
+      for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+        int qb, h, b;
+        decode(idx, qb, h, b);
+        const int nkv = qb + 1, ob = li & 1;
+        const int nidx = idx + gridDim.x;
+        if (li == 0) issue_s(0, 0, 0, nkv);
+        for (int j = 0; j < nkv; ++j, ++n) {
+          if (j + 1 < nkv) issue_s(n + 1, li, j + 1, nkv);
+          const int s = n & 1;  // K / V stage, S buffer and P buffer of block n
+          // O[ob] was last read by the epilogue of item li - 2
+          if (j == 0) ptx::mbar_wait(&o_free[ob], ((li >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&p_full[s], (n >> 1) & 1);
+          ptx::mbar_wait(&v_full[s], (n >> 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t aV = ptx::smem_u32(sV + s * L::KV);
+          const uint32_t aP = ptx::smem_u32(sP + s * L::P);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          ptx::umma_bf16(tO, kdesc(aP, kk), mndesc(aV, kk), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::umma_commit(&pv_done[s]);
-        ptx::umma_commit(&v_empty[s]);
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            ptx::umma_bf16(tO[ob], kdesc(aP, kk), mndesc(aV, kk), idO,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+          ptx::umma_commit(&pv_done[s]);
+          ptx::umma_commit(&v_empty[s]);
+          // the next item's first S goes after this item's last PV (its Q
+          // load is then hidden behind this PV and the epilogue)
+          if (j == nkv - 1 && nidx < n_items) {
+            int qb2, h2, b2;
+            decode(nidx, qb2, h2, b2);
+            issue_s(n + 1, li + 1, 0, qb2 + 1);
+          }
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // query row within the block (= TMEM lane)
-    const int q = qb * BQ + r;       // position within the sample
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const float sl2 = d.scale * kLog2e;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int s = j & 1;
-      ptx::mbar_wait(&s_full[s], (j >> 1) & 1);
-      ptx::tc_fence_after();
-      // Row max over this block's 128 raw scores.  One softmax warp per SM
-      // sub-partition, so the softmax is issue-bound: 3-input max with 4
-      // independent partials, the scale folded into the exponent's FFMA2
-      // (max(s * c) = c * max(s), c > 0), MUFU ex2 without range fix-up, and
-      // packed fp32x2 row sums -- ~3 instructions per score instead of ~10.
-      uint32_t v[4][32];
+    const long long T = static_cast<long long>(d.B) * d.S;
+    int n = 0;
+    for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+      int qb, h, b;
+      decode(idx, qb, h, b);
+      const int g = h / (d.nh / d.nkv), row0 = b * d.S;
+      const int q = qb * BQ + r;  // position within the sample
+      const int nkv = qb + 1, ob = li & 1;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nkv; ++j, ++n) {
+        const int s = n & 1;
+        ptx::mbar_wait(&s_full[s], (n >> 1) & 1);
+        ptx::tc_fence_after();
+        // Row max over this block's 128 raw scores.  One softmax warp per SM
+        // sub-partition, so the softmax is issue-bound: 3-input max with 4
+        // independent partials, the scale folded into the exponent's FFMA2
+        // (max(s * c) = c * max(s), c > 0), MUFU ex2 without range fix-up, and
+        // packed fp32x2 row sums -- ~3 instructions per score instead of ~10.
+        uint32_t v[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS[s] + lane_off + c * 32, v[c]);
-      ptx::tmem_ld_wait();
-      if (j == qb) {  // diagonal block: keys after the query are masked
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS[s] + lane_off + c * 32, v[c]);
+        ptx::tmem_ld_wait();
+        if (j == qb) {  // diagonal block: keys after the query are masked
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i > r) v[c][i] = __float_as_uint(-INFINITY);
+        }
+        float mxp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i > r) v[c][i] = __float_as_uint(-INFINITY);
-      }
-      float mxp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          mxp[0] = ptx::max3f(mxp[0], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
-          mxp[1] = ptx::max3f(mxp[1], __uint_as_float(v[c][i + 2]), __uint_as_float(v[c][i + 3]));
-          mxp[2] = ptx::max3f(mxp[2], __uint_as_float(v[c][i + 4]), __uint_as_float(v[c][i + 5]));
-          mxp[3] = ptx::max3f(mxp[3], __uint_as_float(v[c][i + 6]), __uint_as_float(v[c][i + 7]));
-        }
-      const float mx = ptx::max3f(mxp[0], mxp[1], fmaxf(mxp[2], mxp[3])) * sl2;
-      // S buffer consumed: the MMA may overwrite it with S_{j+2}
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&s_free[s]);
-      // lazy rescale: a row moves its reference max only when the max grows by
-      // more than 2^8; the O read-modify-write is warp-collective (tcgen05.ld /
-      // st are .sync.aligned), so the whole warp does it when any lane needs it
-      // -- and only then waits for every PV so far (PV_{j-1}) to have landed
-      const bool need = mx > m_run + 8.f;
-      float corr = 1.f;
-      if (need) {
-        corr = exp2f(m_run - mx);  // 0 on the first block
-        l_run *= corr;
-        m_run = mx;
-      }
-      const bool rescale = j > 0 && __any_sync(0xffffffffu, need);
-      if (rescale) {
-        ptx::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t o[32];
-          ptx::tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-          tmem_st_32x32b_x32(tO + lane_off + c * 32, o);
-        }
-        tmem_st_wait();
-      }
-      // P buffer s was last read by PV_{j-2}
-      if (j >= 2) ptx::mbar_wait(&pv_done[s], ((j - 2) >> 1) & 1);
-      uint8_t* sPb = sP + s * L::P;
-      // P = 2^(s * scale * log2e - m) -> bf16, K-major SW128: row r, 16-byte
-      // chunk cc of tile t at t*TILE + r*128 + ((cc ^ (r & 7)) * 16); row
-      // sum in 4 packed fp32x2 partials
-      const uint64_t scale2 = ptx::f32x2(sl2, sl2), negm2 = ptx::f32x2(-m_run, -m_run);
-      uint64_t lp2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const uint64_t x2 = ptx::ffma2(
-                ptx::f32x2(__uint_as_float(v[c][i + e]), __uint_as_float(v[c][i + e + 1])), scale2,
-                negm2);
-            float x0, x1;
-            ptx::f32x2_split(x2, x0, x1);
-            p[e] = ptx::ex2_ftz(x0);
-            p[e + 1] = ptx::ex2_ftz(x1);
-            lp2[e >> 1] = ptx::fadd2(lp2[e >> 1], ptx::f32x2(p[e], p[e + 1]));
+          for (int i = 0; i < 32; i += 8) {
+            mxp[0] = ptx::max3f(mxp[0], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
+            mxp[1] =
+                ptx::max3f(mxp[1], __uint_as_float(v[c][i + 2]), __uint_as_float(v[c][i + 3]));
+            mxp[2] =
+                ptx::max3f(mxp[2], __uint_as_float(v[c][i + 4]), __uint_as_float(v[c][i + 5]));
+            mxp[3] =
+                ptx::max3f(mxp[3], __uint_as_float(v[c][i + 6]), __uint_as_float(v[c][i + 7]));
           }
-          const int key = c * 32 + i;  // 8 keys = one 16-byte chunk
-          const int t = key >> 6, cc = (key & 63) >> 3;
-          uint4 pk;
-          pk.x = ptx::pack_bf16x2(p[0], p[1]);
-          pk.y = ptx::pack_bf16x2(p[2], p[3]);
-          pk.z = ptx::pack_bf16x2(p[4], p[5]);
-          pk.w = ptx::pack_bf16x2(p[6], p[7]);
-          *reinterpret_cast<uint4*>(sPb + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) = pk;
+        const float mx = ptx::max3f(mxp[0], mxp[1], fmaxf(mxp[2], mxp[3])) * sl2;
+        // S buffer consumed: the MMA may overwrite it with S_{n+2}
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[s]);
+        // lazy rescale: a row moves its reference max only when the max grows
+        // by more than 2^8; the O read-modify-write is warp-collective
+        // (tcgen05.ld / st are .sync.aligned), so the whole warp does it when
+        // any lane needs it -- and only then waits for the previous PV
+        const bool need = mx > m_run + 8.f;
+        float corr = 1.f;
+        if (need) {
+          corr = exp2f(m_run - mx);  // 0 on the first block
+          l_run *= corr;
+          m_run = mx;
         }
+        const bool rescale = j > 0 && __any_sync(0xffffffffu, need);
+        if (rescale) {
+          ptx::mbar_wait(&pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(tO[ob] + lane_off + c * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st_32x32b_x32(tO[ob] + lane_off + c * 32, o);
+          }
+          tmem_st_wait();
+        }
+        // P buffer s was last read by PV_{n-2}
+        if (n >= 2) ptx::mbar_wait(&pv_done[s], ((n - 2) >> 1) & 1);
+        uint8_t* sPb = sP + s * L::P;
+        // P = 2^(s * scale * log2e - m) -> bf16, K-major SW128: row r, 16-byte
+        // chunk cc of tile t at t*TILE + r*128 + ((cc ^ (r & 7)) * 16); row
+        // sum in 4 packed fp32x2 partials
+        const uint64_t scale2 = ptx::f32x2(sl2, sl2), negm2 = ptx::f32x2(-m_run, -m_run);
+        uint64_t lp2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float p[8];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const uint64_t x2 = ptx::ffma2(
+                  ptx::f32x2(__uint_as_float(v[c][i + e]), __uint_as_float(v[c][i + e + 1])),
+                  scale2, negm2);
+              float x0, x1;
+              ptx::f32x2_split(x2, x0, x1);
+              p[e] = ptx::ex2_ftz(x0);
+              p[e + 1] = ptx::ex2_ftz(x1);
+              lp2[e >> 1] = ptx::fadd2(lp2[e >> 1], ptx::f32x2(p[e], p[e + 1]));
+            }
+            const int key = c * 32 + i;  // 8 keys = one 16-byte chunk
+            const int t = key >> 6, cc = (key & 63) >> 3;
+            uint4 pk;
+            pk.x = ptx::pack_bf16x2(p[0], p[1]);
+            pk.y = ptx::pack_bf16x2(p[2], p[3]);
+            pk.z = ptx::pack_bf16x2(p[4], p[5]);
+            pk.w = ptx::pack_bf16x2(p[6], p[7]);
+            *reinterpret_cast<uint4*>(sPb + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) = pk;
+          }
+        }
+        {
+          float a0, a1;
+          ptx::f32x2_split(ptx::fadd2(ptx::fadd2(lp2[0], lp2[1]), ptx::fadd2(lp2[2], lp2[3])),
+                           a0, a1);
+          l_run += a0 + a1;
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy P writes -> tensor-core reads
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[s]);
       }
-      {
-        float a0, a1, b0, b1;
-        ptx::f32x2_split(ptx::fadd2(ptx::fadd2(lp2[0], lp2[1]), ptx::fadd2(lp2[2], lp2[3])), a0, a1);
-        (void)b0;
-        (void)b1;
-        l_run += a0 + a1;
+      // ---- epilogue of the item: O[ob] -> bf16 rows, lse
+      ptx::mbar_wait(&pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+      ptx::tc_fence_after();
+      // Training-time-test cache entries (unroll step n_diag >= 1): one extra
+      // score per earlier step i at this row, q . k_i (q from the swizzled
+      // smem tile, k_i from HBM), merged into the running max / sum; their
+      // values are added to O row-wise in the store loop below.
+      float pd[kMaxDiag];
+      float corr = 1.f;
+      if (nd > 0) {
+        float mnew = m_run;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          const uint4* kr = reinterpret_cast<const uint4*>(
+              d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + g * HD);
+          float dot = 0.f;
+#pragma unroll
+          for (int c8 = 0; c8 < HD / 8; ++c8) {
+            const uint4 qv = *reinterpret_cast<const uint4*>(
+                sQ + (c8 >> 3) * TILE + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
+            const uint4 kv = __ldg(kr + c8);
+            dot += ptx::dot_bf16x8(qv, kv);
+          }
+          pd[i] = dot * sl2;
+          mnew = fmaxf(mnew, pd[i]);
+        }
+        // sQ read: the producer may load the next item's Q
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(q_empty);
+        corr = exp2f(m_run - mnew);
+        l_run *= corr;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          pd[i] = exp2f(pd[i] - mnew);
+          l_run += pd[i];
+        }
+        m_run = mnew;
       }
-      ptx::fence_proxy_async_smem();  // generic-proxy P writes -> tensor-core reads
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* orow = out + static_cast<long long>(row0 + q) * d.Q + h * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        ptx::tmem_ld_32x32b_x32(tO[ob] + lane_off + c * 32, o);
+        ptx::tmem_ld_wait();
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * corr;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          const uint4* vr = reinterpret_cast<const uint4*>(
+              d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + d.KV +
+              g * HD + c * 32);
+#pragma unroll
+          for (int v8 = 0; v8 < 4; ++v8) {
+            float vf[8];
+            ptx::unpack_bf16x8(__ldg(vr + v8), vf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[v8 * 8 + e] += pd[i] * vf[e];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          ptx::st_global_v4(orow + c * 32 + i, ptx::pack_bf16x2(acc[i] * inv, acc[i + 1] * inv),
+                            ptx::pack_bf16x2(acc[i + 2] * inv, acc[i + 3] * inv),
+                            ptx::pack_bf16x2(acc[i + 4] * inv, acc[i + 5] * inv),
+                            ptx::pack_bf16x2(acc[i + 6] * inv, acc[i + 7] * inv));
+      }
+      // O[ob] read: the MMA may start item li + 2's accumulation in it
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&p_full[s]);
+      if (lane == 0) ptx::mbar_arrive(&o_free[ob]);
+      lse[h * T + row0 + q] = (m_run + log2f(l_run)) * kLn2;
     }
-    ptx::mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
-    ptx::tc_fence_after();
-    const long long T = static_cast<long long>(d.B) * d.S;
-    // Training-time-test cache entries (unroll step n_diag >= 1): one extra
-    // score per earlier step i at this row, q . k_i (q from the swizzled smem
-    // tile, k_i from HBM), merged into the running max / sum; their values
-    // are added to O row-wise in the store loop below.
-    const int nd = d.n_diag;
-    float pd[kMaxDiag];
-    float corr = 1.f;
-    if (nd > 0) {
-      float mnew = m_run;
-#pragma unroll 1
-      for (int i = 0; i < nd; ++i) {
-        const uint4* kr = reinterpret_cast<const uint4*>(
-            d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + g * HD);
-        float dot = 0.f;
-#pragma unroll
-        for (int c8 = 0; c8 < HD / 8; ++c8) {
-          const uint4 qv = *reinterpret_cast<const uint4*>(
-              sQ + (c8 >> 3) * TILE + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
-          const uint4 kv = __ldg(kr + c8);
-          dot += ptx::dot_bf16x8(qv, kv);
-        }
-        pd[i] = dot * sl2;
-        mnew = fmaxf(mnew, pd[i]);
-      }
-      corr = exp2f(m_run - mnew);
-      l_run *= corr;
-#pragma unroll 1
-      for (int i = 0; i < nd; ++i) {
-        pd[i] = exp2f(pd[i] - mnew);
-        l_run += pd[i];
-      }
-      m_run = mnew;
-    }
-    const float inv = 1.f / l_run;
-    __nv_bfloat16* orow = out + static_cast<long long>(row0 + q) * d.Q + h * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      ptx::tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
-      ptx::tmem_ld_wait();
-      float acc[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * corr;
-#pragma unroll 1
-      for (int i = 0; i < nd; ++i) {
-        const uint4* vr = reinterpret_cast<const uint4*>(
-            d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + d.KV +
-            g * HD + c * 32);
-#pragma unroll
-        for (int v8 = 0; v8 < 4; ++v8) {
-          float vf[8];
-          ptx::unpack_bf16x8(__ldg(vr + v8), vf);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[v8 * 8 + e] += pd[i] * vf[e];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 32; i += 8)
-        ptx::st_global_v4(orow + c * 32 + i, ptx::pack_bf16x2(acc[i] * inv, acc[i + 1] * inv),
-                          ptx::pack_bf16x2(acc[i + 2] * inv, acc[i + 3] * inv),
-                          ptx::pack_bf16x2(acc[i + 4] * inv, acc[i + 5] * inv),
-                          ptx::pack_bf16x2(acc[i + 6] * inv, acc[i + 7] * inv));
-    }
-    lse[h * T + row0 + q] = (m_run + log2f(l_run)) * kLn2;
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -945,7 +1010,16 @@ void forward_tc_t(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     init = true;
   }
-  dim3 grid(d.S / BQ, d.nh, d.B);
+  // persistent: one CTA per SM (SPECSIM_ATTN_FWD_GRID=items: one per work item)
+  static const bool per_item = [] {
+    const char* e = std::getenv("SPECSIM_ATTN_FWD_GRID");
+    return e && std::string(e) == "items";
+  }();
+  const int n_items = (d.S / BQ) * d.nh * d.B;
+  int dev = 0, sms = 0;
+  SPECSIM_CUDA(cudaGetDevice(&dev));
+  SPECSIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = per_item ? n_items : std::min(n_items, sms);
   count_launches();
   attn_fwd_tc_kernel<HD><<<grid, 192, smem, s>>>(tm, o, lse, d);
 }
