@@ -1,8 +1,10 @@
-// Causal GQA attention forward on the 5th-generation tensor cores.
+// Causal GQA attention (forward, and the dK/dV and dQ backward kernels
+// below) on the 5th-generation tensor cores.
 //
-// One CTA = one (sample, query head, 128-query block).  Warp roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j (128-key blocks) into a
-//               2-deep ring (SWIZZLE_128B tiles, one tensor map over qkv)
+// Forward: persistent, one CTA per SM looping over work items (sample, query
+// head, 128-query block), most keys first.  Warp roles:
+//   warp 0      TMA producer: the item's Q, then K_j / V_j (128-key blocks)
+//               into a 2-deep ring (SWIZZLE_128B tiles, one tensor map over qkv)
 //   warp 1      MMA issuer (one lane): S_j = Q K_j^T into one of two TMEM
 //               S buffers, then O += P_j V_j with P_j from shared memory
 //   warps 2..5  softmax: one query row per thread (TMEM lane), so row max /
@@ -11,7 +13,7 @@
 //               overlaps the PV MMA of block j; lazy rescaling (only when the
 //               row max grows by more than 2^8) keeps O read-modify-writes --
 //               the one step that must wait for PV_j -- rare
-// TMEM: S0 | S1 | O  (128 + 128 + HD fp32 columns).
+// TMEM: S0 | S1 | O0 | O1 (128 columns each; O double-buffered across items).
 #include <cuda_bf16.h>
 
 #include <algorithm>
