@@ -583,8 +583,7 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
   const unsigned g = static_cast<unsigned>(nb);
 #define SPECSIM_RMS_BWD(C)                                                                     \
   rmsnorm_bwd_kernel<C><<<g, kNormThreads, 0, s>>>(dy, lddy, x, ldx, gather, w, rstd, resid, \
-                                                   out_f32, out_bf16, ldo,                   \
-                                                   dw ? dw_partial : nullptr, T, H)
+                                                   out_f32, out_bf16, ldo, dw_partial, T, H)
   if (H <= 1024)
     SPECSIM_RMS_BWD(1);
   else if (H <= 2048)
@@ -595,8 +594,12 @@ void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long l
     SPECSIM_RMS_BWD(8);
 #undef SPECSIM_RMS_BWD
   if (!dw) return;
+  colsum(dw_partial, nb, H, dw, s);
+}
+
+void colsum(const float* parts, long long rows, int H, float* out, cudaStream_t s) {
   count_launches();
-  colsum_kernel<<<blocks_for(H, 32), 256, 0, s>>>(dw_partial, nb, H, dw);
+  colsum_kernel<<<blocks_for(H, 32), 256, 0, s>>>(parts, rows, H, out);
 }
 
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,

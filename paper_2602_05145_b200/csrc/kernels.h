@@ -58,12 +58,16 @@ void rmsnorm_fwd(const __nv_bfloat16* x, long long ldx, const int32_t* gather, c
 // dx = rstd*(dy*w) - x*rstd^3*mean(dy*w*x);  out_f32 = resid + dx (resid nullable),
 // out_bf16 = bf16(out_f32) (nullable); dx skipped entirely when both outputs null.
 // dw[i] = sum_t dy*x*rstd (deterministic two-pass; dw_partial scratch
-// [ceil(T/rows_per_block), H]); dw nullable.  x may be gathered (embedding rows).
+// [ceil(T/rows_per_block), H]).  dw null: the per-block partials are only
+// written (when dw_partial is non-null) for a later colsum over several calls.
+// x may be gathered (embedding rows).
 void rmsnorm_bwd(const float* dy, long long lddy, const __nv_bfloat16* x, long long ldx,
                  const int32_t* gather, const float* w, const float* rstd, const float* resid,
                  float* out_f32, __nv_bfloat16* out_bf16, long long ldo, float* dw,
                  float* dw_partial, long long T, int H, cudaStream_t s);
 long long rmsnorm_bwd_partial_rows(long long T);
+// out[i] = sum over rows of parts[row, i] (fixed order: deterministic)
+void colsum(const float* parts, long long rows, int H, float* out, cudaStream_t s);
 
 // NeoX RoPE on the q and k heads of a [T, NQ] row-major buffer, in place.
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,

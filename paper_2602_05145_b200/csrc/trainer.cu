@@ -234,6 +234,10 @@ class DraftTrainerImpl {
   // K > 1: fp32 gradient w.r.t. the pass input (flows into the previous pass's
   // output), the cache part of dq, and the k | v accumulators of passes >= 1
   float *dg_in = nullptr, *dq_add = nullptr, *dkv_acc = nullptr;
+  // K > 1: per-pass dw partials of the final / post / hidden norms ([K][nbT, H]
+  // each), summed once at pass 0 -- no extra pass over the K*T rows
+  float *dwp_fin = nullptr, *dwp_post = nullptr, *dwp_hid = nullptr;
+  long long nbT = 0;
   // pinned host scalars
   long long* h_nglobal = nullptr;
   double* h_stats = nullptr;
@@ -407,7 +411,11 @@ class DraftTrainerImpl {
     arena.reserve(&dU, KT * 2 * H);
     arena.reserve(&Dattn, KT * sh.n_heads);
     arena.reserve(&dw_part, kern::rmsnorm_bwd_partial_rows(KT) * H);
+    nbT = kern::rmsnorm_bwd_partial_rows(T);
     if (K > 1) {
+      arena.reserve(&dwp_fin, K * nbT * H);
+      arena.reserve(&dwp_post, K * nbT * H);
+      arena.reserve(&dwp_hid, K * nbT * H);
       arena.reserve(&dg_in, T * H);
       arena.reserve(&dq_add, T * Q);
       arena.reserve(&dkv_acc, KT * 2 * KV);
@@ -926,10 +934,9 @@ class DraftTrainerImpl {
       timed(PH_ELEM, 0, [&] {
         kern::rmsnorm_bwd(dn + R * H, H, h + R * H, H, nullptr, pf("w_fin"), rstd_fin + R,
                           j < K - 1 ? dg_in : nullptr, dh, dh_b + R * H, H,
-                          one ? gf("w_fin") : nullptr, dw_part, T, sh.hidden, stream);
-        if (j == 0 && !one)
-          kern::rmsnorm_bwd(dn, H, h, H, nullptr, pf("w_fin"), rstd_fin, nullptr, nullptr,
-                            nullptr, H, gf("w_fin"), dw_part, KT, sh.hidden, stream);
+                          one ? gf("w_fin") : nullptr, one ? dw_part : dwp_fin + j * nbT * H, T,
+                          sh.hidden, stream);
+        if (j == 0 && !one) kern::colsum(dwp_fin, K * nbT, sh.hidden, gf("w_fin"), stream);
       });
       run(p_dact[j]);
       if (j == 0) {
@@ -947,15 +954,14 @@ class DraftTrainerImpl {
       }
       timed(PH_ELEM, 0, [&] {
         kern::rmsnorm_bwd(dz + R * H, H, r + R * H, H, nullptr, pf("w_post"), rstd_post + R, dh,
-                          dr, dr_b + R * H, H, one ? gf("w_post") : nullptr, dw_part, T,
-                          sh.hidden, stream);
+                          dr, dr_b + R * H, H, one ? gf("w_post") : nullptr,
+                          one ? dw_part : dwp_post + j * nbT * H, T, sh.hidden, stream);
       });
       run(p_dO[j]);
       if (j == 0) {
         if (!one)
           timed(PH_ELEM, 0, [&] {
-            kern::rmsnorm_bwd(dz, H, r, H, nullptr, pf("w_post"), rstd_post, nullptr, nullptr,
-                              nullptr, H, gf("w_post"), dw_part, KT, sh.hidden, stream);
+            kern::colsum(dwp_post, K * nbT, sh.hidden, gf("w_post"), stream);
           });
         run_dw(p_dw_o, f_dw_o);
         bucket_ready(n_chunks + 2);  // o, w_post
@@ -990,12 +996,13 @@ class DraftTrainerImpl {
         // a later pass's fp32 dg flows into the previous pass's output
         kern::rmsnorm_bwd(dUj + H, 2 * H, g + R * H, H, nullptr, pf("w_hid"), rstd_b + R, dr,
                           j > 0 ? dg_in : nullptr, j > 0 ? nullptr : dg_b, H,
-                          one ? gf("w_hid") : nullptr, dw_part, T, sh.hidden, stream);
+                          one ? gf("w_hid") : nullptr, one ? dw_part : dwp_hid + j * nbT * H, T,
+                          sh.hidden, stream);
         if (j == 0 && !one) {
+          // w_in has no dx (frozen embedding): one dw pass over every pass's rows
           kern::rmsnorm_bwd(dU, 2 * H, E, H, u, pf("w_in"), rstd_a, nullptr, nullptr, nullptr, H,
                             gf("w_in"), dw_part, KT, sh.hidden, stream);
-          kern::rmsnorm_bwd(dU + H, 2 * H, g, H, nullptr, pf("w_hid"), rstd_b, nullptr, nullptr,
-                            nullptr, H, gf("w_hid"), dw_part, KT, sh.hidden, stream);
+          kern::colsum(dwp_hid, K * nbT, sh.hidden, gf("w_hid"), stream);
         }
       });
     }
