@@ -66,3 +66,41 @@ def test_gemm_many_tiles_persistent(cg):
     assert np.abs(out - ref).max() <= 1e-3 * 16
     out, ref, _ = run_gemm(1, 1, 1, 4096, 512, 2048, seed=6, cg=cg)
     assert np.abs(out - ref).max() <= 1e-3 * 46
+
+
+def _shapes(seed, n):
+    rng = np.random.default_rng(seed)
+    return [tuple(int(8 * rng.integers(lo, hi)) for lo, hi in ((8, 90), (8, 120), (2, 80)))
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", _shapes(11, 4))
+def test_gemm_random_shapes(a_mn, b_mn, M, N, K):
+    """Seeded random M / N / K (multiples of 8: TMA row pitch) for every
+    operand-major form: partial M / N tiles and short or ragged K."""
+    out, ref, _ = run_gemm(a_mn, b_mn, 1, M, N, K, seed=M + N + K)
+    assert np.abs(out - ref).max() <= 1e-3 * np.sqrt(K), (M, N, K)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (200, 328, 136), (1024, 1536, 512)])
+def test_gemm_fused_adamw_epilogue(M, N, K):
+    """Weight-gradient GEMM with the AdamW update in the epilogue (256-bit
+    optimizer-state accesses, partial tiles): first step from m = v = 0 with
+    lr 1e-3, betas (0.9, 0.95), no decay -> p - lr / (1 - 0.9) * m / (sqrt(v) / sqrt(1 - 0.95) + eps)."""
+    rng = np.random.default_rng(M)
+    A_bits, A = rand_bf16(rng, (M, K))
+    B_bits, B = rand_bf16(rng, (N, K))
+    A_st = np.ascontiguousarray(A_bits.T)  # MN-major, as the dW GEMMs
+    B_st = np.ascontiguousarray(B_bits.T)
+    p0 = (0.02 * rng.standard_normal((M, N))).astype(np.float32)
+    Cbuf = p0.copy()
+    ms = C.c_float(0)
+    _lib.call("specsim_debug_gemm", 1, 1, 6 | (2 << 8), M, N, K, _lib.ptr(A_st), M,
+              _lib.ptr(B_st), N, _lib.ptr(Cbuf), N, None, 0, 0, C.byref(ms))
+    g = (A.astype(np.float64) @ B.astype(np.float64).T).astype(np.float32)
+    m = 0.1 * g
+    v = 0.05 * g * g
+    ref = p0 - (1e-3 / 0.1) * m / (np.sqrt(v) / np.sqrt(0.05) + 1e-8)
+    well = np.abs(g) > 1e-3 * np.abs(g).max()
+    assert np.abs(Cbuf - ref)[well].max() <= 2e-5, np.abs(Cbuf - ref)[well].max()
