@@ -56,6 +56,9 @@ CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long 
   return m;
 }
 
+// SMs the persistent GEMM grid may occupy.  SPECSIM_GEMM_SMS=n caps it (A/B
+// knob for data-parallel runs: leaves SMs free for the NCCL kernels that
+// overlap the backward).
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -63,6 +66,10 @@ int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    if (const char* e = std::getenv("SPECSIM_GEMM_SMS")) {
+      const int cap = std::atoi(e);
+      if (cap >= 2 && cap < n) n = cap & ~1;  // whole CTA pairs
+    }
   }
   return n;
 }

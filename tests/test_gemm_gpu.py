@@ -104,3 +104,23 @@ def test_gemm_fused_adamw_epilogue(M, N, K):
     ref = p0 - (1e-3 / 0.1) * m / (np.sqrt(v) / np.sqrt(0.05) + 1e-8)
     well = np.abs(g) > 1e-3 * np.abs(g).max()
     assert np.abs(Cbuf - ref)[well].max() <= 2e-5, np.abs(Cbuf - ref)[well].max()
+
+
+def test_gemm_reduced_grid_is_exact():
+    """SPECSIM_GEMM_SMS caps the persistent grid (SMs left to concurrent NCCL
+    kernels in data-parallel runs); the tile loop must give identical results."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+            "import numpy as np; from test_gemm_gpu import run_gemm;"
+            "o, r, _ = run_gemm(1, 1, 1, 2048, 1536, 512, seed=9);"
+            "np.save('/tmp/specsim_gemm_grid.npy', o)")
+    import os
+    import pathlib
+    root = pathlib.Path(__file__).resolve().parents[1]
+    outs = []
+    for sms in ("0", "40"):
+        env = dict(os.environ, SPECSIM_GEMM_SMS=sms)
+        subprocess.run([sys.executable, "-c", code], cwd=root, env=env, check=True)
+        outs.append(np.load("/tmp/specsim_gemm_grid.npy"))
+    assert np.array_equal(outs[0], outs[1])
