@@ -54,6 +54,10 @@ class Rng {
 double expected_accept_length(double alpha, int gamma);
 int sample_accept_length(Rng& rng, double alpha, int gamma);
 double alpha_from_accept_length(double ell, int gamma);
+// workload.cpp:41-47: alpha(n) = ceiling - (ceiling - start) exp(-n / tau),
+// clamped to [0, 1] (the reference's analytic stand-in for alpha_eval).
+double current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
+                     double trained_samples);
 // oldest floor(9n/10) samples train, the rest evaluate.
 void split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
 

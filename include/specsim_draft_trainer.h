@@ -75,6 +75,12 @@ int specsim_expected_accept_length(double alpha, int32_t gamma, double* out);
 int specsim_sample_accept_length(specsim_rng* rng, double alpha, int32_t gamma, int32_t* out);
 /* perf_model.cpp:213-224 (bisection to kBisectionTol = 1e-6) */
 int specsim_alpha_from_accept_length(double ell, int32_t gamma, double* out);
+/* workload.cpp:41-47: the reference's analytic draft-quality law (the value its
+ * train() returns as alpha_eval; the real trainer measures top-1 instead):
+ * ceiling - (ceiling - start) exp(-max(n, 0) / tau), clamped to [0, 1].
+ * Phase checks as workload.cpp:25-36 (SPECSIM_ECONFIG). */
+int specsim_current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
+                          double trained_samples, double* out);
 /* SPEC.md:348 chronological 9:1 split: the oldest floor(9n/10) samples train. */
 int specsim_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
 

@@ -109,6 +109,7 @@ SIGNATURES = {
     "specsim_sample_accept_length": [P, F64, I32, PI32],
     "specsim_alpha_from_accept_length": [F64, I32, PF64],
     "specsim_split_train_eval": [I64, PI64, PI64],
+    "specsim_current_alpha": [F64, F64, F64, F64, PF64],
     "specsim_dp_shard": [I64, I32, I32, I32, I64, P, PI32],
     "specsim_dp_buckets": [C.POINTER(DraftShape), I32, P, P, I32, PI32, PI32],
     "specsim_bytes_per_token": [C.POINTER(SignalGeometry), PI64],

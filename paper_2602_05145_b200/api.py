@@ -109,6 +109,14 @@ def split_train_eval(n: int):
     return a.value, b.value
 
 
+def current_alpha(alpha_start, alpha_ceiling, tau_samples, trained_samples):
+    """workload.cpp:41-47 (the reference's analytic alpha law)."""
+    o = C.c_double()
+    call("specsim_current_alpha", alpha_start, alpha_ceiling, tau_samples, trained_samples,
+         C.byref(o))
+    return o.value
+
+
 def dp_shard(n_items: int, per_rank: int, world: int, rank: int, step: int):
     idx = np.zeros(max(1, per_rank), np.int64)
     n = C.c_int32()

@@ -61,6 +61,24 @@ int sample_accept_length(Rng& rng, double alpha, int gamma) {
   return k;
 }
 
+// workload.cpp:41-47 (+ the PhaseSpec checks of workload.cpp:25-36, as a
+// ConfigError): the analytic draft-quality law the reference's train() uses
+// for alpha_eval; kept so simulator-mode callers have it next to the real
+// trainer that replaces it.
+double current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
+                     double trained_samples) {
+  Problems p("invalid phase");
+  p.check(alpha_start >= 0.0 && alpha_start <= 1.0, "alpha_start outside [0,1]");
+  p.check(alpha_ceiling >= 0.0 && alpha_ceiling <= 1.0, "alpha_ceiling outside [0,1]");
+  p.check(alpha_start <= alpha_ceiling, "alpha_start > alpha_ceiling");
+  p.check(tau_samples > 0.0, "tau_samples <= 0");
+  p.throw_if_any<ConfigError>();
+  const double n = std::max(0.0, trained_samples);
+  const double alpha =
+      alpha_ceiling - (alpha_ceiling - alpha_start) * std::exp(-n / tau_samples);
+  return std::clamp(alpha, 0.0, 1.0);
+}
+
 double alpha_from_accept_length(double ell, int gamma) {
   if (gamma < 1) throw std::invalid_argument("gamma must be >= 1");
   if (!(ell >= 1.0 && ell <= gamma + 1.0))
@@ -173,6 +191,13 @@ int specsim_sample_accept_length(specsim_rng* r, double alpha, int32_t gamma, in
 }
 int specsim_alpha_from_accept_length(double ell, int32_t gamma, double* out) {
   return guard([&] { *out = alpha_from_accept_length(ell, gamma); });
+}
+int specsim_current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
+                          double trained_samples, double* out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output");
+    *out = current_alpha(alpha_start, alpha_ceiling, tau_samples, trained_samples);
+  });
 }
 int specsim_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval) {
   return guard([&] { split_train_eval(n, n_train, n_eval); });

@@ -124,3 +124,15 @@ def test_shape_validation_precedes_device_checks():
     with pytest.raises(_lib.SpecsimError) as e:
         api.DraftTrainer(dict(api.CONFIGS["C1"], ttt_steps=3))
     assert e.value.status == _lib.ECUDA
+
+
+def test_current_alpha_bit_exact_with_reference():
+    """workload.cpp:41-47 through the C ABI vs the compiled reference's own
+    outputs (golden vectors); phase checks are configuration errors."""
+    for a0, astar, tau, n, hx in GOLD["current_alpha"]:
+        assert api.current_alpha(a0, astar, tau, n).hex() == hx, (a0, astar, tau, n)
+    assert api.current_alpha(0.3, 0.6, 100.0, -5.0) == 0.3  # n clamped at 0
+    with pytest.raises(_lib.ConfigError):
+        api.current_alpha(0.7, 0.6, 100.0, 1.0)
+    with pytest.raises(_lib.ConfigError):
+        api.current_alpha(0.3, 0.6, 0.0, 1.0)
