@@ -111,8 +111,14 @@ std::vector<ParamDesc> param_registry(const DraftShape& sh, long long* total) {
 }
 
 // vocabulary chunk of the LM-head backward: multiple of the GEMM N tile, ~32k
+// (SPECSIM_VOCAB_CHUNK overrides, A/B experiments)
 long long vocab_chunk(long long V) {
-  long long vc = std::min<long long>(V, 32768);
+  static const long long target = [] {
+    const char* e = std::getenv("SPECSIM_VOCAB_CHUNK");
+    const long long v = e ? std::atoll(e) : 32768;
+    return v > 0 ? v : 32768;
+  }();
+  long long vc = std::min<long long>(V, target);
   vc = (vc + gemm::BN - 1) / gemm::BN * gemm::BN;
   return vc > V ? V : vc;
 }
