@@ -667,6 +667,16 @@ void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, co
                                         n, reinterpret_cast<uint4*>(ring_feat), cap, pos);
 }
 
+__global__ void fetch_mapped_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                    int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcv(src + i);
+}
+
+void fetch_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s) {
+  count_launches();
+  fetch_mapped_kernel<<<1, 128, 0, s>>>(src, dst, n_words);
+}
+
 void pack_packed(const __nv_bfloat16* src, int W, int n, __nv_bfloat16* ring_feat, long long cap,
                  long long pos, cudaStream_t s) {
   if (n <= 0) return;

@@ -69,6 +69,11 @@ long long rmsnorm_bwd_partial_rows(long long T);
 // out[i] = sum over rows of parts[row, i] (fixed order: deterministic)
 void colsum(const float* parts, long long rows, int H, float* out, cudaStream_t s);
 
+// dst[0..n_words) = src[...] where src is MAPPED pinned host memory, read by
+// the SMs over PCIe: stages the per-step inputs without a copy-engine H2D,
+// which would queue behind bulk ingest DMA issued earlier on another stream.
+void fetch_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s);
+
 // NeoX RoPE on the q and k heads of a [T, NQ] row-major buffer, in place.
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,
           const float* cos_t, const float* sin_t, bool inverse, cudaStream_t s);

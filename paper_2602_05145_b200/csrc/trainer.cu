@@ -431,7 +431,7 @@ class DraftTrainerImpl {
     arena.commit();
     h = g + T * H;
     adam_dev = &d_in->hp;
-    SPECSIM_CUDA(cudaMallocHost(&h_in, 2 * sizeof(StepInputs)));
+    SPECSIM_CUDA(cudaHostAlloc(&h_in, 2 * sizeof(StepInputs), cudaHostAllocMapped));
     std::memset(h_in, 0, 2 * sizeof(StepInputs));
     for (auto& e : in_ev) SPECSIM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const char* ng = std::getenv("SPECSIM_NO_GRAPH");
@@ -1080,7 +1080,11 @@ class DraftTrainerImpl {
       s.hp = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
                            hp.bc2_sqrt, 0.f};
     }
-    SPECSIM_CUDA(cudaMemcpyAsync(d_in, &s, sizeof(StepInputs), cudaMemcpyHostToDevice, stream));
+    // SM loads from mapped pinned memory, not a copy-engine H2D: the latter
+    // would wait behind whatever ingest DMA the caller queued before this step
+    static_assert(sizeof(StepInputs) % 4 == 0, "StepInputs is copied in words");
+    kern::fetch_mapped(reinterpret_cast<const uint32_t*>(&s), reinterpret_cast<uint32_t*>(d_in),
+                       static_cast<int>(sizeof(StepInputs) / 4), stream);
     SPECSIM_CUDA(cudaEventRecord(in_ev[in_slot], stream));
   }
 

@@ -17,7 +17,7 @@ B, S, H, V = cfg["micro_batch"], cfg["seq_len"], cfg["hidden"], cfg["vocab"]
 L, W, K = S + 2, 3 * H, 10
 tr = api.DraftTrainer(cfg, seed=1)
 pool = 2 * B
-buf = api.HiddenStateBuffer(api.SignalGeometry(H), capacity_tokens=(pool + 3 * K * B) * L)
+buf = api.HiddenStateBuffer(api.SignalGeometry(H), capacity_tokens=(pool + 7 * K * B) * L)
 caps = [api.synth_capture(1, i, L, V, H) for i in range(pool)]
 pinned = []
 for c in caps:
@@ -57,4 +57,18 @@ for rep in range(3):
     res["append_issue_ms"] = round(1e3 * (t1 - t0), 2)
     res["train_after_appends_ms"] = round(1e3 * (t2 - t1), 2)
     res["e2e_ms"] = round(1e3 * (t2 - t0), 2)
+# copy engine alone: the K steps' appends with nothing else running
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    appends(K)
+    torch.cuda.synchronize()
+    res["dma_only_ms"] = round(1e3 * (time.perf_counter() - t0), 2)
+res["h2d_GBps"] = round(K * B * L * (2 * W + 4) / res["dma_only_ms"] / 1e6, 1)
+# resident job while the DMA of a later job streams in (no dependency)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+appends(K)
+tr.train(buf, [k % pool for k in range(K * B)], [], epochs=1)
+res["resident_with_concurrent_dma_ms"] = round(1e3 * (time.perf_counter() - t0), 2)
 print(json.dumps(res))

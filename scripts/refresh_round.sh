@@ -7,9 +7,9 @@ set -u
 mkdir -p gpurun_out
 (nproc; lscpu | grep -E "Model name") > gpurun_out/host.txt
 timeout 900 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
-timeout 900 python bench.py --config C4 --steps 6 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err
-timeout 900 python bench.py --config C5 --steps 6 --no-cpu-baseline > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
-timeout 900 python bench.py --ttt 7 --steps 5 --no-cpu-baseline > gpurun_out/bench_C2_ttt7.json 2> gpurun_out/bench_C2_ttt7.err
+timeout 900 python bench.py --config C4 --steps 20 --warmup 6 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err
+timeout 900 python bench.py --config C5 --steps 20 --warmup 6 --no-cpu-baseline > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
+timeout 900 python bench.py --ttt 7 --steps 12 --warmup 4 --no-cpu-baseline > gpurun_out/bench_C2_ttt7.json 2> gpurun_out/bench_C2_ttt7.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-e2e \
   --no-cpu-baseline > /dev/null 2>&1
