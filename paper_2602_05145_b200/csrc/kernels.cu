@@ -495,36 +495,50 @@ __global__ void pack_packed_kernel(const uint4* __restrict__ src, int W8, int n,
   for (int c = threadIdx.x; c < W8; c += blockDim.x) dst[c] = s[c];
 }
 
-__global__ void ce_grad_kernel(const __half* __restrict__ logits, long long ldl,
-                               const gemm::CePartial* __restrict__ part,
-                               const float* __restrict__ lse, const float* __restrict__ coef,
-                               const int32_t* __restrict__ y, int v0, int vn, long long T,
-                               __nv_bfloat16* __restrict__ dlog, long long ldd) {
-  // one row per blockIdx.y; 8 columns per thread (one 16-byte load and store);
-  // the stored value is l - m with m the row max of the 128-column half tile
-  // (the forward's partial), so p = 2^((delta + m - lse) log2 e)
+constexpr int kCeGradSeg = 4;  // 16-byte segments per thread, all loads issued first
+
+__global__ void __launch_bounds__(256) ce_grad_kernel(
+    const __half* __restrict__ logits, long long ldl, const gemm::CePartial* __restrict__ part,
+    const float* __restrict__ lse, const float* __restrict__ coef,
+    const int32_t* __restrict__ y, int v0, int vn, long long T, __nv_bfloat16* __restrict__ dlog,
+    long long ldd) {
+  // one row per blockIdx.y; each thread owns kCeGradSeg 8-column segments
+  // strided by the block width (coalesced), with every logit load in flight
+  // before the first use; the stored value is l - m with m the row max of the
+  // 128-column half tile (the forward's partial), so p = 2^((delta + m - lse) log2 e)
   const long long t = blockIdx.y;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (j >= vn) return;
+  const int j0 = (blockIdx.x * kCeGradSeg * blockDim.x + threadIdx.x) * 8;
+  const int stride = blockDim.x * 8;
   const float l2e = 1.4426950408889634f;
-  const float off = part[static_cast<long long>((v0 + j) >> 7) * T + t].max - lse[t];
+  uint4 raw[kCeGradSeg];
+#pragma unroll
+  for (int k = 0; k < kCeGradSeg; ++k) {
+    const int j = j0 + k * stride;
+    if (j < vn) raw[k] = __ldcs(reinterpret_cast<const uint4*>(logits + t * ldl + v0 + j));
+  }
+  const float lse_t = lse[t];
   const float coef_t = coef[t];
   const int tgt = y[t] - v0;
-  const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(logits + t * ldl + v0 + j));
-  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-  float x[8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-    x[2 * i] = f.x;
-    x[2 * i + 1] = f.y;
-  }
+  for (int k = 0; k < kCeGradSeg; ++k) {
+    const int j = j0 + k * stride;
+    if (j >= vn) break;
+    const float off = part[static_cast<long long>((v0 + j) >> 7) * T + t].max - lse_t;
+    const uint32_t w[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+    float x[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float p = exp2f((x[i] + off) * l2e);
-    x[i] = (p - (j + i == tgt ? 1.f : 0.f)) * coef_t;
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float p = exp2f((x[i] + off) * l2e);
+      x[i] = (p - (j + i == tgt ? 1.f : 0.f)) * coef_t;
+    }
+    *reinterpret_cast<uint4*>(dlog + t * ldd + j) = pack8(x);
   }
-  *reinterpret_cast<uint4*>(dlog + t * ldd + j) = pack8(x);
 }
 
 }  // namespace
@@ -626,7 +640,8 @@ void ce_grad(const __half* logits, long long ldl, const gemm::CePartial* partial
              __nv_bfloat16* dlog, long long ldd, cudaStream_t s) {
   if (T == 0) return;
   count_launches();
-  ce_grad_kernel<<<dim3(blocks_for(vn / 8, 256), static_cast<unsigned>(T)), 256, 0, s>>>(
+  ce_grad_kernel<<<dim3(blocks_for(vn / 8, 256 * kCeGradSeg), static_cast<unsigned>(T)), 256, 0,
+                   s>>>(
       logits, ldl, partials, lse, coef, y, v0, vn, T, dlog, ldd);
 }
 

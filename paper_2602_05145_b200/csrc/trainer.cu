@@ -249,8 +249,9 @@ class DraftTrainerImpl {
   double* h_stats = nullptr;
   // Per-step inputs (batch spec, caller's global token count, AdamW
   // constants).  The captured step reads them from device memory; the host
-  // fills one of two pinned slots and a stream-ordered copy (outside the
-  // graph) moves it, so train() can enqueue steps back-to-back.
+  // fills one of two mapped pinned slots and a stream-ordered one-warp fetch
+  // kernel (outside the graph) moves it, so train() can enqueue steps
+  // back-to-back.
   struct StepInputs {
     kern::BatchSpec spec;
     long long nglobal;  // > 0: caller-provided global valid-token count
@@ -1066,9 +1067,9 @@ class DraftTrainerImpl {
     return hp;
   }
 
-  // Host: fill the next pinned slot and enqueue its copy to d_in (stream
+  // Host: fill the next pinned slot and enqueue its fetch into d_in (stream
   // ordered before the step's launch, after the previous step).  A slot is
-  // reused only once the copy issued from it two steps ago has executed.
+  // reused only once the fetch issued from it two steps ago has executed.
   void stage(const kern::BatchSpec& spec, int64_t global_valid, bool train) {
     in_slot ^= 1;
     SPECSIM_CUDA(cudaEventSynchronize(in_ev[in_slot]));
