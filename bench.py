@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--ttt", type=int, default=1,
                     help="EAGLE-3 training-time-test unroll passes per step (1 = the headline "
                          "single-pass step)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: fixed global batch of sequences split over the ranks "
+                         "(0 = weak scaling, the config's per-rank micro-batch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seq", type=int, default=256,
@@ -164,8 +167,8 @@ def run_reference(args):
     tps = steps * seq / dt
     line = dict(impl="reference", metric="draft-train tokens/sec", value=round(tps, 3),
                 unit="tokens/s", n_gpus=args.gpus, steps=steps, warmup=warm,
-                ms_per_step=round(1e3 * dt / steps, 1), higher_is_better=True, scaling="weak",
-                vs_baseline=None, dtype="f32 (bf16-rounded operands)", data="synthetic",
+                ms_per_step=round(1e3 * dt / steps, 1), higher_is_better=True,
+                scaling=scaling_of(args), vs_baseline=None, dtype="f32 (bf16-rounded operands)", data="synthetic",
                 config=config_block(args, cfg),
                 cpu_baseline=dict(value=round(tps, 3), unit="tokens/s", cores=oracle.num_threads(),
                                   kind="port",
@@ -188,7 +191,16 @@ def workload_cfg(args, api):
     cfg = dict(api.CONFIGS[args.config])
     if args.ttt > 1:
         cfg["ttt_steps"] = args.ttt
+    if args.global_batch:
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        if args.global_batch % world:
+            raise SystemExit(f"--global-batch {args.global_batch} is not divisible by {world} ranks")
+        cfg["micro_batch"] = args.global_batch // world
     return cfg
+
+
+def scaling_of(args):
+    return "strong" if args.global_batch else "weak"
 
 
 def config_block(args, cfg):
@@ -234,10 +246,12 @@ def run_ours(args):
     pool_n = 2 * B
     L = S + 1 + cfg.get("ttt_steps", 1)  # every unroll pass fully unmasked
     W = 3 * H
-    # ring: the resident pool + every batch the e2e leg appends (warm-up and
-    # timed), so the FIFO ring never evicts the pool the device-timed leg reads
-    e2e_steps = 0 if args.no_e2e else max(1, args.warmup) + args.steps
-    buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + e2e_steps * B) * L, device=local)
+    # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps,
+    # <= 64 sequences) + one batch of slack; an e2e job may evict the pool
+    # (FIFO), which is then re-appended outside the timed regions
+    per_job = max(1, min(16, 64 // B))
+    buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + (per_job + 1) * B) * L,
+                                device=local)
     # synthetic captured requests; generated by the library in
     # parallel threads (ctypes releases the GIL)
     from concurrent.futures import ThreadPoolExecutor
@@ -257,13 +271,25 @@ def run_ours(args):
     # step's B*world slice goes to rank i mod world (specsim_dp_shard), so rank r
     # must hold exactly the ids at slice positions == r (mod world).
     RID = 10 ** 9
-    for i, (t, ids, a) in enumerate(pinned):
-        _lib.call("specsim_hsbuf_append_packed", buf.h, rank * RID + i, a, t.data_ptr(),
-                  ids.data_ptr(), L, 0)
+    pool_base = [0]
+    next_id = [0]  # same sequence on every rank -> globally known ids
+
+    def load_pool():
+        """(re-)append the pool under fresh ids: synchronous, outside timing"""
+        pool_base[0] = next_id[0]
+        for i, (t, ids, a) in enumerate(pinned):
+            _lib.call("specsim_hsbuf_append_packed", buf.h, rank * RID + pool_base[0] + i, a,
+                      t.data_ptr(), ids.data_ptr(), L, 0)
+        next_id[0] += pool_n
+
+    load_pool()
+
+    def pool_id(r, i):
+        return r * RID + pool_base[0] + i % pool_n
 
     def batch(k):
         """this rank's B pool samples for step k (step / eval calls: local ids)"""
-        return [rank * RID + (k * B + j) % pool_n for j in range(B)]
+        return [pool_id(rank, k * B + j) for j in range(B)]
 
     def global_job(steps, id_of):
         return api.global_job(steps, B, world, id_of)
@@ -287,12 +313,11 @@ def run_ours(args):
     # train(job) runs the steps; each step waits only for its own samples'
     # copies, so the DMA of later batches overlaps earlier steps.  The job's
     # losses / counters come back to the host.
-    next_id = [pool_n]  # same sequence on every rank -> globally known ids
     h2d = B * L * (W * 2 + 4)
     losses = []
 
-    def run_e2e(nsteps, per_job=16):
-        # jobs of <= 16 steps bound the ring: each job's batches are appended
+    def run_e2e(nsteps):
+        # jobs of <= per_job steps bound the ring: each job's batches are appended
         # (asynchronously, this rank's own samples), then the global job trains
         done = 0
         while done < nsteps:
@@ -319,10 +344,12 @@ def run_ours(args):
     # pinned-host appends above, host wall clock.  The e2e leg runs between
     # the two halves of the device-timed leg (value, e2e, value) so both sample
     # the same point of the power / clock ramp of a short run.
+    valid = 0
     for k in range(args.warmup):
-        tr.step(buf, batch(k))
+        valid = int(tr.step(buf, batch(k))["valid_tokens"])
     if not args.no_e2e:
         run_e2e(max(1, args.warmup))
+        load_pool()
     # value leg in two halves around one end-to-end leg of all K steps: both
     # legs centred on the same point of the power / clock ramp, and the e2e
     # leg's unhidden first-batch DMA paid once, as in a single job
@@ -334,7 +361,7 @@ def run_ours(args):
     clocks.start()
     for hi, hs in enumerate(halves):
         job = global_job(hs, lambda r, k, j, o=done_steps:
-                         r * RID + ((args.warmup + o + k) * B + j) % pool_n)
+                         pool_id(r, (args.warmup + o + k) * B + j))
         barrier()
         launches0 = _lib.kernel_launches()
         tr.region_begin()
@@ -352,6 +379,7 @@ def run_ours(args):
             e2e_dev_ms = tr.region_end()
             barrier()
             dt_e2e = max_over_ranks(time.perf_counter() - t0)
+            load_pool()
     clk = clocks.stop()
     barrier()
     value = world * T * args.steps / (region_ms / 1e3)
@@ -413,10 +441,11 @@ def run_ours(args):
 
     line = dict(metric="draft-train tokens/sec", value=round(value, 1), unit="tokens/s",
                 n_gpus=world, steps=args.steps, warmup=args.warmup,
-                ms_per_step=round(step_ms, 3), higher_is_better=True, scaling="weak",
+                ms_per_step=round(step_ms, 3), higher_is_better=True, scaling=scaling_of(args),
                 vs_baseline=None, dtype="bf16", data="synthetic (seeded captured hidden states, "
                 "random-init draft weights)", config=config_block(args, cfg), e2e=e2e,
                 roofline=roofline, gpu_launches=int(launches),
+                valid_tokens_per_rank_step=valid,
                 whole_step=dict(tflops=round(whole_step_tflops, 1),
                                 frac_of_peak=round(whole_step_tflops / pk["bf16_sustained"], 4),
                                 gflop_per_token=round(fl["total"] / 1e9, 4)),

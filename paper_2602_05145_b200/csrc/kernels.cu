@@ -502,12 +502,13 @@ __global__ void __launch_bounds__(256) ce_grad_kernel(
     const float* __restrict__ lse, const float* __restrict__ coef,
     const int32_t* __restrict__ y, int v0, int vn, long long T, __nv_bfloat16* __restrict__ dlog,
     long long ldd) {
-  // one row per blockIdx.y; each thread owns kCeGradSeg 8-column segments
+  // one row per blockIdx.x (T may exceed the 65535 limit of grid.y); each
+  // thread owns kCeGradSeg 8-column segments
   // strided by the block width (coalesced), with every logit load in flight
   // before the first use; the stored value is l - m with m the row max of the
   // 128-column half tile (the forward's partial), so p = 2^((delta + m - lse) log2 e)
-  const long long t = blockIdx.y;
-  const int j0 = (blockIdx.x * kCeGradSeg * blockDim.x + threadIdx.x) * 8;
+  const long long t = blockIdx.x;
+  const int j0 = (blockIdx.y * kCeGradSeg * blockDim.x + threadIdx.x) * 8;
   const int stride = blockDim.x * 8;
   const float l2e = 1.4426950408889634f;
   uint4 raw[kCeGradSeg];
@@ -640,7 +641,7 @@ void ce_grad(const __half* logits, long long ldl, const gemm::CePartial* partial
              __nv_bfloat16* dlog, long long ldd, cudaStream_t s) {
   if (T == 0) return;
   count_launches();
-  ce_grad_kernel<<<dim3(blocks_for(vn / 8, 256 * kCeGradSeg), static_cast<unsigned>(T)), 256, 0,
+  ce_grad_kernel<<<dim3(static_cast<unsigned>(T), blocks_for(vn / 8, 256 * kCeGradSeg)), 256, 0,
                    s>>>(
       logits, ldl, partials, lse, coef, y, v0, vn, T, dlog, ldd);
 }

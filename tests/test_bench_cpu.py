@@ -1,0 +1,54 @@
+"""bench.py host logic on CPU: the reference arm's JSON line (the driver runs it
+on the GPU box's host cores) and the weak / strong scaling workload split."""
+import json
+import pathlib
+import subprocess
+import sys
+import types
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+from paper_2602_05145_b200 import api  # noqa: E402
+
+
+def _args(**kw):
+    base = dict(config="C2", ttt=1, global_batch=0, gpus=1)
+    base.update(kw)
+    return types.SimpleNamespace(**base)
+
+
+def test_weak_scaling_keeps_the_per_rank_micro_batch(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "8")
+    cfg = bench.workload_cfg(_args(gpus=8), api)
+    assert cfg["micro_batch"] == api.CONFIGS["C2"]["micro_batch"]
+    assert bench.scaling_of(_args()) == "weak"
+
+
+def test_strong_scaling_splits_the_global_batch(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "8")
+    a = _args(config="C5", global_batch=16, gpus=8)
+    cfg = bench.workload_cfg(a, api)
+    assert cfg["micro_batch"] == 2
+    assert bench.scaling_of(a) == "strong"
+    assert bench.config_block(a, cfg)["global_batch"] == 16
+    monkeypatch.setenv("WORLD_SIZE", "3")
+    with pytest.raises(SystemExit):
+        bench.workload_cfg(_args(global_batch=16, gpus=3), api)
+
+
+def test_reference_arm_line():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "1", "--warmup", "0",
+                          "--cpu-sample-seq", "64"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["metric"] == "draft-train tokens/sec"
+    assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["higher_is_better"] is True and d["scaling"] == "weak"
