@@ -366,3 +366,41 @@ def test_swiglu_backward_epilogue_equals_unfused(monkeypatch):
     assert l0 == l1
     for nm in g0:
         assert rel(g0[nm], g1[nm]) <= 1e-5, (nm, rel(g0[nm], g1[nm]))
+
+
+def test_max_batch_rows_split_additivity():
+    """Maximum micro-batch (kMaxBatch = 64 sequences, T = 65,536 rows: more rows
+    than a CUDA grid's y extent) vs the same rows in four 16-sequence steps
+    normalised by the full batch's valid count (`global_valid`): the loss and
+    every gradient are additive over rows, so the four parts must sum to the
+    full step.  lr = 1e-30 keeps the weights fixed between the steps.  Bound:
+    fp32 accumulation order over different row tilings, rel-Frobenius <= 2e-3."""
+    c = dict(hidden=256, vocab=4096, seq_len=1024, n_heads=4, n_kv_heads=2, head_dim=64,
+             ffn=512, micro_batch=64, rms_eps=1e-5, rope_theta=10000.0)
+    L = c["seq_len"] + 2
+    buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 64 * L + 1024)
+    for i in range(64):
+        # ragged tail: a few short samples (masked positions, padding rows)
+        n = L if i % 9 else L - 300 - i
+        cap = oracle.synth_capture(SEED, i, n, c["vocab"], c["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+    tr = api.DraftTrainer(c, lr=1e-30, seed=SEED)
+    tr.keep_grads(True)
+    names = ("fc", "qkv", "o", "gate_up", "down", "lm_head", "w_in", "w_hid", "w_post", "w_fin")
+    full = tr.step(buf, list(range(64)))
+    g_full = {nm: tr.get_grad(nm).astype(np.float64) for nm in names}
+    n_valid = full["valid_tokens"]
+    assert full["positions"] == 64 * c["seq_len"]
+    loss, g_sum, valid = 0.0, {nm: 0.0 for nm in names}, 0
+    for q in range(4):
+        r = tr.step(buf, list(range(16 * q, 16 * q + 16)), global_valid=n_valid)
+        loss += r["loss"]
+        valid += r["valid_tokens"]
+        for nm in names:
+            g_sum[nm] = g_sum[nm] + tr.get_grad(nm).astype(np.float64)
+    assert valid == n_valid
+    assert abs(loss - full["loss"]) <= 1e-4 * abs(full["loss"]), (loss, full["loss"])
+    for nm in names:
+        rel = np.linalg.norm(g_sum[nm] - g_full[nm]) / np.linalg.norm(g_full[nm])
+        assert rel <= 2e-3, (nm, rel)
+    tr.close(); buf.close()
