@@ -31,6 +31,19 @@
 // epilogue's probe variants, 5: the 128-bit epilogue (scripts/adamw_probe.sh)
 #define SPECSIM_ADAMW_VARIANT 0
 #endif
+#ifndef SPECSIM_ADAMW_PREFETCH
+// fused-AdamW epilogue: L2 prefetch of the optimizer state (p, m, v) of the
+// thread's row.  0 none; 1 the whole half-tile row before waiting for the
+// accumulator; 2 the first 32-column chunk before the wait, then chunk c+1
+// while chunk c is processed
+#define SPECSIM_ADAMW_PREFETCH 0
+#endif
+#ifndef SPECSIM_ADAMW_WINDOW
+// probe only (scripts/adamw_probe.sh): > 0 folds every optimizer-state access
+// of the 256-bit epilogue into a window of this many elements (a power of 2),
+// i.e. the same SM <-> L2 traffic with the state L2-resident instead of in HBM
+#define SPECSIM_ADAMW_WINDOW 0
+#endif
 
 namespace specsim {
 namespace gemm {
@@ -254,6 +267,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int mb, nb;
       tile_coords(tile, args, mb, nb);
       const int m0 = mb * C_::TILE_M + static_cast<int>(rank) * BM, n0 = nb * BN;
+      if constexpr (EPI == EPI_ADAMW && SPECSIM_ADAMW_PREFETCH > 0) {
+        // the state of this thread's row streams into L2 while the tile's
+        // mainloop runs (the epilogue would otherwise wait on DRAM latency)
+        const int prow = m0 + quad * 32 + lane;
+        const int pc = n0 + c_begin;
+        if (prow < args.M && pc < args.N) {
+          const int ncol = SPECSIM_ADAMW_PREFETCH == 1 ? min(BN / 2, args.N - pc)
+                                                       : min(32, args.N - pc);
+          const long long e = static_cast<long long>(prow) * args.ldc + pc;
+          ptx::prefetch_l2_bulk(args.opt_p + e, 4u * ncol);
+          ptx::prefetch_l2_bulk(args.opt_m + e, 4u * ncol);
+          ptx::prefetch_l2_bulk(args.opt_v + e, 4u * ncol);
+        }
+      }
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const int row_base = m0 + quad * 32;
@@ -435,6 +462,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const AdamDev hp = *args.opt_hp;
 #pragma unroll 1
         for (int c = c_begin; c < c_end; c += 32) {
+          if constexpr (SPECSIM_ADAMW_PREFETCH == 2) {
+            const int pc = n0 + c + 32;
+            if (row_ok && c + 32 < c_end && pc < args.N) {
+              const long long e = static_cast<long long>(row) * args.ldc + pc;
+              const uint32_t nb4 = 4u * min(32, args.N - pc);
+              ptx::prefetch_l2_bulk(args.opt_p + e, nb4);
+              ptx::prefetch_l2_bulk(args.opt_m + e, nb4);
+              ptx::prefetch_l2_bulk(args.opt_v + e, nb4);
+            }
+          }
           uint32_t r[32];
           __syncwarp();
           ptx::tmem_ld_32x32b_x32(t_row + c, r);
@@ -461,6 +498,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int rw = row_base + rl;
               ok[it] = col_ok && rw < args.M;
               e[it] = static_cast<long long>(rw) * args.ldc + col;
+              if constexpr (SPECSIM_ADAMW_WINDOW > 0) e[it] &= SPECSIM_ADAMW_WINDOW - 1;
               const float4 a = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
               const float4 b = *reinterpret_cast<const float4*>(stg + rl * 36 + cl + 4);
               gv[it][0] = a.x; gv[it][1] = a.y; gv[it][2] = a.z; gv[it][3] = a.w;
