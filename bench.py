@@ -392,6 +392,23 @@ def run_ours(args):
                    timing="host wall clock around the async pinned-host appends + train(job) "
                           "of the K steps, run between the two halves of the device-timed leg, "
                           "max over ranks")
+        # ingest alone (reported separately): one job's worth of
+        # pinned-host appends with nothing else running, host wall clock
+        n_in = per_job * B
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(n_in):
+            t, idt, a = pinned[i % pool_n]
+            _lib.call("specsim_hsbuf_append_packed", buf.h, rank * RID + next_id[0] + i, a,
+                      t.data_ptr(), idt.data_ptr(), L, 2)
+        torch.cuda.synchronize()
+        dt_in = time.perf_counter() - t0
+        next_id[0] += n_in
+        e2e["ingest"] = dict(h2d_GBps=round(n_in * L * (W * 2 + 4) / dt_in / 1e9, 1),
+                             tokens_per_s=round(n_in * L / dt_in, 1),
+                             sample=f"{n_in} captured requests of {L} tokens appended "
+                                    "(append_packed, async pinned DMA), nothing else running")
+        load_pool()
 
     # ------------------------------------------------------------ roofline leg
     # Per-phase device time with CUDA events around every launch (a graph with
