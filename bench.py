@@ -246,10 +246,11 @@ def run_ours(args):
     pool_n = 2 * B
     L = S + 1 + cfg.get("ttt_steps", 1)  # every unroll pass fully unmasked
     W = 3 * H
-    # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps,
-    # <= 64 sequences) + one batch of slack; an e2e job may evict the pool
-    # (FIFO), which is then re-appended outside the timed regions
-    per_job = max(1, min(16, 64 // B))
+    # ring: the resident pool + the batches of one e2e train(job) (<= 32 steps,
+    # <= 128 sequences; the reference's jobs hold n_threshold = 2048 samples,
+    # SPEC.md:364) + one batch of slack; an e2e job may evict the pool (FIFO),
+    # which is then re-appended outside the timed regions
+    per_job = max(1, min(32, 128 // B))
     buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + (per_job + 1) * B) * L,
                                 device=local)
     # synthetic captured requests; generated by the library in
