@@ -693,6 +693,11 @@ void fetch_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t 
   fetch_mapped_kernel<<<1, 128, 0, s>>>(src, dst, n_words);
 }
 
+void store_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s) {
+  count_launches();
+  fetch_mapped_kernel<<<1, 128, 0, s>>>(src, dst, n_words);
+}
+
 void pack_packed(const __nv_bfloat16* src, int W, int n, __nv_bfloat16* ring_feat, long long cap,
                  long long pos, cudaStream_t s) {
   if (n <= 0) return;

@@ -73,6 +73,10 @@ void colsum(const float* parts, long long rows, int H, float* out, cudaStream_t 
 // the SMs over PCIe: stages the per-step inputs without a copy-engine H2D,
 // which would queue behind bulk ingest DMA issued earlier on another stream.
 void fetch_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s);
+// The reverse: dst (mapped pinned host memory) = src (device), stores over
+// PCIe from the SMs; used for the per-step loss / counters so no D2H
+// copy-engine transfer sits in the trainer stream behind ingest DMA.
+void store_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s);
 
 // NeoX RoPE on the q and k heads of a [T, NQ] row-major buffer, in place.
 void rope(__nv_bfloat16* qkv, long long T, int S, int NQ, int n_rot_heads, int hd,

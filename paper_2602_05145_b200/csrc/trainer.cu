@@ -438,7 +438,7 @@ class DraftTrainerImpl {
     const char* ng = std::getenv("SPECSIM_NO_GRAPH");
     use_graphs = !(ng && ng[0] == '1');
     SPECSIM_CUDA(cudaMallocHost(&h_nglobal, sizeof(long long)));
-    SPECSIM_CUDA(cudaMallocHost(&h_stats, 4 * sizeof(double)));
+    SPECSIM_CUDA(cudaHostAlloc(&h_stats, 4 * sizeof(double), cudaHostAllocMapped));
     SPECSIM_CUDA(cudaMemsetAsync(Mst, 0, sizeof(float) * total, stream));
     SPECSIM_CUDA(cudaMemsetAsync(Vst, 0, sizeof(float) * total, stream));
     SPECSIM_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * total, stream));
@@ -1118,9 +1118,17 @@ class DraftTrainerImpl {
     });
   }
 
+  // the step's loss / valid / correct (3 doubles) into mapped pinned memory
+  // by a one-warp kernel: a D2H copy-engine transfer here would queue behind
+  // ingest DMA the caller issued earlier and stall every later step
+  void stats_to_host(double* dst_mapped) {
+    kern::store_mapped(reinterpret_cast<const uint32_t*>(stats),
+                       reinterpret_cast<uint32_t*>(dst_mapped), 6, stream);
+  }
+
   StepResult end_step() {
     SPECSIM_CUDA(cudaEventRecord(ev_end, stream));
-    SPECSIM_CUDA(cudaMemcpyAsync(h_stats, stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    stats_to_host(h_stats);
     SPECSIM_CHECK_LAUNCH();
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
     float ms = 0;
@@ -1264,7 +1272,7 @@ class DraftTrainerImpl {
     if (need > hist_cap) {
       if (hist_buf) cudaFreeHost(hist_buf);
       hist_buf = nullptr;
-      SPECSIM_CUDA(cudaMallocHost(&hist_buf, sizeof(double) * need * 2));
+      SPECSIM_CUDA(cudaHostAlloc(&hist_buf, sizeof(double) * need * 2, cudaHostAllocMapped));
       hist_cap = need * 2;
     }
     double* hist = hist_buf;
@@ -1276,8 +1284,7 @@ class DraftTrainerImpl {
         prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, true);
         launch(buf, true);
         step_count += 1;
-        SPECSIM_CUDA(cudaMemcpyAsync(hist + 3 * k++, stats, 3 * sizeof(double),
-                                     cudaMemcpyDeviceToHost, stream));
+        stats_to_host(hist + 3 * k++);
       }
     }
     // alpha_eval = top-1 accuracy of the new draft on D_eval
@@ -1285,8 +1292,7 @@ class DraftTrainerImpl {
       shard(ne, j, mine, job.eval_ids);
       prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, false);
       launch(buf, false);
-      SPECSIM_CUDA(cudaMemcpyAsync(hist + 3 * k++, stats, 3 * sizeof(double),
-                                   cudaMemcpyDeviceToHost, stream));
+      stats_to_host(hist + 3 * k++);
     }
     SPECSIM_CHECK_LAUNCH();
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
