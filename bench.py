@@ -246,15 +246,18 @@ def run_ours(args):
     pool_n = 2 * B
     L = S + 1 + cfg.get("ttt_steps", 1)  # every unroll pass fully unmasked
     W = 3 * H
-    # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps,
-    # <= 64 sequences) + one batch of slack; an e2e job may evict the pool
-    # (FIFO), which is then re-appended outside the timed regions.  Longer
-    # jobs queue more asynchronous appends than the driver's per-stream work
-    # queue holds: the host then blocks inside the appends until the DMA
-    # drains and the job's steps stop overlapping it (measured: 30-step jobs
-    # read e2e 9% below the device number, 8- / 16-step jobs 2%).
-    # SPECSIM_BENCH_E2E_JOB overrides the job length (that experiment).
-    per_job = int(os.environ.get("SPECSIM_BENCH_E2E_JOB", "0")) or max(1, min(16, 64 // B))
+    # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps
+    # and <= 2 GiB of captured states) + one batch of slack; an e2e job may
+    # evict the pool (FIFO), which is then re-appended outside the timed
+    # regions.  Larger jobs queue more asynchronous DMA than the driver's
+    # per-stream work queue holds: the host then blocks inside the appends
+    # until the DMA drains and the job's steps stop overlapping it (measured
+    # at C2: 6 GB jobs read e2e 9% below the device number, 1.6-3.2 GB jobs
+    # 2%; C4 / C5 4-6 GB jobs 6-8%).  SPECSIM_BENCH_E2E_JOB overrides the job
+    # length (that experiment).
+    step_bytes = B * L * (W * 2 + 4)
+    per_job = int(os.environ.get("SPECSIM_BENCH_E2E_JOB", "0")) or \
+        max(1, min(16, (2 << 30) // step_bytes))
     buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + (per_job + 1) * B) * L,
                                 device=local)
     # synthetic captured requests; generated by the library in
