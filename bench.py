@@ -85,6 +85,13 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a few hundred ms to start: wait for its first
+            # sample so even a short timed region is covered
+            t0 = time.time()
+            while time.time() - t0 < 5 and self.proc.poll() is None:
+                if self.path.stat().st_size > 0:
+                    break
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 

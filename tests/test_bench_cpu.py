@@ -52,3 +52,31 @@ def test_reference_arm_line():
     assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["higher_is_better"] is True and d["scaling"] == "weak"
+
+
+@pytest.mark.gpu
+def test_bench_line_contract_gpu():
+    """The driver parses one JSON line from `bench.py`: every contract key with
+    sane values, on the tiny config so it runs in seconds."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "C1", "--steps", "4",
+                          "--warmup", "3", "--cpu-sample-seq", "32"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "roofline", "cpu_baseline", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 4 and d["warmup"] == 3 and d["n_gpus"] == 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["ingest"]["h2d_GBps"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "tensor"
+    assert 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"], abs=1e-4)  # 4 decimals
+    assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["gpu_launches"] >= 4 * 20  # every step is tens of our own kernels
+    assert d["clocks"]["sm_max_mhz"] > 0
+    assert d["config"]["workload"].startswith("C1")
