@@ -870,6 +870,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // S is double-buffered (columns 128 and 384): S_{j+1} is computed while the
+  // softmax warps turn S_j / dP_j into dS_j, off the per-block critical path
   const uint32_t tdQ = tmem, tS = tmem + 128, tdP = tmem + 256;
 
   if (warp == 0) {
@@ -901,19 +903,29 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q), adO = ptx::smem_u32(smem + L::OFF_DO);
       const uint32_t aS = ptx::smem_u32(smem + L::OFF_DS);
       ptx::mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
+      // S_j into buffer j & 1; that buffer last held S_{j-2}, released by the
+      // s_free of block j-2, which issuing dP_{j-1} already waited for
+      auto issue_s = [&](int j) {
         const int st = j & 1;
         ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
-        ptx::mbar_wait(s_free, (j & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::umma_bf16(tS + (j & 1) * 256, kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        ptx::mbar_wait(s_free, (j & 1) ^ 1);  // softmax of j-1 done with dP (and S_{j-1})
         ptx::tc_fence_after();
         const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
         const uint32_t aV = ptx::smem_u32(smem + L::OFF_V + st * L::T128);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          ptx::umma_bf16(tS, kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk)
           ptx::umma_bf16(tdP, kdesc(adO, kk), kdesc(aV, kk), idS, kk > 0 ? 1u : 0u);
-        }
-        ptx::umma_commit(s_full);
+        ptx::umma_commit(s_full);  // S_j and dP_j
+        if (j + 1 < nkv) issue_s(j + 1);
         ptx::mbar_wait(ds_full, j & 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -945,7 +957,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t sv[32], pv[32];
-        ptx::tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        ptx::tmem_ld_32x32b_x32(tS + (j & 1) * 256 + lane_off + c * 32, sv);
         ptx::tmem_ld_32x32b_x32(tdP + lane_off + c * 32, pv);
         ptx::tmem_ld_wait();
 #pragma unroll
