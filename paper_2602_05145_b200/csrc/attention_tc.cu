@@ -836,8 +836,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* k_full = bar + 1;   // [2]
   uint64_t* k_empty = bar + 3;  // [2]
   uint64_t* s_full = bar + 5;
-  uint64_t* s_free = bar + 6;
-  uint64_t* ds_full = bar + 7;
+  uint64_t* ds_full = bar + 7;  // (bar + 6 unused)
   uint64_t* ds_free = bar + 8;
   uint64_t* all_done = bar + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
@@ -859,7 +858,6 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_init(&k_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_free, 4);
     ptx::mbar_init(ds_full, 4);
     ptx::mbar_init(ds_free, 1);
     ptx::mbar_init(all_done, 1);
@@ -914,25 +912,32 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < HD / 16; ++kk)
           ptx::umma_bf16(tS + (j & 1) * 256, kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
       };
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        ptx::mbar_wait(s_free, (j & 1) ^ 1);  // softmax of j-1 done with dP (and S_{j-1})
-        ptx::tc_fence_after();
-        const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
-        const uint32_t aV = ptx::smem_u32(smem + L::OFF_V + st * L::T128);
+      // dP_j into the single dP buffer (free once the softmax of j-1 is done:
+      // the caller has waited ds_full of j-1), then the S_j / dP_j commit
+      auto issue_dp = [&](int j) {
+        const uint32_t aV = ptx::smem_u32(smem + L::OFF_V + (j & 1) * L::T128);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           ptx::umma_bf16(tdP, kdesc(adO, kk), kdesc(aV, kk), idS, kk > 0 ? 1u : 0u);
         ptx::umma_commit(s_full);  // S_j and dP_j
-        if (j + 1 < nkv) issue_s(j + 1);
-        ptx::mbar_wait(ds_full, j & 1);
+      };
+      issue_s(0);
+      issue_dp(0);
+      if (nkv > 1) issue_s(1);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        ptx::mbar_wait(ds_full, j & 1);  // softmax of j done: dP, S_j buffer, dS_j written
         ptx::tc_fence_after();
+        // dP_{j+1} first, so the softmax of j+1 starts while dQ_j runs
+        if (j + 1 < nkv) issue_dp(j + 1);
+        const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           ptx::umma_bf16(tdQ, kdesc(aS, kk), mndesc(aK, kk), idQ, (j > 0 || kk > 0) ? 1u : 0u);
         ptx::umma_commit(ds_free);
         ptx::umma_commit(&k_empty[st]);
+        // S_{j+2} reuses S_j's buffer and K stage j & 1 (refilled once dQ_j is done)
+        if (j + 2 < nkv) issue_s(j + 2);
       }
       ptx::umma_commit(all_done);
     }
@@ -950,9 +955,6 @@ __global__ void __launch_bounds__(192, 1)
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(s_full, j & 1);
       ptx::tc_fence_after();
-      // dS is written straight into the (single) smem tile, so wait for the
-      // dQ MMA of j-1 to have consumed it
-      ptx::mbar_wait(ds_free, (j & 1) ^ 1);
       const bool diag = (j == qb);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -960,9 +962,10 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tmem_ld_32x32b_x32(tS + (j & 1) * 256 + lane_off + c * 32, sv);
         ptx::tmem_ld_32x32b_x32(tdP + lane_off + c * 32, pv);
         ptx::tmem_ld_wait();
+        uint32_t ddc[4][4];
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
-          uint32_t dd[4];
+          uint32_t* dd = ddc[i >> 3];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
             const int kcol = c * 32 + i + e;
@@ -982,19 +985,22 @@ __global__ void __launch_bounds__(192, 1)
                 ptx::fadd2(ptx::f32x2(__uint_as_float(pv[i + e]), __uint_as_float(pv[i + e + 1])),
                            nD2)));
           }
+        }
+        // dS goes straight into the (single) smem tile: the first chunk's
+        // math above overlaps the dQ MMA of j-1, which must be done reading it
+        if (c == 0) ptx::mbar_wait(ds_free, (j & 1) ^ 1);
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
           const int key = c * 32 + i;
           const int t = key >> 6, cc = (key & 63) >> 3;
           *reinterpret_cast<uint4*>(sS + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(dd[0], dd[1], dd[2], dd[3]);
+              make_uint4(ddc[i >> 3][0], ddc[i >> 3][1], ddc[i >> 3][2], ddc[i >> 3][3]);
         }
       }
       ptx::tc_fence_before();
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive(s_free);
-        ptx::mbar_arrive(ds_full);
-      }
+      if (lane == 0) ptx::mbar_arrive(ds_full);  // also frees S_j and dP for the MMA warp
     }
     ptx::mbar_wait(all_done, 0);
     ptx::tc_fence_after();
