@@ -155,7 +155,11 @@ int specsim_hsbuf_append(specsim_hsbuf* buf, int64_t sample_id, double alpha,
  * ASYNCHRONOUSLY on the buffer's stream so the DMA overlaps a running step —
  * the caller keeps the buffers unmodified until the next trainer step / eval
  * on this buffer returns or specsim_hsbuf_sync() is called.  Trainer steps
- * are ordered after every append by an event (no host synchronisation). */
+ * are ordered after every append by an event (no host synchronisation).
+ * Keep at most ~2 GiB of mode-2 appends queued ahead of the steps that
+ * consume them: beyond a few GB the driver's per-stream work queue is full,
+ * the call blocks until earlier DMA drains and the overlap is lost
+ * (DESIGN.md §10). */
 int specsim_hsbuf_append_packed(specsim_hsbuf* buf, int64_t sample_id, double alpha,
                                 const uint16_t* features, const int32_t* token_ids, int32_t n,
                                 int mode);
