@@ -358,9 +358,17 @@ __global__ void __launch_bounds__(256) ce_reduce_kernel(
   const long long t = static_cast<long long>(blockIdx.x) * 32 + lane;
   CeAcc a{-INFINITY, 0.f, -INFINITY, 0x7fffffff};
   if (t < T) {
-    for (int nb = warp; nb < num_nb; nb += 8) {
-      const gemm::CePartial p = part[static_cast<long long>(nb) * T + t];
-      ce_merge(a, p.max, p.sum, p.target, p.argmax);
+    // eight partials in flight per lane before merging (the merge chain is
+    // serial; the loads are not)
+    constexpr int U = 8;
+    for (int nb0 = warp; nb0 < num_nb; nb0 += 8 * U) {
+      gemm::CePartial p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (nb0 + 8 * u < num_nb) p[u] = part[static_cast<long long>(nb0 + 8 * u) * T + t];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (nb0 + 8 * u < num_nb) ce_merge(a, p[u].max, p[u].sum, p[u].target, p[u].argmax);
     }
   }
   red[warp][lane] = a;
