@@ -243,10 +243,18 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ p
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, slice = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (col < H)
-    for (long long r = slice; r < rows; r += 8) s += part[r * H + col];
-  red[slice][lane] = s;
+  // four independent accumulators (rows r, r+8, r+16, r+24 of the slice):
+  // four loads in flight per thread, still a fixed summation order
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  if (col < H) {
+    long long r = slice;
+    for (; r + 24 < rows; r += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += part[(r + 8 * u) * H + col];
+    }
+    for (int u = 0; r < rows; r += 8, ++u) a[u] += part[r * H + col];
+  }
+  red[slice][lane] = (a[0] + a[1]) + (a[2] + a[3]);
   __syncthreads();
   if (slice == 0 && col < H) {
     float t = 0.f;
