@@ -38,6 +38,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+/* The library is built with hidden default visibility; every entry point
+ * declared here is exported (and nothing else of the C++ internals). */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -387,6 +393,16 @@ int specsim_trainer_region(specsim_trainer* t, int end, double* ms);
 int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
                                 int32_t* launches7);
 
+/* Per-row device state of the last step / eval, copied to the host (parity
+ * tests: the target gather and top-1 are checked bit-exact against the
+ * oracle).  name: "u", "y", "m", "argmax" (int32, K*B*S rows:
+ * unroll slice j at rows j*B*S; eval fills slice 0 only), "lse" (fp32, K*B*S
+ * rows), "F" (bf16 bits, [B*S, layers*hidden]: the micro-batch features the
+ * fc GEMM read).  *n_elems (nullable) receives the element count; host_out
+ * may be NULL to query it, otherwise it must hold cap_elems >= that count. */
+int specsim_trainer_read_rows(const specsim_trainer* t, const char* name, void* host_out,
+                              int64_t cap_elems, int64_t* n_elems);
+
 /* ------------------------------------------------------ kernel test hooks */
 /* Host-buffer wrappers around single kernels, used by the parity tests.
  * GEMM: epi 0 bf16 out, 1 f32 out, 2 f32 accumulate (C in/out), 3 bf16 out
@@ -406,6 +422,10 @@ int specsim_debug_attention(int32_t B, int32_t S, int32_t nh, int32_t nkv, int32
 
 #ifdef __cplusplus
 }
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
 #endif
 
 #endif /* SPECSIM_DRAFT_TRAINER_H */

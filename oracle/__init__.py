@@ -74,6 +74,8 @@ def lib():
                                      C.c_int64, C.c_int, C.c_int, C.POINTER(StepOut)]
         L.orc_forward.argtypes = [C.POINTER(Shape), P, P, P, P, P, P, C.c_int64, C.c_int,
                                   C.POINTER(StepOut), P, P]
+        L.orc_forward_ex.argtypes = [C.POINTER(Shape), P, P, P, P, P, P, C.c_int64, C.c_int,
+                                     C.POINTER(StepOut), P, P, P, P, P]
         L.orc_adamw.argtypes = [C.c_int64, P, P, P, P, P, C.c_int64]
         L.orc_num_threads.restype = C.c_int
         _lib = L
@@ -262,15 +264,24 @@ def train_step(shape, adamw, step_k, params, mst, vst, E, F, u, y, m, global_val
     return out, grads
 
 
-def forward(shape, params, E, F, u, y, m, global_valid=0, round_bf16=True):
+def forward(shape, params, E, F, u, y, m, global_valid=0, round_bf16=True, margin=False,
+            probe=None):
+    """(StepOut, lse, argmax[, margin][, probe_gap]) over the K*B*S rows;
+    margin = top-1 minus top-2 logit per row (0 on ties); probe_gap[r] = the
+    oracle's max logit minus its logit at vocabulary index probe[r]."""
     out = StepOut()
     T = shape.B * shape.S * ttt_of(shape)
     lse = np.zeros(T, np.float32)
     am = np.zeros(T, np.int32)
-    if lib().orc_forward(C.byref(shape), _p(params), _p(E), _p(F), _p(u), _p(y), _p(m),
-                         global_valid, 1 if round_bf16 else 0, C.byref(out), _p(lse), _p(am)):
+    mg = np.zeros(T, np.float32) if margin else None
+    pr = None if probe is None else np.ascontiguousarray(probe[:T], np.int32)
+    pl = None if probe is None else np.zeros(T, np.float32)
+    if lib().orc_forward_ex(C.byref(shape), _p(params), _p(E), _p(F), _p(u), _p(y), _p(m),
+                            global_valid, 1 if round_bf16 else 0, C.byref(out), _p(lse), _p(am),
+                            _p(mg), _p(pr), _p(pl)):
         raise ValueError("bad shape")
-    return out, lse, am
+    res = (out, lse, am) + ((mg,) if margin else ()) + ((pl,) if probe is not None else ())
+    return res
 
 
 def adamw(p, m, v, g, hp, step_k):

@@ -278,7 +278,7 @@ static float silu(float x) { return x / (1.0f + expf(-x)); }
 /* activations of one unroll step of the decoder layer (+ its LM head) */
 typedef struct step_acts {
   float *E_rows, *U, *rstd_a, *rstd_b, *qkv, *o, *lse_attn, *r, *z, *rstd_post, *gu, *act, *h,
-      *nrm, *rstd_fin, *lse, *dlog;
+      *nrm, *rstd_fin, *lse, *dlog, *margin;
   int32_t* argmax;
 } step_acts;
 
@@ -301,7 +301,7 @@ static void model_free(model* M) {
     step_acts* a = &M->st[j];
     float** ptrs[] = {&a->E_rows, &a->U,   &a->rstd_a,   &a->rstd_b, &a->qkv, &a->o,
                       &a->lse_attn, &a->r, &a->z,        &a->rstd_post, &a->gu, &a->act,
-                      &a->h,      &a->nrm, &a->rstd_fin, &a->lse,    &a->dlog};
+                      &a->h,      &a->nrm, &a->rstd_fin, &a->lse,    &a->dlog, &a->margin};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) {
       free(*ptrs[i]);
       *ptrs[i] = NULL;
@@ -493,18 +493,23 @@ static void ce_stats(model* M, const int32_t* y, const int32_t* mask, int64_t gl
     const int32_t* mj = mask + (int64_t)j * T;
     a->lse = falloc(T);
     a->argmax = (int32_t*)calloc((size_t)T, sizeof(int32_t));
+    a->margin = falloc(T);
     double loss = 0.0;
     int64_t top1 = 0;
 #pragma omp parallel for schedule(static) reduction(+ : loss, top1)
     for (int64_t t = 0; t < T; ++t) {
       const float* l = a->dlog + t * V;
-      float mx = -INFINITY;
+      float mx = -INFINITY, mx2 = -INFINITY; /* top-1 / top-2 logits (ties: margin 0) */
       int32_t am = 0;
       for (int64_t v = 0; v < V; ++v)
         if (l[v] > mx) {
+          mx2 = mx;
           mx = l[v];
           am = (int32_t)v;
+        } else if (l[v] > mx2) {
+          mx2 = l[v];
         }
+      a->margin[t] = mx - mx2;
       double sum = 0.0;
       for (int64_t v = 0; v < V; ++v) sum += exp((double)l[v] - mx);
       const float lse = mx + (float)log(sum);
@@ -547,6 +552,14 @@ static int shape_ok(const orc_shape* s) {
 int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, const uint16_t* F,
                 const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
                 int round_bf16, orc_step_out* out, float* lse_out, int32_t* argmax_out) {
+  return orc_forward_ex(s, params, E, F, u, y, mask, global_valid, round_bf16, out, lse_out,
+                        argmax_out, NULL, NULL, NULL);
+}
+
+int orc_forward_ex(const orc_shape* s, const float* params, const uint16_t* E, const uint16_t* F,
+                   const int32_t* u, const int32_t* y, const int32_t* mask, int64_t global_valid,
+                   int round_bf16, orc_step_out* out, float* lse_out, int32_t* argmax_out,
+                   float* margin_out, const int32_t* probe_idx, float* probe_gap) {
   if (!shape_ok(s)) return 1;
   int64_t off[ORC_NPARAMS];
   orc_param_layout(s, NULL, NULL, NULL, off);
@@ -558,6 +571,14 @@ int orc_forward(const orc_shape* s, const float* params, const uint16_t* E, cons
   for (int j = 0; j < M.K; ++j) {
     if (lse_out) memcpy(lse_out + (int64_t)j * M.T, M.st[j].lse, sizeof(float) * M.T);
     if (argmax_out) memcpy(argmax_out + (int64_t)j * M.T, M.st[j].argmax, sizeof(int32_t) * M.T);
+    if (margin_out) memcpy(margin_out + (int64_t)j * M.T, M.st[j].margin, sizeof(float) * M.T);
+    if (probe_idx && probe_gap)
+      for (int64_t t = 0; t < M.T; ++t) {
+        const int64_t r = (int64_t)j * M.T + t;
+        const int32_t v = probe_idx[r];
+        const float* l = M.st[j].dlog + t * M.V;
+        probe_gap[r] = (v >= 0 && v < M.V) ? l[M.st[j].argmax[t]] - l[v] : NAN;
+      }
   }
   model_free(&M);
   return 0;

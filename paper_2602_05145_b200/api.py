@@ -415,6 +415,20 @@ class DraftTrainer:
     def keep_grads(self, on: bool = True):
         call("specsim_trainer_keep_grads", self.h, 1 if on else 0)
 
+    _ROW_DTYPES = {"u": np.int32, "y": np.int32, "m": np.int32, "argmax": np.int32,
+                   "lse": np.float32, "F": np.uint16}
+
+    def read_rows(self, name):
+        """Device per-row state of the last step / eval (u, y, m, argmax, lse
+        over K*B*S rows; F as [B*S, layers*hidden] bf16 bits)."""
+        n = C.c_int64()
+        call("specsim_trainer_read_rows", self.h, name.encode(), None, 0, C.byref(n))
+        a = np.zeros(n.value, self._ROW_DTYPES[name])
+        call("specsim_trainer_read_rows", self.h, name.encode(), ptr(a), n.value, C.byref(n))
+        if name == "F":
+            a = a.reshape(self.shape["micro_batch"] * self.shape["seq_len"], -1)
+        return a
+
     def set_embedding(self, e_bf16):
         a = np.ascontiguousarray(e_bf16, np.uint16)
         call("specsim_trainer_set_embedding", self.h, ptr(a))

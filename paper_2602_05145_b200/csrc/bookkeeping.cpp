@@ -3,7 +3,7 @@
 // Semantics follow the reference (rng.hpp:13-39, perf_model.cpp:30-41,
 // perf_model.cpp:159-177, perf_model.cpp:213-224, SPEC.md:237-241,
 // SPEC.md:294) and are checked bit-exact against the compiled
-// reference by tests/test_bookkeeping_capi.py.  Compiled without FP
+// reference by tests/test_capi_cpu.py (golden vectors from oracle/_ref).  Compiled without FP
 // contraction (see Makefile) so every double rounds like the reference.
 #include <algorithm>
 #include <cmath>
@@ -12,10 +12,12 @@
 #include <thread>
 #include <vector>
 
+#include "bookkeeping.h"
 #include "common.h"
 #include "specsim/draft_trainer.hpp"
 
 namespace specsim {
+namespace bk {
 
 double Rng::uniform() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
 
@@ -95,6 +97,8 @@ double alpha_from_accept_length(double ell, int gamma) {
   return 0.5 * (lo + hi);
 }
 
+}  // namespace bk
+
 void split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval) {
   if (n < 0) throw std::invalid_argument("sample count must be >= 0");
   *n_train = (9 * n) / 10;
@@ -129,17 +133,18 @@ void synth_capture(uint64_t seed, int64_t index, int length, int vocab, int hidd
   p.check(vocab >= 1, "vocab must be >= 1");
   p.check(hidden >= 1 && layers >= 1, "hidden and layers must be >= 1");
   p.throw_if_any();
-  Rng rng(seed + static_cast<uint64_t>(index));
+  bk::Rng rng(seed + static_cast<uint64_t>(index));
   int total = 0, steps = 0;
   while (total < length) {
-    int k = sample_accept_length(rng, alpha, gamma);
+    int k = bk::sample_accept_length(rng, alpha, gamma);
     k = std::min(k, length - total);  // request completes mid-step
     if (accept_lengths) accept_lengths[steps] = k;
     total += k;
     ++steps;
   }
   if (n_steps) *n_steps = steps;
-  if (alpha_s) *alpha_s = alpha_from_accept_length(static_cast<double>(length) / steps, gamma);
+  if (alpha_s)
+    *alpha_s = bk::alpha_from_accept_length(static_cast<double>(length) / steps, gamma);
   for (int i = 0; i < length; ++i) {
     const auto id = static_cast<int32_t>(std::floor(rng.uniform() * vocab));
     if (ids) ids[i] = id;
@@ -157,7 +162,7 @@ void synth_capture(uint64_t seed, int64_t index, int length, int vocab, int hidd
 using namespace specsim;
 
 struct specsim_rng {
-  Rng r;
+  bk::Rng r;
 };
 
 extern "C" {
@@ -165,7 +170,7 @@ extern "C" {
 int specsim_rng_create(uint64_t seed, specsim_rng** out) {
   return guard([&] {
     if (!out) throw std::invalid_argument("out is null");
-    *out = new specsim_rng{Rng(seed)};
+    *out = new specsim_rng{bk::Rng(seed)};
   });
 }
 int specsim_rng_destroy(specsim_rng* r) {
@@ -184,19 +189,19 @@ int specsim_rng_next_u64(specsim_rng* r, uint64_t* out) {
   return guard([&] { *out = r->r.next_u64(); });
 }
 int specsim_expected_accept_length(double alpha, int32_t gamma, double* out) {
-  return guard([&] { *out = expected_accept_length(alpha, gamma); });
+  return guard([&] { *out = bk::expected_accept_length(alpha, gamma); });
 }
 int specsim_sample_accept_length(specsim_rng* r, double alpha, int32_t gamma, int32_t* out) {
-  return guard([&] { *out = sample_accept_length(r->r, alpha, gamma); });
+  return guard([&] { *out = bk::sample_accept_length(r->r, alpha, gamma); });
 }
 int specsim_alpha_from_accept_length(double ell, int32_t gamma, double* out) {
-  return guard([&] { *out = alpha_from_accept_length(ell, gamma); });
+  return guard([&] { *out = bk::alpha_from_accept_length(ell, gamma); });
 }
 int specsim_current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
                           double trained_samples, double* out) {
   return guard([&] {
     if (!out) throw std::invalid_argument("null output");
-    *out = current_alpha(alpha_start, alpha_ceiling, tau_samples, trained_samples);
+    *out = bk::current_alpha(alpha_start, alpha_ceiling, tau_samples, trained_samples);
   });
 }
 int specsim_split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval) {

@@ -4,7 +4,7 @@
 // accepted-token hidden states are packed on the serving stream into a device
 // staging segment, copied D2H on the capture stream into a pinned host
 // segment (two segments, double-buffered), and flushed by a writer thread to
-// "TIDESIG1" shard files (format in include/specsim/draft_trainer.hpp).
+// "TIDESIG1" shard files (format in proj/include/specsim/draft_trainer.hpp).
 // load_shards() is the training side's reader into the HBM ring.
 #include <condition_variable>
 #include <cstdio>

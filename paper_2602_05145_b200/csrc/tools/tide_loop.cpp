@@ -35,8 +35,49 @@
 #include <vector>
 
 #include "specsim/draft_trainer.hpp"
+#include "specsim_draft_trainer.h"
 
 using namespace specsim;
+
+namespace {
+// The reference's Rng / accept-length model (rng.hpp:13-39,
+// perf_model.cpp:171-177, 213-224) through the library's C ABI: the C++
+// header does not redeclare those reference names.
+void ok(int status) {
+  if (status != SPECSIM_OK) throw std::runtime_error(specsim_last_error());
+}
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) { ok(specsim_rng_create(seed, &r_)); }
+  ~Rng() { specsim_rng_destroy(r_); }
+  Rng(const Rng&) = delete;
+  Rng& operator=(const Rng&) = delete;
+  double uniform() {
+    double u = 0;
+    ok(specsim_rng_uniform(r_, &u));
+    return u;
+  }
+  double normal(double mean, double sd) {
+    double v = 0;
+    ok(specsim_rng_normal(r_, mean, sd, &v));
+    return v;
+  }
+  specsim_rng* get() { return r_; }
+
+ private:
+  specsim_rng* r_ = nullptr;
+};
+int sample_accept_length(Rng& rng, double alpha, int gamma) {
+  int32_t k = 0;
+  ok(specsim_sample_accept_length(rng.get(), alpha, gamma, &k));
+  return k;
+}
+double alpha_from_accept_length(double ell, int gamma) {
+  double a = 0;
+  ok(specsim_alpha_from_accept_length(ell, gamma, &a));
+  return a;
+}
+}  // namespace
 
 namespace {
 

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "attention.h"
+#include "bookkeeping.h"
 #include "common.h"
 #include "handles.h"
 #include "gemm.h"
@@ -504,7 +505,7 @@ class DraftTrainerImpl {
     for (unsigned w = 0; w < nt; ++w)
       th.emplace_back([=] {
         for (long long j = w; j < nblk; j += nt) {
-          Rng rng(seed_base + (static_cast<uint64_t>(pidx) << 32) + static_cast<uint64_t>(j));
+          bk::Rng rng(seed_base + (static_cast<uint64_t>(pidx) << 32) + static_cast<uint64_t>(j));
           const long long e0 = j << 20, e1 = std::min(n, e0 + (1ll << 20));
           for (long long e = e0; e < e1; ++e) out[e] = static_cast<float>(rng.normal(0.0, 0.02));
         }
@@ -1572,6 +1573,34 @@ int specsim_trainer_region(specsim_trainer* t, int end, double* ms) {
       SPECSIM_CUDA(cudaEventElapsedTime(&v, im.ev_region[0], im.ev_region[1]));
       if (ms) *ms = v;
     }
+  });
+}
+
+int specsim_trainer_read_rows(const specsim_trainer* t, const char* name, void* host_out,
+                              int64_t cap_elems, int64_t* n_elems) {
+  return guard([&] {
+    auto& im = impl_of(t);
+    const std::string nm = name ? name : "";
+    const void* src = nullptr;
+    size_t esz = 4;
+    long long n = im.KT;
+    if (nm == "u") src = im.u;
+    else if (nm == "y") src = im.y;
+    else if (nm == "m") src = im.m;
+    else if (nm == "argmax") src = im.argmax;
+    else if (nm == "lse") src = im.lse;
+    else if (nm == "F") {
+      src = im.F;
+      esz = 2;
+      n = im.T * im.W3;
+    } else
+      throw std::invalid_argument("unknown row buffer '" + nm + "'");
+    if (n_elems) *n_elems = n;
+    if (!host_out) return;
+    if (cap_elems < n) throw std::invalid_argument("host buffer too small");
+    DeviceGuard dg(im.device);
+    SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+    SPECSIM_CUDA(cudaMemcpy(host_out, src, esz * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
   });
 }
 

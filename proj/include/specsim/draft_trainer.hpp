@@ -1,67 +1,71 @@
 // C++ API of the B200-native TIDE draft-training hot path.
 //
-// Namespace, error taxonomy (ConfigError vs std::invalid_argument,
-// errors.hpp:8-13) and the seeded Rng semantics (rng.hpp:13-39) follow the
-// reference; the classes implement the seams SPEC.md describes but the
+// Lives where the reference keeps its public headers (proj/include/specsim/)
+// so it drops in next to errors.hpp / rng.hpp / perf_model.hpp /
+// workload.hpp: it defines no name those headers define.  ConfigError is the
+// reference's own class (errors.hpp:10) whenever that header is reachable;
+// the reference's Rng and perf_model functions (rng.hpp:13,
+// perf_model.hpp:54-80) are neither declared nor exported here (the library
+// keeps its bit-exact restatement internal, behind hidden visibility, and
+// exposes it only through the C ABI's specsim_rng_* / specsim_*accept*
+// functions).  The classes implement the seams SPEC.md describes but the
 // reference never implemented: the signal buffer (SPEC.md:237-241, 267-275,
 // 341-344) and the trainer actor train(job) -> TrainingOutcome
-// (SPEC.md:380-405).  The C ABI in ../specsim_draft_trainer.h wraps these.
+// (SPEC.md:380-405).  The C ABI in include/specsim_draft_trainer.h wraps them.
 #pragma once
 
 #include <cstdint>
 #include <deque>
 #include <memory>
-#include <random>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
-namespace specsim {
+#if defined(__GNUC__)
+#define SPECSIM_CXX_API __attribute__((visibility("default")))
+#else
+#define SPECSIM_CXX_API
+#endif
 
 // ---------------------------------------------------------------- errors
-// The reference's split (proj/include/specsim/errors.hpp:8-13):
-// std::invalid_argument = domain error (CLI exit 1), ConfigError =
-// configuration error (CLI exit 2); device failures have their own types.
+// The reference's split (errors.hpp:8-13): std::invalid_argument = domain
+// error (CLI exit 1), ConfigError = configuration error (CLI exit 2).  The
+// reference's header is used when it is on the include path (installed next
+// to this file, or proj/include of the reference on -I); otherwise the same
+// single-class definition stands in, token for token, so both spellings are
+// one type (one typeinfo name) across the library boundary.
+#if __has_include(<specsim/errors.hpp>)
+#pragma GCC visibility push(default)
+#include <specsim/errors.hpp>
+#pragma GCC visibility pop
+#else
+#pragma GCC visibility push(default)
+namespace specsim {
 class ConfigError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
-class CudaError : public std::runtime_error {
+}  // namespace specsim
+#pragma GCC visibility pop
+#endif
+
+namespace specsim {
+
+// Device failures have their own types (C ABI status 3 / 4).
+class SPECSIM_CXX_API CudaError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
-class NcclError : public std::runtime_error {
+class SPECSIM_CXX_API NcclError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
 
-// ------------------------------------------------------------------ Rng
-// Seeded mt19937_64 with hand-rolled conversions so a seed reproduces the
-// same stream as the reference's specsim::Rng.
-class Rng {
- public:
-  explicit Rng(uint64_t seed) : eng_(seed) {}
-  uint64_t next_u64() { return eng_(); }
-  double uniform();                       // [0, 1), 53 bits
-  double normal(double mean, double sd);  // Box-Muller, cosine branch
-  long long geometric(double mean);       // {1, 2, ...}
-
- private:
-  std::mt19937_64 eng_;
-};
-
-double expected_accept_length(double alpha, int gamma);
-int sample_accept_length(Rng& rng, double alpha, int gamma);
-double alpha_from_accept_length(double ell, int gamma);
-// workload.cpp:41-47: alpha(n) = ceiling - (ceiling - start) exp(-n / tau),
-// clamped to [0, 1] (the reference's analytic stand-in for alpha_eval).
-double current_alpha(double alpha_start, double alpha_ceiling, double tau_samples,
-                     double trained_samples);
 // oldest floor(9n/10) samples train, the rest evaluate.
-void split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
+SPECSIM_CXX_API void split_train_eval(int64_t n, int64_t* n_train, int64_t* n_eval);
 
-struct SignalGeometry {
+struct SPECSIM_CXX_API SignalGeometry {
   int hidden_dim = 0;
   int layers_tapped = 3;
   int bytes_per_element = 2;
@@ -76,12 +80,13 @@ struct SynthCapture {
   std::vector<int32_t> accept_lengths;
   double alpha_s = 0;
 };
-void synth_capture(uint64_t seed, int64_t index, int length, int vocab, int hidden, int layers,
-                   double alpha, int gamma, int32_t* ids, uint16_t* features,
-                   int32_t* accept_lengths, int32_t* n_steps, double* alpha_s);
+SPECSIM_CXX_API void synth_capture(uint64_t seed, int64_t index, int length, int vocab,
+                                   int hidden, int layers, double alpha, int gamma, int32_t* ids,
+                                   uint16_t* features, int32_t* accept_lengths, int32_t* n_steps,
+                                   double* alpha_s);
 
 // ---------------------------------------------------- hidden-state buffer
-class HiddenStateBuffer {
+class SPECSIM_CXX_API HiddenStateBuffer {
  public:
   struct Stats {
     int64_t records = 0, bytes = 0, flushes = 0, cumulative_bytes = 0, samples = 0,
@@ -154,7 +159,7 @@ class HiddenStateBuffer {
 };
 
 // ------------------------------------------------------------- trainer
-struct DraftShape {
+struct SPECSIM_CXX_API DraftShape {
   int hidden = 0, vocab = 0, seq_len = 0, n_heads = 0, n_kv_heads = 0, head_dim = 0, ffn = 0,
       layers_tapped = 3, micro_batch = 1;
   float rms_eps = 1e-5f;
@@ -176,10 +181,10 @@ struct DpBucket {
   long long off, n;
 };
 // Buckets in the order the backward finalises them (they tile the registry).
-std::vector<DpBucket> dp_buckets(const DraftShape& shape);
+SPECSIM_CXX_API std::vector<DpBucket> dp_buckets(const DraftShape& shape);
 // True when every bucket splits into `world` shards of whole 8-element groups
 // (the ZeRO-1 path; otherwise the trainer all-reduces).
-bool zero_shardable(const std::vector<DpBucket>& buckets, int world);
+SPECSIM_CXX_API bool zero_shardable(const std::vector<DpBucket>& buckets, int world);
 
 struct StepResult {
   double loss = 0;
@@ -223,7 +228,7 @@ struct TrainingOutcome {
 // A request's rows may be split over several records (one per verify step,
 // interleaved with other requests of the batch); end_sample() writes its
 // final alpha label.  load_shards() regroups records per sample.
-class SignalCapture {
+class SPECSIM_CXX_API SignalCapture {
  public:
   struct Stats {
     int64_t records = 0, bytes = 0, flushes = 0, cumulative_bytes = 0;  // SPEC accounting
@@ -261,11 +266,12 @@ class SignalCapture {
 // Loads shard files (in order) into the device ring: records are regrouped
 // per sample_id (first-appearance order) and each sample appended
 // contiguously.  Returns the number of samples loaded.
-int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& paths);
+SPECSIM_CXX_API int64_t load_shards(HiddenStateBuffer& buf,
+                                    const std::vector<std::string>& paths);
 
 class DraftTrainerImpl;
 
-class DraftTrainer {
+class SPECSIM_CXX_API DraftTrainer {
  public:
   DraftTrainer(const DraftShape& shape, const AdamWConfig& opt, uint64_t seed, int rank,
                int world, const uint8_t* nccl_id, int device);
@@ -290,7 +296,7 @@ class DraftTrainer {
 // gate, sample store, and maybe_trigger_training -- the caller of train(job)
 // -- with the deploy-if-improved gate.  Host logic in double precision, same
 // operation order as the SPEC recurrences (bit-reproducible).
-struct ControllerConfig {
+struct SPECSIM_CXX_API ControllerConfig {
   double lambda_short = 0.9;  // SPEC adapt_control DESIGN DECISIONS defaults
   double lambda_long = 0.99;
   double epsilon = 0.05;
@@ -319,7 +325,7 @@ struct TriggerDecision {
   int32_t action = -1;     // 1 deploy, 0 tie (neither), -1 reject / not triggered
 };
 
-class AdaptiveController {
+class SPECSIM_CXX_API AdaptiveController {
  public:
   explicit AdaptiveController(const ControllerConfig& cfg);
   // Warm-up: the first n_init observations initialise both EMAs to their mean

@@ -70,6 +70,63 @@ def test_attention_fwd_bwd(B, S, nh, nkv, hd):
     assert rel(g[:, Q + KV:], dQKV[:, Q + KV:]) < 2e-2
 
 
+def ref_by_head(qkv, dO, S, nh, nkv, hd):
+    """float64 reference one head at a time (B = 1): S x S score matrices only,
+    so S = 4096 with 64 heads fits in host memory."""
+    Q, KV, rep = nh * hd, nkv * hd, nh // nkv
+    x = qkv.astype(np.float64)
+    do_all = dO.astype(np.float64)
+    O = np.zeros((S, Q))
+    LSE = np.zeros((nh, S))
+    dQKV = np.zeros((S, Q + 2 * KV))
+    mask = np.triu(np.ones((S, S), bool), 1)
+    for h in range(nh):
+        kv = h // rep
+        q = x[:, h * hd:(h + 1) * hd]
+        k = x[:, Q + kv * hd:Q + (kv + 1) * hd]
+        v = x[:, Q + KV + kv * hd:Q + KV + (kv + 1) * hd]
+        sc = np.where(mask, -np.inf, q @ k.T / np.sqrt(hd))
+        mx = sc.max(-1, keepdims=True)
+        p = np.exp(sc - mx)
+        l = p.sum(-1, keepdims=True)
+        p /= l
+        o = p @ v
+        O[:, h * hd:(h + 1) * hd] = o
+        LSE[h] = (mx + np.log(l))[:, 0]
+        do = do_all[:, h * hd:(h + 1) * hd]
+        ds = p * (do @ v.T - (do * o).sum(-1, keepdims=True)) / np.sqrt(hd)
+        dQKV[:, h * hd:(h + 1) * hd] = ds @ k
+        dQKV[:, Q + kv * hd:Q + (kv + 1) * hd] += ds.T @ q
+        dQKV[:, Q + KV + kv * hd:Q + KV + (kv + 1) * hd] += p.T @ do
+    return O, LSE, dQKV
+
+
+# The large configurations' head geometry at their full sequence lengths: C2
+# (S 2048, 32 q / 8 kv heads, GQA group 4: 16 key blocks per query block) and
+# C4 / C5 (S 4096, 64 q / 8 kv heads, GQA group 8: 32 key blocks).
+@pytest.mark.parametrize("S,nh,nkv", [(2048, 32, 8), (4096, 64, 8)])
+def test_attention_large_configs(S, nh, nkv):
+    hd = 128
+    rng = np.random.default_rng(S + nh)
+    NQ = (nh + 2 * nkv) * hd
+    qkv_bits, qkv = rand_bf16(rng, (S, NQ))
+    do_bits, do = rand_bf16(rng, (S, nh * hd))
+    o = np.zeros((S, nh * hd), np.uint16)
+    lse = np.zeros((nh, S), np.float32)
+    dqkv = np.zeros((S, NQ), np.uint16)
+    _lib.call("specsim_debug_attention", 1, S, nh, nkv, hd, _lib.ptr(qkv_bits), _lib.ptr(do_bits),
+              _lib.ptr(o), _lib.ptr(lse), _lib.ptr(dqkv))
+    O, LSE, dQKV = ref_by_head(qkv, do, S, nh, nkv, hd)
+    assert rel(bf16_bits_to_f32(o), O) < 1e-2
+    np.testing.assert_allclose(lse, LSE, rtol=1e-4, atol=1e-3)
+    g = bf16_bits_to_f32(dqkv)
+    Q, KV = nh * hd, nkv * hd
+    errs = [rel(g[:, :Q], dQKV[:, :Q]), rel(g[:, Q:Q + KV], dQKV[:, Q:Q + KV]),
+            rel(g[:, Q + KV:], dQKV[:, Q + KV:])]
+    print(S, nh, nkv, "dq/dk/dv rel", errs)
+    assert max(errs) < 2e-2
+
+
 def test_attention_rejects_bad_shapes():
     z = np.zeros(16, np.uint16)
     f = np.zeros(16, np.float32)

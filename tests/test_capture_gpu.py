@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 
 def read_shard(path):
-    """Reader of the format documented in include/specsim/draft_trainer.hpp."""
+    """Reader of the format documented in proj/include/specsim/draft_trainer.hpp."""
     b = open(path, "rb").read()
     magic, ver, layers, hidden, bpe, n_rec, payload = struct.unpack_from("<8sIIIIQQ", b, 0)
     assert magic == b"TIDESIG1" and ver == 1 and bpe == 2 and payload + 40 == len(b)

@@ -4,15 +4,17 @@ weights (initialisation is bit-exact), then loss, every parameter gradient,
 the AdamW update, eval top-1 and train(job) outcome.
 
 Tolerances (fp32 accumulation-order + bf16 rounding-point noise; the oracle
-rounds at the same points, oracle.h): loss rel <= 2e-3; grads rel-Frobenius
-<= 1e-2; post-AdamW |dp_gpu - dp_cpu| <= 0.05 lr on >= 99% of elements whose
-oracle gradient is well determined; token gather / mask / valid counts exact.
+rounds at the same points, oracle.h) are tests/_parity.py's: loss rel <= 2e-3;
+grads rel-Frobenius <= 1e-2; post-AdamW |dp_gpu - dp_cpu| <= 0.05 lr on >=
+99.9% of elements whose oracle gradient is well determined; token gather
+(u / y / m / F rows) bit-exact; top-1 exact on rows with logit margin > 1e-2.
 """
 import numpy as np
 import pytest
 
 import oracle
 from paper_2602_05145_b200 import _lib, api
+from _parity import LARGE_LOGIT_TOL, oracle_state, step_and_compare
 
 pytestmark = pytest.mark.gpu
 SEED = 20260217
@@ -84,36 +86,17 @@ def test_step_matches_oracle(name):
     c = SHAPES[name]
     S, B = c["seq_len"], c["micro_batch"]
     lens = [S + 2] * (B - 2) + [S // 2 + 3, S + 40]
-    c, shp, tr, buf, ids, (F, u, y, m) = setup(name, lens, n_present=B - 1 if B > 2 else None)
-    layout, total = oracle.param_layout(shp)
+    c, shp, tr, buf, ids, _ = setup(name, lens, n_present=B - 1 if B > 2 else None)
+    caps = [oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+            for i, L in enumerate(lens[:len(ids)])]
+    samples = [(cp["ids"], cp["features"]) for cp in caps]
     P = oracle.init_params(shp, SEED)
     E = oracle.init_embedding(shp, SEED)
     Mst, Vst = np.zeros_like(P), np.zeros_like(P)
-    report = {}
+    well = {}
     for k in (1, 2):
-        P0 = P.copy()
-        out, grads = oracle.train_step(shp, HP, k, P, Mst, Vst, E, F, u, y, m, round_bf16=True)
-        r = tr.step(buf, ids)
-        assert r["valid_tokens"] == int(m.sum()) == out.valid
-        assert r["positions"] == B * S
-        assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
-        assert abs(r["top1_correct"] - out.top1) <= max(2, 0.01 * out.valid)
-        for nm, rr, cc, off in layout:
-            g_gpu = tr.get_grad(nm).reshape(-1)
-            g_cpu = grads[off:off + rr * cc]
-            e = rel(g_gpu, g_cpu)
-            report[(k, nm)] = e
-            assert e <= 1e-2, (k, nm, e)
-            p_gpu = tr.get_param(nm).reshape(-1)
-            d_gpu = p_gpu - P0[off:off + rr * cc]
-            d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
-            well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
-            if well.sum() > 0:
-                ok = np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]
-                assert ok.mean() >= 0.99, (k, nm, ok.mean())
-            # keep both sides on identical weights for the next step
-            tr.set_param(nm, P[off:off + rr * cc].reshape(rr, cc))
-    print("grad rel errors:", {f"{k}:{n}": round(v, 5) for (k, n), v in report.items()})
+        rep = step_and_compare(tr, buf, ids, shp, samples, P, Mst, Vst, E, k, HP, well=well)
+        print(name, k, rep)
     tr.close()
     buf.close()
 
@@ -308,7 +291,8 @@ def test_step_matches_oracle_at_bench_model_dims():
     128, FFN 14336; 818.9 M parameters) on a short batch (S 128, B 2: one full
     sample and one masked tail) so the CPU oracle finishes in seconds.  The
     oracle starts from the trainer's own weights (init is bit-exact, tested
-    above at small shapes)."""
+    above at small shapes).  The full-length (S 2048) step is in
+    tests/test_parity_large_gpu.py."""
     c = dict(api.CONFIGS["C2"], seq_len=128, micro_batch=2)
     shp = oshape(c)
     tr = api.DraftTrainer(c, lr=HP[0], betas=(HP[1], HP[2]), eps=HP[3], weight_decay=HP[4],
@@ -320,30 +304,11 @@ def test_step_matches_oracle_at_bench_model_dims():
         cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
         buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
         samples.append((cap["ids"], cap["features"]))
-    F, u, y, m = oracle.gather_batch(shp, samples)
-    layout, total = oracle.param_layout(shp)
-    P = np.zeros(total, np.float32)
-    for nm, rr, cc, off in layout:
-        P[off:off + rr * cc] = tr.get_param(nm).reshape(-1)
-    E = tr.get_embedding()
-    P0 = P.copy()
+    _, P, E = oracle_state(tr, shp)
     Mst, Vst = np.zeros_like(P), np.zeros_like(P)
-    out, grads = oracle.train_step(shp, HP, 1, P, Mst, Vst, E, F, u, y, m, round_bf16=True)
-    r = tr.step(buf, [0, 1])
-    assert r["valid_tokens"] == out.valid == int(m.sum())
-    assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
-    errs = {}
-    for nm, rr, cc, off in layout:
-        g_cpu = grads[off:off + rr * cc]
-        e = rel(tr.get_grad(nm).reshape(-1), g_cpu)
-        errs[nm] = round(e, 5)
-        assert e <= 1e-2, (nm, e)
-        d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
-        d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
-        well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
-        ok = np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]
-        assert ok.mean() >= 0.99, (nm, ok.mean())
-    print("C2-dims grad rel errors:", errs)
+    rep = step_and_compare(tr, buf, [0, 1], shp, samples, P, Mst, Vst, E, 1, HP,
+                           sync_weights=False, logit_tol=LARGE_LOGIT_TOL)
+    print("C2-dims:", rep)
     tr.close()
     buf.close()
 

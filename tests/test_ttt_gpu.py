@@ -5,15 +5,17 @@ the cache entries of passes 1..j), decay-weighted loss.  The oracle's unroll
 is itself pinned against a SpecForge-layout torch autograd restatement
 (tests/test_oracle_vs_torch.py::test_ttt_step_matches_torch).
 
-Tolerances as tests/test_trainer_gpu.py: loss rel <= 2e-3, every gradient
-rel-Frobenius <= 1e-2, AdamW update within 0.05 lr on >= 99% of well-determined
-elements, valid counts exact.
+Tolerances as tests/_parity.py: loss rel <= 2e-3, every gradient
+rel-Frobenius <= 1e-2, AdamW update within 0.05 lr on >= 99.9% of
+well-determined elements, gather of every unroll slice bit-exact, top-1 exact
+on rows with logit margin > 1e-2.
 """
 import numpy as np
 import pytest
 
 import oracle
 from paper_2602_05145_b200 import api
+from _parity import step_and_compare
 
 pytestmark = pytest.mark.gpu
 SEED = 20260217
@@ -28,6 +30,10 @@ CASES = {
     "s256_k4": dict(hidden=256, vocab=2048, seq_len=256, n_heads=4, n_kv_heads=2, head_dim=64,
                     ffn=512, micro_batch=2, rms_eps=1e-5, rope_theta=10000.0, ttt_steps=4,
                     ttt_decay=0.7),
+    # GQA group 8 (C4 / C5 head geometry: 8 query heads per KV head) with Q != H:
+    # the cache-entry kernel's rep = 8 instantiation
+    "gqa8_k3": dict(hidden=512, vocab=2048, seq_len=256, n_heads=8, n_kv_heads=1, head_dim=128,
+                    ffn=1024, micro_batch=2, rms_eps=1e-6, rope_theta=1000000.0, ttt_steps=3),
 }
 
 
@@ -65,34 +71,13 @@ def test_ttt_step_matches_oracle(name):
     n = B - 1 if B > 2 else B
     tr, buf, samples, ids = setup(c, lens, n)
     shp = oshape(c)
-    F, u, y, m = oracle.gather_batch(shp, samples)
-    layout, total = oracle.param_layout(shp)
     P = oracle.init_params(shp, SEED)
     E = oracle.init_embedding(shp, SEED)
     Mst, Vst = np.zeros_like(P), np.zeros_like(P)
-    T = B * S
-    report = {}
+    well = {}
     for k in (1, 2):
-        P0 = P.copy()
-        out, grads = oracle.train_step(shp, HP, k, P, Mst, Vst, E, F, u, y, m, round_bf16=True)
-        r = tr.step(buf, ids)
-        assert r["valid_tokens"] == int(m[:T].sum()) == out.valid
-        assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss), (r["loss"], out.loss)
-        assert abs(r["top1_correct"] - out.top1) <= max(2, 0.01 * out.valid)
-        for nm, rr, cc, off in layout:
-            g_gpu = tr.get_grad(nm).reshape(-1)
-            g_cpu = grads[off:off + rr * cc]
-            e = rel(g_gpu, g_cpu)
-            report[(k, nm)] = e
-            assert e <= 1e-2, (k, nm, e)
-            d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
-            d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
-            well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
-            if well.sum() > 0:
-                ok = np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]
-                assert ok.mean() >= 0.99, (k, nm, ok.mean())
-            tr.set_param(nm, P[off:off + rr * cc].reshape(rr, cc))
-    print(name, "grad rel errors:", {f"{k}:{n}": round(v, 5) for (k, n), v in report.items()})
+        rep = step_and_compare(tr, buf, ids, shp, samples, P, Mst, Vst, E, k, HP, well=well)
+        print(name, k, rep)
     tr.close()
     buf.close()
 
@@ -110,7 +95,8 @@ def test_ttt_fused_adamw_and_eval():
     P = oracle.init_params(shp, SEED)
     E = oracle.init_embedding(shp, SEED)
     z = np.zeros_like(P)
-    out, _ = oracle.train_step(shp, HP, 1, P, z.copy(), z.copy(), E, F, u, y, m, round_bf16=True)
+    out, grads = oracle.train_step(shp, HP, 1, P, z.copy(), z.copy(), E, F, u, y, m,
+                                   round_bf16=True)
     r = tr.step(buf, ids)
     assert abs(r["loss"] - out.loss) <= 2e-3 * abs(out.loss)
     layout, _ = oracle.param_layout(shp)
@@ -118,7 +104,9 @@ def test_ttt_fused_adamw_and_eval():
     for nm, rr, cc, off in layout:
         d_gpu = tr.get_param(nm).reshape(-1) - P0[off:off + rr * cc]
         d_cpu = P[off:off + rr * cc] - P0[off:off + rr * cc]
-        assert (np.abs(d_gpu - d_cpu) <= 0.05 * HP[0]).mean() >= 0.99, nm
+        g_cpu = grads[off:off + rr * cc]
+        well = np.abs(g_cpu) > 0.05 * np.abs(g_cpu).std() + 1e-12
+        assert (np.abs(d_gpu - d_cpu)[well] <= 0.05 * HP[0]).mean() >= 0.999, nm
     # eval = pass 0 of the updated model
     shp1 = oshape(c, ttt=1)
     F1, u1, y1, m1 = oracle.gather_batch(shp1, samples)
