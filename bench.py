@@ -28,10 +28,12 @@ import time
 
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-# NCCL prints its version banner on stdout at communicator init when
-# NCCL_DEBUG is VERSION; keep stdout to the one JSON line of the contract
-if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-    os.environ["NCCL_DEBUG"] = "WARN"
+# NCCL communicator-init lines (rank / nranks / transport, NVLS) go to stderr,
+# where the driver can count the ranks; stdout stays the one JSON line of the
+# contract (NCCL's default debug sink is stdout)
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 WORKLOAD = "C2"
 SEED = 20260217
@@ -172,11 +174,17 @@ def run_reference(args):
         oracle.train_step(shp, hp, warm + k + 1, P, Mst, Vst, E, *batch)
     dt = time.perf_counter() - t0
     tps = steps * seq / dt
+    conf = config_block(args, cfg)
+    # what this arm actually times: one sequence of `seq` positions per step
+    # at the workload's model shape (the whole workload would take hours)
+    conf.update(micro_batch=1, seq_len=seq, global_batch=1, tokens_per_rank_step=seq,
+                workload_micro_batch=cfg["micro_batch"], workload_seq_len=cfg["seq_len"],
+                parallelism="host CPU (rank 0 only)")
     line = dict(impl="reference", metric="draft-train tokens/sec", value=round(tps, 3),
                 unit="tokens/s", n_gpus=args.gpus, steps=steps, warmup=warm,
                 ms_per_step=round(1e3 * dt / steps, 1), higher_is_better=True,
                 scaling=scaling_of(args), vs_baseline=None, dtype="f32 (bf16-rounded operands)", data="synthetic",
-                config=config_block(args, cfg),
+                config=conf, host_cpu=cpu_model(),
                 cpu_baseline=dict(value=round(tps, 3), unit="tokens/s", cores=oracle.num_threads(),
                                   kind="port",
                                   sample=f"{steps} oracle steps of 1 sequence x {seq} positions at "
@@ -188,6 +196,19 @@ def run_reference(args):
                      "repo's C restatement (oracle/) of the same step on the host CPU")
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_model():
+    """lscpu model name and logical core count of the host."""
+    name = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for l in out.splitlines():
+            if l.startswith("Model name"):
+                name = l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return dict(model=name, logical_cpus=os.cpu_count())
 
 
 MODEL_SHAPE = {"C1": "tiny draft head", "C2": "Llama-3.1-8B shape", "C4": "Qwen3-32B shape",
@@ -211,6 +232,7 @@ def scaling_of(args):
 
 
 def config_block(args, cfg):
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     K = cfg.get("ttt_steps", 1)
     ttt = (f", training-time-test unroll {K} passes (loss weights 0.8^j)" if K > 1 else "")
     name = args.config + (f"-TTT{K}" if K > 1 else "")
@@ -221,9 +243,9 @@ def config_block(args, cfg):
                          f"seq {cfg['seq_len']}){ttt}, bf16 GEMMs, synthetic captured hidden states",
                 **extra,
                 hidden=cfg["hidden"], vocab=cfg["vocab"], seq_len=cfg["seq_len"],
-                micro_batch=cfg["micro_batch"], global_batch=cfg["micro_batch"] * args.gpus,
+                micro_batch=cfg["micro_batch"], global_batch=cfg["micro_batch"] * world,
                 tokens_per_rank_step=cfg["micro_batch"] * cfg["seq_len"],
-                parallelism=f"dp{args.gpus}",
+                parallelism=f"dp{world}",
                 l2="inputs larger than L2 (multi-GB per-step working set; no flush needed)")
 
 
@@ -496,7 +518,7 @@ def run_ours(args):
             dtc = time.perf_counter() - t0
             line["cpu_baseline"] = dict(
                 value=round(seq / dtc, 3), unit="tokens/s", cores=oracle.num_threads(),
-                kind="port",
+                kind="port", host_cpu=cpu_model(),
                 sample=f"1 oracle step (fwd+bwd+AdamW, all {args.config} params) on 1 sequence x "
                        f"{seq} positions; {dtc:.1f} s")
         except Exception as e:  # the baseline is reported, never required
@@ -511,8 +533,34 @@ def run_ours(args):
     return 0
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(args):
+    """--gpus N > 1 without a torchrun environment: re-exec this script under
+    torch.distributed.run with N ranks on this node (one per GPU); the exit
+    code is the launcher's.  Under torchrun, WORLD_SIZE must equal --gpus."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1 and args.impl == "ours":
+        return launch_ranks(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}: launch one "
+                         "rank per GPU (torchrun --nproc-per-node N ... --gpus N)")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -16,10 +16,18 @@ const Api& api() {
   static std::string err;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) {
-      if (const char* p = std::getenv("SPECSIM_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+    // an explicit SPECSIM_NCCL_LIB wins (deployment pinning, or the tests'
+    // in-process stand-in); then a copy the host framework already loaded;
+    // then the loader search path
+    void* h = nullptr;
+    if (const char* p = std::getenv("SPECSIM_NCCL_LIB")) {
+      h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+      if (!h) {
+        err = std::string("cannot load SPECSIM_NCCL_LIB=") + p + ": " + dlerror();
+        return;
+      }
     }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
       err = std::string("cannot load libnccl.so.2: ") + dlerror();

@@ -22,8 +22,8 @@ struct Api {
   const char* (*GetErrorString)(ncclResult_t);
 };
 
-// Throws NcclError if no libnccl.so.2 can be found.  Prefers an already
-// loaded copy, then $SPECSIM_NCCL_LIB, then the loader search path.
+// Throws NcclError if no libnccl.so.2 can be found.  Prefers
+// $SPECSIM_NCCL_LIB, then an already loaded copy, then the loader search path.
 const Api& api();
 
 }  // namespace nccl

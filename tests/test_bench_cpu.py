@@ -52,6 +52,41 @@ def test_reference_arm_line():
     assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["higher_is_better"] is True and d["scaling"] == "weak"
+    # the line states what was actually timed: 1 sequence x 64 positions
+    c = d["config"]
+    assert c["micro_batch"] == 1 and c["seq_len"] == 64 and c["tokens_per_rank_step"] == 64
+    assert c["workload_seq_len"] == api.CONFIGS["C1"]["seq_len"]
+    assert "model" in d["host_cpu"]
+
+
+def test_multi_gpu_request_spawns_ranks(monkeypatch):
+    """--gpus N without a torchrun environment re-executes under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous); a WORLD_SIZE
+    that disagrees with --gpus is an error, not a silent 1-rank run."""
+    seen = {}
+
+    def fake_run(cmd, *a, **k):
+        seen["cmd"] = cmd
+        return types.SimpleNamespace(returncode=0)
+
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    assert bench.main() == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    with pytest.raises(SystemExit):
+        bench.main()
+
+
+def test_config_block_reports_the_launched_world(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "8")
+    a = _args(gpus=8)
+    blk = bench.config_block(a, bench.workload_cfg(a, api))
+    assert blk["parallelism"] == "dp8" and blk["global_batch"] == 8 * api.CONFIGS["C2"]["micro_batch"]
 
 
 @pytest.mark.gpu
