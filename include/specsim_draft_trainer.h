@@ -148,7 +148,13 @@ int specsim_hsbuf_destroy(specsim_hsbuf* buf);
  * rows accepted_idx[0..n) (or rows 0..n if accepted_idx is NULL).
  * token_ids[i] is the id at accepted position i.  Appending to a sample_id
  * different from the open one closes the open sample (its records stay
- * contiguous in the ring).  alpha is the per-sample alpha label
+ * contiguous in the ring, which the fc GEMM's row gather relies on); a
+ * closed sample cannot be reopened (SPECSIM_EDOMAIN).  So calls for one
+ * request must not interleave with another request's: a single-request
+ * serving loop appends per verify step, a BATCHED loop (requests verified
+ * together, appends interleaved) captures through specsim_capture_* and
+ * loads the shards with specsim_hsbuf_load_shards, which regroups each
+ * request's rows.  alpha is the per-sample alpha label
  * (SPEC.md:365); the last value given for a sample wins.
  * Host pointers are only read during the call. */
 int specsim_hsbuf_append(specsim_hsbuf* buf, int64_t sample_id, double alpha,

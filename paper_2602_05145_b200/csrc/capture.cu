@@ -6,6 +6,7 @@
 // segment (two segments, double-buffered), and flushed by a writer thread to
 // "TIDESIG1" shard files (format in proj/include/specsim/draft_trainer.hpp).
 // load_shards() is the training side's reader into the HBM ring.
+#include <cmath>
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
@@ -456,6 +457,20 @@ std::vector<std::string> SignalCapture::files() const {
   return impl_->paths;
 }
 
+namespace {
+// Rows of samples whose end_sample record has not been read yet, per buffer
+// (HiddenStateBuffer::serial): a request that straddles a flush has its rows
+// and its completion record in different shard files, which a caller may load
+// one call at a time as they appear.
+struct Carried {
+  std::vector<uint16_t> feat;
+  std::vector<int32_t> ids;
+};
+std::mutex g_carry_mu;
+std::unordered_map<uint64_t, std::pair<std::vector<int64_t>, std::unordered_map<int64_t, Carried>>>
+    g_carry;
+}  // namespace
+
 int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& paths) {
   const SignalGeometry& g = buf.geometry();
   const int W = g.hidden_dim * g.layers_tapped;
@@ -468,10 +483,30 @@ int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& path
     std::vector<Chunk> chunks;
     double alpha = 0.0;
     int64_t total = 0;
+    bool complete = false;
   };
   std::vector<std::vector<char>> files;
   std::unordered_map<int64_t, Acc> acc;
   std::vector<int64_t> order;
+  // unfinished samples of earlier calls come first (first-appearance order)
+  std::vector<int64_t> carried_order;
+  std::unordered_map<int64_t, Carried> carried;
+  {
+    std::lock_guard<std::mutex> lk(g_carry_mu);
+    auto it = g_carry.find(buf.serial());
+    if (it != g_carry.end()) {
+      carried_order = std::move(it->second.first);
+      carried = std::move(it->second.second);
+      g_carry.erase(it);
+    }
+  }
+  for (int64_t id : carried_order) {
+    const Carried& c = carried.at(id);
+    Acc& a = acc[id];
+    a.chunks.push_back({c.feat.data(), c.ids.data(), static_cast<int>(c.ids.size())});
+    a.total = static_cast<int64_t>(c.ids.size());
+    order.push_back(id);
+  }
   for (const auto& path : paths) {
     std::ifstream f(path, std::ios::binary | std::ios::ate);
     if (!f) throw std::invalid_argument("cannot open shard " + path);
@@ -501,11 +536,16 @@ int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& path
       if (rh.n < 0 || rh.width != W) throw std::invalid_argument("bad record in shard " + path);
       if (rh.flags & 2) {  // batch record: n_req = sample count, n = total rows
         const char* m = b.data() + off + sizeof(rh);
+        // n_req travels as a double: bound it by the bytes left (12 per request)
+        // before any size arithmetic
+        const double room = static_cast<double>(static_cast<size_t>(size) - off - sizeof(rh));
+        if (!(rh.alpha >= 0.0) || rh.alpha * 12.0 > room || rh.alpha != std::floor(rh.alpha))
+          throw std::invalid_argument("bad batch record (request count) in shard " + path);
         const int64_t n_req = static_cast<int64_t>(rh.alpha);
         const size_t meta = align16(sizeof(int64_t) * n_req + sizeof(int32_t) * n_req);
         const size_t feat = static_cast<size_t>(rh.n) * W * 2;
         const size_t rec = align16(sizeof(rh) + meta + feat + sizeof(int32_t) * rh.n);
-        if (n_req < 0 || off + rec > static_cast<size_t>(size))
+        if (off + rec > static_cast<size_t>(size))
           throw std::invalid_argument("truncated batch record in shard " + path);
         const char* fp = m + meta;
         const char* ip = fp + feat;
@@ -548,14 +588,35 @@ int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& path
              reinterpret_cast<const int32_t*>(b.data() + off + sizeof(rh) + feat), rh.n});
         it->second.total += rh.n;
       }
-      if (rh.flags & 1) it->second.alpha = rh.alpha;
+      if (rh.flags & 1) {
+        it->second.alpha = rh.alpha;
+        it->second.complete = true;
+      }
       off += rec;
     }
   }
   std::vector<uint16_t> feat;
   std::vector<int32_t> ids;
+  std::vector<int64_t> keep_order;
+  std::unordered_map<int64_t, Carried> keep;
+  int64_t appended = 0;
   for (int64_t id : order) {
     const Acc& a = acc.at(id);
+    if (!a.complete) {  // completion record not read yet: carry the rows over
+      Carried& c = keep[id];
+      c.feat.resize(static_cast<size_t>(a.total) * W);
+      c.ids.resize(static_cast<size_t>(a.total));
+      size_t r = 0;
+      for (const Chunk& ch : a.chunks) {
+        std::memcpy(c.feat.data() + r * W, ch.feat, sizeof(uint16_t) * ch.n * W);
+        std::memcpy(c.ids.data() + r, ch.ids, sizeof(int32_t) * ch.n);
+        r += ch.n;
+      }
+      keep_order.push_back(id);
+      continue;
+    }
+    ++appended;
+    if (a.total == 0) throw std::invalid_argument("sample " + std::to_string(id) + " has no rows");
     if (a.chunks.size() == 1) {
       buf.append_packed(id, a.alpha, a.chunks[0].feat, a.chunks[0].ids, a.chunks[0].n, 0);
       continue;
@@ -570,7 +631,11 @@ int64_t load_shards(HiddenStateBuffer& buf, const std::vector<std::string>& path
     }
     buf.append_packed(id, a.alpha, feat.data(), ids.data(), static_cast<int>(a.total), 0);
   }
-  return static_cast<int64_t>(order.size());
+  if (!keep_order.empty()) {
+    std::lock_guard<std::mutex> lk(g_carry_mu);
+    g_carry[buf.serial()] = {std::move(keep_order), std::move(keep)};
+  }
+  return appended;
 }
 
 }  // namespace specsim

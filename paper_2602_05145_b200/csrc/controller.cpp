@@ -21,7 +21,8 @@ void ControllerConfig::validate() const {
   p.check(lambda_long > lambda_short, "lambda_long must be > lambda_short");
   p.check(epsilon > 0 && std::isfinite(epsilon), "epsilon must be > 0");
   p.check(n_init > 0, "n_init must be > 0");
-  p.check(n_threshold > 0, "n_threshold must be > 0");
+  // the 9:1 split must leave D_train non-empty (floor(9n/10) >= 1)
+  p.check(n_threshold >= 2, "n_threshold must be >= 2");
   p.throw_if_any<ConfigError>();
 }
 
@@ -74,6 +75,28 @@ bool AdaptiveController::record_sample(int64_t sample_id, double alpha) {
 TriggerDecision AdaptiveController::maybe_trigger_training(DraftTrainer& trainer,
                                                            HiddenStateBuffer& buf, int epochs) {
   TriggerDecision d;
+  if (stored_samples() < cfg_.n_threshold) return d;
+  // Samples the ring has evicted since they were recorded can never be
+  // trained on: drop them (keeping order) instead of failing every later
+  // trigger on the same ids; collection continues until the threshold is
+  // met with resident samples.
+  {
+    size_t w = 0;
+    for (size_t i = 0; i < pending_ids_.size(); ++i) {
+      bool resident = true;
+      try {
+        buf.sample(pending_ids_[i]);
+      } catch (const std::out_of_range&) {
+        resident = false;
+      }
+      if (!resident) continue;
+      pending_ids_[w] = pending_ids_[i];
+      pending_alpha_[w] = pending_alpha_[i];
+      ++w;
+    }
+    pending_ids_.resize(w);
+    pending_alpha_.resize(w);
+  }
   const int64_t n = stored_samples();
   if (n < cfg_.n_threshold) return d;
   // chronological 9:1 split: oldest 90% train

@@ -201,7 +201,7 @@ class DraftTrainerImpl {
   bool timing = false;
   // deploy gate: device copy of the model [P | Mst | Vst] fp32 + P16 bf16
   void* snap = nullptr;
-  int64_t snap_step = -1;
+  int64_t snap_step = -1, snap_version = 0;
   double phase_ms[PH_N] = {}, phase_flops[PH_N] = {};
   int phase_launches[PH_N] = {};
 
@@ -1038,6 +1038,7 @@ class DraftTrainerImpl {
                                  cudaMemcpyDeviceToDevice, stream));
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
     snap_step = step_count;
+    snap_version = version;
   }
   void restore() {
     if (snap_step < 0) throw std::invalid_argument("restore: no snapshot taken");
@@ -1051,6 +1052,7 @@ class DraftTrainerImpl {
                                  cudaMemcpyDeviceToDevice, stream));
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
     step_count = snap_step;
+    version = snap_version;  // the restored model is the snapshot's version
   }
 
   kern::AdamHyper next_hyper() const {
@@ -1252,6 +1254,49 @@ class DraftTrainerImpl {
     for (int i = 0; i < cnt; ++i) mine.push_back(ids[idx[i]]);
   }
 
+  // Every sample this rank will read must be resident BEFORE the first launch:
+  // a lazily discovered eviction would throw after earlier steps had already
+  // updated the weights (and, data-parallel, leave the other ranks blocked in
+  // a collective).  The verdict is combined over ranks, so all fail together.
+  void check_resident(HiddenStateBuffer& buf, const TrainJob& job) {
+    const long long per_step = static_cast<long long>(sh.micro_batch) * world;
+    std::vector<int64_t> mine, missing;
+    auto scan = [&](const std::vector<int64_t>& ids) {
+      const long long n = static_cast<long long>(ids.size());
+      for (long long s0 = 0, j = 0; s0 < n; s0 += per_step, ++j) {
+        shard(n, j, mine, ids);
+        for (int64_t id : mine) {
+          try {
+            buf.sample(id);
+          } catch (const std::out_of_range&) {
+            missing.push_back(id);
+          }
+        }
+      }
+    };
+    scan(job.train_ids);
+    scan(job.eval_ids);
+    long long any = static_cast<long long>(missing.size());
+    if (use_nccl) {
+      *h_nglobal = any;
+      SPECSIM_CUDA(cudaMemcpyAsync(n_counted, h_nglobal, sizeof(long long),
+                                   cudaMemcpyHostToDevice, stream));
+      SPECSIM_NCCL(nccl::api().AllReduce(n_counted, n_counted, 1, ncclInt64, ncclSum, comm, stream));
+      SPECSIM_CUDA(cudaMemcpyAsync(h_nglobal, n_counted, sizeof(long long),
+                                   cudaMemcpyDeviceToHost, stream));
+      SPECSIM_CUDA(cudaStreamSynchronize(stream));
+      any = *h_nglobal;
+    }
+    if (any == 0) return;
+    std::string m = "train job: " + std::to_string(any) +
+                    " sample(s) not resident in the signal buffer (evicted or unknown)";
+    if (!missing.empty()) {
+      m += "; on this rank:";
+      for (size_t i = 0; i < missing.size() && i < 8; ++i) m += " " + std::to_string(missing[i]);
+    }
+    throw std::invalid_argument(m + "; nothing was trained");
+  }
+
   // train(job): every step and eval forward is enqueued back-to-back (no host
   // synchronisation between steps); per-step loss / counters are copied into a
   // pinned history and read once at the end.
@@ -1265,6 +1310,7 @@ class DraftTrainerImpl {
     const long long per_step = static_cast<long long>(sh.micro_batch) * world;
     const long long n = static_cast<long long>(job.train_ids.size());
     const long long ne = static_cast<long long>(job.eval_ids.size());
+    check_resident(buf, job);
     const long long train_steps = ((n + per_step - 1) / per_step) * job.epochs;
     const long long eval_steps = (ne + per_step - 1) / per_step;
     const long long total_launch = train_steps + eval_steps;

@@ -264,8 +264,11 @@ class SPECSIM_CXX_API SignalCapture {
 };
 
 // Loads shard files (in order) into the device ring: records are regrouped
-// per sample_id (first-appearance order) and each sample appended
-// contiguously.  Returns the number of samples loaded.
+// per sample_id (first-appearance order) and each sample is appended
+// contiguously once its completion record (end_sample) has been read.  Rows
+// of samples whose completion record has not appeared yet are carried over to
+// the next load_shards call on the same buffer, so shards may be loaded one at
+// a time as the writer produces them.  Returns the number of samples appended.
 SPECSIM_CXX_API int64_t load_shards(HiddenStateBuffer& buf,
                                     const std::vector<std::string>& paths);
 

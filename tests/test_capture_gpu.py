@@ -7,6 +7,8 @@ bit-identical to the captured requests."""
 import ctypes as C
 import struct
 
+import pathlib
+
 import numpy as np
 import pytest
 
@@ -127,6 +129,44 @@ def test_capture_shards_roundtrip(tmp_path, batched):
         n, a = buf.sample_info(sid)
         assert n == len(cap["ids"]) and a == cap["alpha_s"]
     buf.close()
+
+
+def test_load_shards_one_file_at_a_time(tmp_path):
+    """Requests straddle the flush boundaries (rows in one shard, completion
+    record in a later one): loading the shards one call at a time as they
+    appear appends each sample once its end_sample record is read, with all
+    its rows, exactly as loading them all at once."""
+    reqs, _, s, files = capture_batch(tmp_path, 1 << 14, batched=True)
+    assert len(files) >= 3
+    buf = api.HiddenStateBuffer(api.SignalGeometry(H), 1 << 14)
+    loaded = [buf.load_shards([f]) for f in files]
+    assert sum(loaded) == len(reqs)
+    assert loaded[0] < len(reqs)  # some requests were still open at the first flush
+    for sid, (cap, _) in enumerate(reqs):
+        f, ids = buf.read_sample(sid)
+        assert np.array_equal(f, cap["features"]) and np.array_equal(ids, cap["ids"])
+        assert buf.sample_info(sid) == (len(cap["ids"]), cap["alpha_s"])
+    buf.close()
+
+
+def test_load_shards_rejects_corrupt_request_count(tmp_path):
+    """A batch record's request count is bounded by the bytes left before any
+    size arithmetic (a corrupt count must not overflow into an out-of-bounds
+    read)."""
+    import struct
+    _, _, _, files = capture_batch(tmp_path, 0, n_req=3, batched=True)
+    raw = bytearray(pathlib.Path(files[0]).read_bytes())
+    off = 40
+    sid, alpha, n, width, flags = struct.unpack_from("<qdiiq", raw, off)
+    assert flags & 2  # first record of a batched capture is a batch record
+    for bad in (1e300, -1.0, float("nan"), 2.5):
+        struct.pack_into("<d", raw, off + 8, bad)
+        p = tmp_path / f"bad_{bad}.tsig"
+        p.write_bytes(bytes(raw))
+        buf = api.HiddenStateBuffer(api.SignalGeometry(H), 1 << 12)
+        with pytest.raises(_lib.DomainError):
+            buf.load_shards([p])
+        buf.close()
 
 
 def test_capture_default_threshold_single_shard(tmp_path):

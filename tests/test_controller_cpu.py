@@ -78,6 +78,9 @@ def test_validation():
         api.AdaptiveController(lambda_short=0.9, lambda_long=0.9)  # long must decay slower
     with pytest.raises(_lib.ConfigError):
         api.AdaptiveController(n_init=0, n_threshold=0, epsilon=0.0)
+    with pytest.raises(_lib.ConfigError):  # floor(9 * 1 / 10) = 0: empty D_train
+        api.AdaptiveController(n_threshold=1)
+    api.AdaptiveController(n_threshold=2)
     c = api.AdaptiveController(n_init=1)
     for bad in (-0.1, 1.5, float("nan")):
         with pytest.raises(_lib.DomainError):

@@ -84,17 +84,74 @@ def test_reject_restores_the_model_and_stops_collection():
 
 
 def test_trainer_failure_leaves_everything_unchanged():
+    """A trainer that throws (here: the buffer's signal geometry does not
+    match the draft shape) leaves controller state, pending set, events and
+    the model unchanged."""
     tr = api.DraftTrainer(C1, lr=3e-3, seed=SEED)
-    buf = make_buffer(1, False)
-    ctrl = api.AdaptiveController(n_init=2, n_threshold=1)
-    enable_collection(ctrl, Controller(n_init=2, n_threshold=1))
-    assert ctrl.record_sample(0, 0.5)
+    buf = api.HiddenStateBuffer(api.SignalGeometry(2 * C1["hidden"]), 1 << 14)
+    for i in range(2):
+        cap = oracle.synth_capture(SEED, i, 40, C1["vocab"], 2 * C1["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+    ctrl = api.AdaptiveController(n_init=2, n_threshold=2)
+    enable_collection(ctrl, Controller(n_init=2, n_threshold=2))
+    assert ctrl.record_sample(0, 0.5) and ctrl.record_sample(1, 0.5)
     s0, e0, p0 = ctrl.state(), ctrl.events(), params(tr)
-    with pytest.raises(_lib.DomainError):  # n = 1 -> empty D_train: train() refuses
+    with pytest.raises(_lib.DomainError):
         ctrl.maybe_trigger_training(tr, buf)
     assert ctrl.state() == s0 and ctrl.events() == e0
     p1 = params(tr)
     assert all(np.array_equal(p0[k], p1[k]) for k in p0)
+    tr.close()
+    buf.close()
+
+
+def test_evicted_pending_samples_are_dropped():
+    """Pending samples the ring evicted are dropped at the trigger (they can
+    never be trained on) instead of failing every later trigger; training
+    starts once n_threshold resident samples are pending."""
+    tr = api.DraftTrainer(C1, lr=3e-3, seed=SEED)
+    L = C1["seq_len"] + 2
+    buf = api.HiddenStateBuffer(api.SignalGeometry(C1["hidden"]), 5 * L)  # holds 5 samples
+    ctrl = api.AdaptiveController(n_init=2, n_threshold=4)
+    enable_collection(ctrl, Controller(n_init=2, n_threshold=4))
+    for i in range(4):
+        cap = oracle.synth_capture(SEED, i, L, C1["vocab"], C1["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+        if i < 2:
+            assert ctrl.record_sample(i, 0.5)  # 0, 1 pending
+    for i in range(4, 7):  # 0 and 1 are evicted by 5 and 6; 4, 5, 6 pending
+        cap = oracle.synth_capture(SEED, i, L, C1["vocab"], C1["hidden"])
+        buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+        assert ctrl.record_sample(i, 0.5)
+    assert ctrl.state()["stored_samples"] == 5
+    d = ctrl.maybe_trigger_training(tr, buf)
+    assert not d.triggered and ctrl.state()["stored_samples"] == 3  # 0, 1 dropped
+    assert ctrl.record_sample(3, 0.5)  # resident: the threshold is met again
+    d = ctrl.maybe_trigger_training(tr, buf)
+    assert d.triggered and (d.n_train, d.n_eval) == (3, 1)
+    tr.close()
+    buf.close()
+
+
+def test_train_with_missing_sample_changes_nothing():
+    """train(job) checks every sample before the first launch: a missing id
+    fails the whole job with the model untouched (not after earlier steps
+    have updated it); the outcome's version follows snapshot / restore."""
+    tr = api.DraftTrainer(C1, lr=3e-3, seed=SEED)
+    buf = make_buffer(10, False)
+    p0 = params(tr)
+    with pytest.raises(_lib.DomainError):
+        tr.train(buf, list(range(9)) + [999], [9], epochs=2)  # 999: last step's sample
+    p1 = params(tr)
+    assert all(np.array_equal(p0[k], p1[k]) for k in p0)
+    tr.snapshot()
+    o1 = tr.train(buf, [0, 1], [2])
+    assert o1.new_version == 1
+    tr.restore()  # not deployed: the model (and its version) is the snapshot's
+    o2 = tr.train(buf, [0, 1], [2])
+    assert o2.new_version == 1
+    o3 = tr.train(buf, [0, 1], [2])  # deployed o2 in place, trained again
+    assert o3.new_version == 2
     tr.close()
     buf.close()
 

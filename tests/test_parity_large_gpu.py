@@ -21,7 +21,10 @@ from _parity import LARGE_LOGIT_TOL, check_gather, oracle_state, step_and_compar
 
 pytestmark = pytest.mark.gpu
 SEED = 20260217
-HP = [1e-3, 0.9, 0.95, 1e-8, 0.0]
+# lr 1e-4 (the library default): at these widths one lr-1e-3 Adam step moves
+# the logits of the batch's targets so far that the second step's loss is
+# ~1e-4 and its relative error meaningless
+HP = [1e-4, 0.9, 0.95, 1e-8, 0.0]
 
 
 def oshape(c):
