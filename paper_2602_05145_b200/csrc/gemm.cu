@@ -152,9 +152,16 @@ GemmPlan make_plan(const Operand& A, const Operand& B, int M, int N, int K, int 
   p.cg = cg;
   const int bn_cta = BN / cg;
   // A: K-major = [M, K] rows; MN-major = [K, M] rows.  Boxes are per CTA.
-  p.map_a = A.mn_major ? make_map(A.ptr, K, M, A.ld, 64, 64) : make_map(A.ptr, M, K, A.ld, 64, BM);
-  p.map_b =
-      B.mn_major ? make_map(B.ptr, K, N, B.ld, 64, 64) : make_map(B.ptr, N, K, B.ld, 64, bn_cta);
+  // gathered operands (Args::a_rows / b_rows): the map spans the source's rows
+  const long long a_rows = A.rows > 0 ? A.rows : (A.mn_major ? K : M);
+  const long long b_rows = B.rows > 0 ? B.rows : (B.mn_major ? K : N);
+  p.map_a = A.mn_major ? make_map(A.ptr, a_rows, M, A.ld, 64, 64)
+                       : make_map(A.ptr, a_rows, K, A.ld, 64, BM);
+  p.map_b = B.mn_major ? make_map(B.ptr, b_rows, N, B.ld, 64, 64)
+                       : make_map(B.ptr, b_rows, K, B.ld, 64, bn_cta);
+  if ((extra.a_rows && !A.mn_major && M % BM) || (extra.a_rows && A.mn_major && K % 64) ||
+      (extra.b_rows && B.mn_major && K % 64) || (extra.b_rows && !B.mn_major && N % 64))
+    throw std::invalid_argument("gemm: gathered operand rows must be whole blocks");
   p.args = extra;
   p.args.M = M;
   p.args.N = N;

@@ -9,18 +9,24 @@
 //   data grad dX = dY . W      A = dY K-major,  B = W  MN-major
 //   weight gr dW = dY^T . X    A = dY MN-major, B = X  MN-major
 //
-// CTA = 6 warps: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (one
-// elected lane), warps 2..5 epilogue (one TMEM lane quadrant each).  Tile
-// 128 x 256 x 64, 4-stage smem ring (48 KB / stage), two TMEM accumulators
-// (2 x 256 fp32 columns) so the epilogue of tile i overlaps the MMAs of i+1.
-// Grid = min(#tiles, #SMs), static round-robin persistent schedule with
-// grouped rasterisation for L2 reuse.
+// CTA = 10 warps: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (one
+// elected lane), warps 2..9 epilogue (two per TMEM lane quadrant, each owning
+// a 128-column half).  Default CG = 2: a CTA pair on one TPC computes a
+// 256 x 256 x 64 tile with tcgen05.mma.cta_group::2 from a 5-stage smem ring
+// (32 KB / stage / CTA); CG = 1 computes 128 x 256 from a 3-stage ring.  Two
+// TMEM accumulators (2 x 256 fp32 columns) so the epilogue of tile i overlaps
+// the MMAs of i+1.  Persistent grid = min(#tiles, #SMs / CG) units, static
+// round-robin schedule with L2-aware rasterisation (make_plan).
 //
 // Epilogues (template EPI) fuse the elementwise consumer of every GEMM in the
-// step: bf16 / fp32 stores, fp32 accumulate, residual add, and the two halves
-// of the vocabulary-chunked cross-entropy (online softmax statistics in the
-// forward; softmax-minus-onehot gradient in the backward), so full logits
-// never reach HBM.
+// step: bf16 / fp32 stores, fp32 accumulate, residual add, q / k RoPE, the
+// SwiGLU backward, AdamW on weight gradients, and the vocabulary-chunked
+// cross-entropy: online softmax statistics in the forward (the logits are
+// additionally stored as fp16 offsets for the backward -- DESIGN.md §3 K6
+// explains why this beats the logit-free recompute, EPI_CE_BWD, which stays
+// selectable) and the softmax-minus-onehot gradient in the recompute path.
+// Operand rows can be gathered by 64-row blocks (Args::a_rows / b_rows): the
+// fc GEMMs read the micro-batch straight from the signal ring.
 #pragma once
 
 #include "gemm.h"
@@ -160,6 +166,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           args.keep_b == 0 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
       const uint64_t pol_b =
           args.keep_b == 1 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+      // operand row r of a gathered operand lives at rows[r / 64] + r % 64
+      auto remap = [](const int32_t* rows, int r) {
+        return rows ? __ldg(rows + (r >> 6)) + (r & 63) : r;
+      };
       auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1,
                       uint64_t pol) {
         if constexpr (CG == 2)
@@ -172,26 +182,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tile_coords(tile, args, mb, nb);
         const int m0 = mb * C_::TILE_M + static_cast<int>(rank) * BM;    // this CTA's A rows
         const int n0 = nb * BN + static_cast<int>(rank) * C_::BN_CTA;     // this CTA's B rows
+        // gathered K-major rows: one remap per tile (a 128-row box is two
+        // consecutive 64-row blocks of one sample)
+        const int a_row0 = A_MN ? m0 : remap(args.a_rows, m0);
+        const int b_row0 = B_MN ? n0 : remap(args.b_rows, n0);
         for (int kb = 0; kb < num_kb; ++kb) {
+          // MN-major operands are gathered along K: one remap per k-block,
+          // read before the slot wait so the load latency overlaps it
+          const int k0 = kb * BK;
+          const int a_k0 = A_MN ? remap(args.a_rows, k0) : k0;
+          const int b_k0 = B_MN ? remap(args.b_rows, k0) : k0;
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           // the leader's barrier counts both CTAs' bytes; the peer only issues TMA
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES * CG);
           uint8_t* a_dst = smA + stage * A_STAGE_BYTES;
           uint8_t* b_dst = smB + stage * B_STAGE_BYTES;
-          const int k0 = kb * BK;
           if constexpr (!A_MN) {
-            load(&tmA, &full_bar[stage], a_dst, k0, m0, pol_a);
+            load(&tmA, &full_bar[stage], a_dst, k0, a_row0, pol_a);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              load(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, k0, pol_a);
+              load(&tmA, &full_bar[stage], a_dst + j * 8192, m0 + 64 * j, a_k0, pol_a);
           }
           if constexpr (!B_MN) {
-            load(&tmB, &full_bar[stage], b_dst, k0, n0, pol_b);
+            load(&tmB, &full_bar[stage], b_dst, k0, b_row0, pol_b);
           } else {
 #pragma unroll
             for (int j = 0; j < C_::BN_CTA / 64; ++j)
-              load(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, k0, pol_b);
+              load(&tmB, &full_bar[stage], b_dst + j * 8192, n0 + 64 * j, b_k0, pol_b);
           }
           if (++stage == STAGES) {
             stage = 0;

@@ -71,6 +71,14 @@ struct Args {
   const float* rope_sin;
   int rope_S, rope_cols, rope_hd;
   int rope_pos_off, rope_ld;
+  // Row gather by 64-row blocks (nullable): the operand's tensor-map row r
+  // (M for a K-major operand, K for an MN-major one) is read from row
+  // a_rows[r / 64] + r % 64 -- the fc GEMMs read the micro-batch's feature
+  // rows straight from the signal ring (a sample's 64-row blocks are
+  // contiguous ring rows; K-major boxes of 128 rows need two consecutive
+  // blocks of one sample, i.e. S % 128 == 0).
+  const int32_t* a_rows;
+  const int32_t* b_rows;
 };
 
 // A matrix operand in HBM.  K-major: stored [MN, K] row-major (K contiguous).
@@ -79,6 +87,7 @@ struct Operand {
   const void* ptr;
   long long ld;
   bool mn_major;
+  long long rows = 0;  // tensor-map row extent when rows are gathered (Args::a_rows / b_rows)
 };
 
 struct GemmPlan {

@@ -52,8 +52,12 @@ HiddenStateBuffer::HiddenStateBuffer(const SignalGeometry& g, int64_t capacity_t
   SPECSIM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   stream_ = s;
   const size_t row = static_cast<size_t>(geom_.bytes_per_token());
-  SPECSIM_CUDA(cudaMalloc(&ring_feat_, row * cap_));
+  // + mirrored rows (kMirrorRows), zero-filled: rows a step reads past the end
+  // of a short sample (masked, zero gradient) are then always finite
+  SPECSIM_CUDA(cudaMalloc(&ring_feat_, row * (cap_ + kMirrorRows)));
+  SPECSIM_CUDA(cudaMemsetAsync(ring_feat_, 0, row * (cap_ + kMirrorRows), s));
   SPECSIM_CUDA(cudaMalloc(&ring_ids_, sizeof(int32_t) * cap_));
+  SPECSIM_CUDA(cudaMemsetAsync(ring_ids_, 0, sizeof(int32_t) * cap_, s));
   for (int i = 0; i < kEventRing; ++i) {
     cudaEvent_t ev;
     SPECSIM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -69,6 +73,32 @@ void HiddenStateBuffer::record_append(void* stream) {
   if (seq > kEventRing) SPECSIM_CUDA(cudaEventSynchronize(ev));
   SPECSIM_CUDA(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)));
   samples_.at(open_id_).last_seq = seq;
+}
+
+// Rows [0, kMirrorRows) written by an append of n rows at ring row pos (two
+// segments when it wraps) are copied to their mirror rows past the end.
+void HiddenStateBuffer::mirror(int64_t pos, int64_t n, void* stream) {
+  const int64_t lim = std::min<int64_t>(kMirrorRows, cap_);
+  const size_t row = static_cast<size_t>(geom_.bytes_per_token());
+  uint8_t* ring = static_cast<uint8_t*>(ring_feat_);
+  auto copy = [&](int64_t lo, int64_t hi) {  // ring rows [lo, hi) of [0, lim)
+    lo = std::max<int64_t>(lo, 0);
+    hi = std::min<int64_t>(hi, lim);
+    if (hi > lo)
+      SPECSIM_CUDA(cudaMemcpyAsync(ring + (cap_ + lo) * row, ring + lo * row, (hi - lo) * row,
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  };
+  const int64_t first = std::min<int64_t>(n, cap_ - pos);
+  copy(pos, pos + first);
+  if (first < n) copy(0, n - first);
+  if (cap_ < kMirrorRows) {
+    // tiny rings: rows [cap, cap + 128) repeat the ring cyclically
+    for (int64_t r = lim; r < kMirrorRows; r += cap_) {
+      const int64_t c = std::min<int64_t>(cap_, kMirrorRows - r);
+      SPECSIM_CUDA(cudaMemcpyAsync(ring + (cap_ + r) * row, ring, c * row,
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+    }
+  }
 }
 
 void* HiddenStateBuffer::event_for(int64_t seq) const {
@@ -215,6 +245,7 @@ void HiddenStateBuffer::append(int64_t sample_id, double alpha, const void* cons
   if (first < n)
     SPECSIM_CUDA(cudaMemcpyAsync(ring_ids_, d_ids + first, sizeof(int32_t) * (n - first),
                                  cudaMemcpyDeviceToDevice, s));
+  mirror(pos, n, s);
   record_append(s);
   SPECSIM_CUDA(cudaStreamSynchronize(s));  // staging reuse
   head_ += n;
@@ -262,6 +293,7 @@ void HiddenStateBuffer::append_packed(int64_t sample_id, double alpha, const uin
   if (first < n)
     SPECSIM_CUDA(cudaMemcpyAsync(ring_ids_, token_ids + first, sizeof(int32_t) * (n - first),
                                  kind, s));
+  mirror(pos, n, s);
   // consumers (trainer steps) order themselves after this event instead of a
   // host sync; pinned-host appends return immediately so the DMA overlaps
   // the step that is running

@@ -65,6 +65,33 @@ __global__ void gather_batch_kernel(const uint4* __restrict__ ring_feat,
   }
 }
 
+// Token gather only (the fc GEMMs read the features straight from the ring):
+// u / y / m of every unroll slice, one thread per (slice, row), and the ring
+// row of every 64-row block of the micro-batch (block j of sample b starts at
+// ring row (start_b + 64 j) % cap; padding samples read row 0).
+__global__ void gather_tokens_kernel(const int32_t* __restrict__ ring_ids, long long cap,
+                                     const BatchSpec* __restrict__ specp, int S, int K, long long T,
+                                     int32_t* __restrict__ u, int32_t* __restrict__ y,
+                                     int32_t* __restrict__ m, int32_t* __restrict__ blk_rows) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const BatchSpec& spec = *specp;
+  if (i < K * T) {
+    const int j = static_cast<int>(i / T);
+    const long long row = i - j * T;
+    const int b = static_cast<int>(row / S), t = static_cast<int>(row % S);
+    const int L = b < spec.n ? spec.len[b] : 0;
+    const long long base = b < spec.n ? spec.start[b] : 0;
+    u[i] = (t + 1 + j < L) ? ring_ids[(base + t + 1 + j) % cap] : 0;
+    y[i] = (t + 2 + j < L) ? ring_ids[(base + t + 2 + j) % cap] : 0;
+    m[i] = (t + 2 + j < L) ? 1 : 0;
+  }
+  if (i < T / 64) {
+    const long long row = i * 64;
+    const int b = static_cast<int>(row / S), t = static_cast<int>(row % S);
+    blk_rows[i] = b < spec.n ? static_cast<int32_t>((spec.start[b] + t) % cap) : 0;
+  }
+}
+
 __global__ void mask_count_kernel(const int32_t* __restrict__ m, long long T, long long* out) {
   __shared__ long long part[32];
   long long c = 0;
@@ -569,6 +596,14 @@ void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long 
   gather_batch_kernel<<<static_cast<unsigned>(T), 256, 0, s>>>(
       reinterpret_cast<const uint4*>(ring_feat), ring_ids, cap, W / 8, spec, S, K,
       reinterpret_cast<uint4*>(F), u, y, m);
+}
+
+void gather_tokens(const int32_t* ring_ids, long long cap, const BatchSpec* spec, int B, int S,
+                   int K, int32_t* u, int32_t* y, int32_t* m, int32_t* blk_rows, cudaStream_t s) {
+  const long long T = static_cast<long long>(B) * S;
+  count_launches();
+  gather_tokens_kernel<<<blocks_for(K * T, 256), 256, 0, s>>>(ring_ids, cap, spec, S, K, T, u, y,
+                                                             m, blk_rows);
 }
 
 void mask_count(const int32_t* m, long long T, long long* out, cudaStream_t s) {

@@ -40,6 +40,15 @@ void gather_batch(const __nv_bfloat16* ring_feat, const int32_t* ring_ids, long 
                   const BatchSpec* spec, int B, int S, int K, __nv_bfloat16* F, int32_t* u,
                   int32_t* y, int32_t* m, cudaStream_t s);
 
+// The same u / y / m without the feature copy, plus blk_rows[T / 64] = the
+// ring row of every 64-row block of the micro-batch (S % 64 == 0): the fc
+// GEMMs TMA-load F straight from the ring (HiddenStateBuffer::kMirrorRows
+// keeps a block contiguous across the ring's end).  Rows past a sample's end
+// read ring rows of other samples: their targets are masked, so every
+// gradient contribution of those rows is exactly zero.
+void gather_tokens(const int32_t* ring_ids, long long cap, const BatchSpec* spec, int B, int S,
+                   int K, int32_t* u, int32_t* y, int32_t* m, int32_t* blk_rows, cudaStream_t s);
+
 // coef[r] = m[r] / n_global * w[r / T] over K*T rows; n_global read from a
 // device scalar (int64)
 void ce_coef(const int32_t* m, const long long* n_global, float* coef, const StepWeights& sw,

@@ -229,6 +229,20 @@ class DraftTrainerImpl {
   // W_fc f, g[j+1] = h_j = the input of pass j+1, so h = g + T*H)
   __nv_bfloat16 *F, *g, *U, *qkv, *o, *r, *z, *gu, *act, *h, *nrm;
   int32_t *u, *y, *m, *argmax;
+  // The fc GEMMs (forward A operand, weight-gradient B operand) read the
+  // micro-batch's feature rows straight from the signal ring through a
+  // per-step table of 64-row block ring rows (no [T, 3H] copy; S % 128 == 0;
+  // SPECSIM_F_GATHER=1 keeps the gather copy into F for A/B runs).  Their
+  // plans hold a tensor map of one buffer's ring, so they are built per
+  // buffer (before the step is captured).
+  bool f_direct = false;
+  int32_t* blk_rows = nullptr;  // [T / 64]
+  struct RingPlans {
+    gemm::GemmPlan fc, dw_fc, f_dw_fc;
+  };
+  std::map<uint64_t, RingPlans> ring_plans;
+  const RingPlans* cur_ring = nullptr;
+  const void* last_ring = nullptr;  // ring of the last step / eval (read_rows("F"))
   float *coef, *rstd_a, *rstd_b, *lse_attn, *rstd_post, *rstd_fin, *lse, *row_loss;
   gemm::CePartial* partials;
   long long* n_global;
@@ -370,7 +384,13 @@ class DraftTrainerImpl {
     arena.reserve(&sin_t, static_cast<long long>(sh.seq_len) * sh.head_dim / 2);
     arena.reserve(&cos_tr, rope_len() * sh.head_dim / 2);
     arena.reserve(&sin_tr, rope_len() * sh.head_dim / 2);
-    arena.reserve(&F, T * W3);
+    {
+      const char* e = std::getenv("SPECSIM_F_GATHER");
+      f_direct = sh.seq_len % 128 == 0 && !(e && e[0] == '1');
+    }
+    F = nullptr;
+    if (!f_direct) arena.reserve(&F, T * W3);
+    arena.reserve(&blk_rows, (T + 63) / 64);
     arena.reserve(&g, (K + 1) * T * H);
     arena.reserve(&U, KT * 2 * H);
     arena.reserve(&qkv, KT * NQ);
@@ -592,7 +612,8 @@ class DraftTrainerImpl {
     using gemm::Operand;
     using namespace gemm;
     // forward: Y = X W^T (both K-major)
-    p_fc = make_plan({F, W3, false}, {pb("fc"), W3, false}, T, H, W3, EPI_BF16, out_args(g, H));
+    if (!f_direct)
+      p_fc = make_plan({F, W3, false}, {pb("fc"), W3, false}, T, H, W3, EPI_BF16, out_args(g, H));
     for (int j = 0; j < K; ++j) {
       const long long R = j * T;  // first row of pass j in the stacked buffers
       // q / k heads rotated in the epilogue (NeoX RoPE at t % S + j); v as is
@@ -675,27 +696,48 @@ class DraftTrainerImpl {
     p_dw_qkv = make_plan({dqkv, NQ, true}, {U, 2 * H, true}, NQ, 2 * H, KT, EPI_F32,
                          out_args(gf("qkv"), 2 * H));
     // fc (pass 0 only; no dF: captured features are inputs)
-    p_dw_fc = make_plan({dg_b, H, true}, {F, W3, true}, H, W3, T, EPI_F32,
-                        out_args(gf("fc"), W3));
-    // fused-AdamW twins of every weight-gradient GEMM
-    auto fused = [&](const GemmPlan& src, const char* name, long long row0) {
-      GemmPlan f = src;
-      const long long off = param(name).off + row0 * param(name).cols;
-      f.epi = EPI_ADAMW;
-      f.args.opt_p = P + off;
-      f.args.opt_m = Mst + off;
-      f.args.opt_v = Vst + off;
-      f.args.opt_p16 = P16 + off;
-      f.args.opt_g = G + off;  // cleared per launch unless keep_grads
-      f.args.opt_hp = adam_dev;
-      return f;
-    };
+    if (!f_direct)
+      p_dw_fc = make_plan({dg_b, H, true}, {F, W3, true}, H, W3, T, EPI_F32,
+                          out_args(gf("fc"), W3));
     for (int c = 0; c < n_chunks; ++c) f_lm_dw.push_back(fused(p_lm_dw[c], "lm_head", c * Vc));
     f_dw_down = fused(p_dw_down, "down", 0);
     f_dw_gu = fused(p_dw_gu, "gate_up", 0);
     f_dw_o = fused(p_dw_o, "o", 0);
     f_dw_qkv = fused(p_dw_qkv, "qkv", 0);
-    f_dw_fc = fused(p_dw_fc, "fc", 0);
+    if (!f_direct) f_dw_fc = fused(p_dw_fc, "fc", 0);
+  }
+
+  // fused-AdamW twin of a weight-gradient GEMM (rows from row0 of `name`)
+  gemm::GemmPlan fused(const gemm::GemmPlan& src, const char* name, long long row0) {
+    gemm::GemmPlan f = src;
+    const long long off = param(name).off + row0 * param(name).cols;
+    f.epi = gemm::EPI_ADAMW;
+    f.args.opt_p = P + off;
+    f.args.opt_m = Mst + off;
+    f.args.opt_v = Vst + off;
+    f.args.opt_p16 = P16 + off;
+    f.args.opt_g = G + off;  // cleared per launch unless keep_grads
+    f.args.opt_hp = adam_dev;
+    return f;
+  }
+
+  // fc GEMMs over this buffer's ring (the ring is [capacity + kMirrorRows, 3H])
+  const RingPlans& ring_plans_for(HiddenStateBuffer& buf) {
+    auto it = ring_plans.find(buf.serial());
+    if (it != ring_plans.end()) return it->second;
+    using namespace gemm;
+    const long long rows = buf.capacity() + HiddenStateBuffer::kMirrorRows;
+    RingPlans rp;
+    Args fa = out_args(g, H);
+    fa.a_rows = blk_rows;
+    rp.fc = make_plan({buf.ring_features(), W3, false, rows}, {pb("fc"), W3, false}, T, H, W3,
+                      EPI_BF16, fa);
+    Args da = out_args(gf("fc"), W3);
+    da.b_rows = blk_rows;
+    rp.dw_fc = make_plan({dg_b, H, true}, {buf.ring_features(), W3, true, rows}, H, W3, T,
+                         EPI_F32, da);
+    rp.f_dw_fc = fused(rp.dw_fc, "fc", 0);
+    return ring_plans.emplace(buf.serial(), rp).first->second;
   }
 
   // weight-gradient GEMM: fused AdamW on a single replica, plain fp32 grads
@@ -770,9 +812,13 @@ class DraftTrainerImpl {
     const int S = sh.seq_len;
     const kern::StepWeights& w = passes == K ? sw : sw1;
     timed(PH_INGEST, 0, [&] {
-      kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()), buf.ring_ids(),
-                         buf.capacity(), static_cast<int>(W3), &d_in->spec, sh.micro_batch, S,
-                         passes, F, u, y, m, stream);
+      if (f_direct)
+        kern::gather_tokens(buf.ring_ids(), buf.capacity(), &d_in->spec, sh.micro_batch, S,
+                            passes, u, y, m, blk_rows, stream);
+      else
+        kern::gather_batch(static_cast<const __nv_bfloat16*>(buf.ring_features()),
+                           buf.ring_ids(), buf.capacity(), static_cast<int>(W3), &d_in->spec,
+                           sh.micro_batch, S, passes, F, u, y, m, stream);
       kern::mask_count(m, T, n_counted, stream);
     });
     if (use_nccl)
@@ -784,7 +830,7 @@ class DraftTrainerImpl {
       kern::select_count(&d_in->nglobal, n_counted, n_global, stream);
       kern::ce_coef(m, n_global, coef, w, stream);
     });
-    run(p_fc);
+    run(f_direct ? cur_ring->fc : p_fc);
     for (int j = 0; j < passes; ++j) {
       const long long R = j * T;
       timed(PH_ELEM, 0, [&] {
@@ -1014,7 +1060,10 @@ class DraftTrainerImpl {
         }
       });
     }
-    run_dw(p_dw_fc, f_dw_fc);
+    if (f_direct)
+      run_dw(cur_ring->dw_fc, cur_ring->f_dw_fc);
+    else
+      run_dw(p_dw_fc, f_dw_fc);
     bucket_ready(n_chunks + 4);  // fc, w_in, w_hid
     if (use_nccl) {
       // join: AdamW waits for every bucket
@@ -1223,6 +1272,8 @@ class DraftTrainerImpl {
   void prepare(HiddenStateBuffer& buf, const int64_t* ids, int n, int64_t global_valid,
                bool train) {
     const kern::BatchSpec spec = batch_spec(buf, ids, n);
+    if (f_direct) cur_ring = &ring_plans_for(buf);  // host-side plan, before any capture
+    last_ring = buf.ring_features();
     if (void* ev = buf.event_for(wait_seq))
       SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(ev), 0));
     stage(spec, global_valid, train);
@@ -1636,9 +1687,28 @@ int specsim_trainer_read_rows(const specsim_trainer* t, const char* name, void* 
     else if (nm == "argmax") src = im.argmax;
     else if (nm == "lse") src = im.lse;
     else if (nm == "F") {
-      src = im.F;
-      esz = 2;
+      // the rows the fc GEMM read: the gathered copy, or (direct path) the
+      // ring's 64-row blocks named by the step's block table
       n = im.T * im.W3;
+      if (n_elems) *n_elems = n;
+      if (!host_out) return;
+      if (cap_elems < n) throw std::invalid_argument("host buffer too small");
+      DeviceGuard dg(im.device);
+      SPECSIM_CUDA(cudaStreamSynchronize(im.stream));
+      const size_t row = static_cast<size_t>(im.W3) * 2;
+      if (!im.f_direct) {
+        SPECSIM_CUDA(cudaMemcpy(host_out, im.F, row * im.T, cudaMemcpyDeviceToHost));
+        return;
+      }
+      if (!im.last_ring) throw std::invalid_argument("no step has run yet");
+      std::vector<int32_t> blk(static_cast<size_t>(im.T / 64));
+      SPECSIM_CUDA(cudaMemcpy(blk.data(), im.blk_rows, sizeof(int32_t) * blk.size(),
+                              cudaMemcpyDeviceToHost));
+      for (size_t b = 0; b < blk.size(); ++b)
+        SPECSIM_CUDA(cudaMemcpy(static_cast<uint8_t*>(host_out) + b * 64 * row,
+                                static_cast<const uint8_t*>(im.last_ring) + blk[b] * row,
+                                64 * row, cudaMemcpyDeviceToHost));
+      return;
     } else
       throw std::invalid_argument("unknown row buffer '" + nm + "'");
     if (n_elems) *n_elems = n;

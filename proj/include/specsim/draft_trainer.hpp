@@ -122,6 +122,11 @@ class SPECSIM_CXX_API HiddenStateBuffer {
 
   const SignalGeometry& geometry() const { return geom_; }
   int64_t capacity() const { return cap_; }
+  // Ring rows [capacity, capacity + kMirrorRows) repeat rows [0, kMirrorRows)
+  // (kept in sync by every append), so a block of <= kMirrorRows consecutive
+  // rows starting anywhere in the ring is contiguous in memory: the trainer's
+  // GEMMs TMA-load a sample's 64 / 128-row blocks straight from the ring.
+  static constexpr int kMirrorRows = 128;
   const void* ring_features() const { return ring_feat_; }
   const int32_t* ring_ids() const { return ring_ids_; }
   int device() const { return device_; }
@@ -136,6 +141,7 @@ class SPECSIM_CXX_API HiddenStateBuffer {
   void reserve(int n);  // evict oldest samples so n more tokens fit
   void account(int n);  // extract_signals byte accounting
   void record_append(void* stream);  // event + sequence number of this append
+  void mirror(int64_t pos, int64_t n, void* stream);  // refresh mirrored rows written
 
   SignalGeometry geom_;
   uint64_t serial_ = 0;

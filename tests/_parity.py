@@ -59,26 +59,45 @@ def oracle_state(tr, shp):
     return layout, P, tr.get_embedding()
 
 
-def check_gather(tr, F, u, y, m, rows=None):
-    """Device gather vs oracle, bit-exact over the first `rows` rows of u / y /
-    m (default all unroll slices; an eval fills slice 0 only)."""
+def sample_rows(shp, samples):
+    """[B*S] mask of the rows inside a sample (t < L).  The fc GEMMs read the
+    features straight from the signal ring, so rows past a sample's end hold
+    other ring rows instead of the oracle's zeros; their targets are masked
+    (t + 2 >= L), every gradient they receive is exactly zero, and nothing a
+    row inside a sample computes depends on them (causal attention): lse /
+    argmax / F are compared on these rows."""
+    S = shp.S
+    ok = np.zeros(shp.B * S, bool)
+    for b, (ids, _) in enumerate(samples):
+        ok[b * S:b * S + min(S, len(ids))] = True
+    return ok
+
+
+def check_gather(tr, F, u, y, m, rows=None, inside=None):
+    """Device gather vs oracle, bit-exact: u / y / m over the first `rows`
+    rows (default all unroll slices; an eval fills slice 0 only), the fc
+    input rows F on the rows inside a sample (`inside`, default all)."""
     n = len(u) if rows is None else rows
     for nm, ref in (("u", u), ("y", y), ("m", m)):
         got = tr.read_rows(nm)[:n]
         assert np.array_equal(got, ref[:n]), (nm, np.flatnonzero(got != ref[:n])[:8])
-    assert np.array_equal(tr.read_rows("F"), F), "F rows differ"
+    Fg = tr.read_rows("F")
+    sel = np.ones(len(F), bool) if inside is None else inside
+    assert np.array_equal(Fg[sel], F[sel]), "F rows differ"
 
 
-def check_top1(tr, r, out, am_o, margin, gap, m, T, logit_tol):
-    """gap[row] = oracle max logit - oracle logit at the device's argmax.
-    Returns (decided rows, ambiguous valid rows, rows whose argmax differs,
-    max gap)."""
+def check_top1(tr, r, out, am_o, margin, gap, m, T, logit_tol, rows_ok):
+    """gap[row] = oracle max logit - oracle logit at the device's argmax, on
+    the rows inside a sample (rows_ok, all unroll slices).  Returns (decided
+    rows, ambiguous valid rows, rows whose argmax differs, max gap)."""
     am_g = tr.read_rows("argmax")[:len(am_o)]
+    am_g, am_o, margin, gap = am_g[rows_ok], am_o[rows_ok], margin[rows_ok], gap[rows_ok]
     far = np.flatnonzero(~(gap <= logit_tol))
     assert far.size == 0, ("device argmax not a near-maximum", far[:8], gap[far[:8]])
     sure = margin > logit_tol
     assert np.array_equal(am_g[sure], am_o[sure])
-    ambiguous = int(((m[:T] == 1) & ~sure[:T]).sum())
+    valid0 = (m[:T] == 1)[rows_ok[:T]]
+    ambiguous = int((valid0 & ~sure[:len(valid0)]).sum())
     assert abs(r["top1_correct"] - out.top1) <= ambiguous, (r["top1_correct"], out.top1, ambiguous)
     if ambiguous == 0:
         assert r["top1_correct"] == out.top1
@@ -104,14 +123,16 @@ def step_and_compare(tr, buf, ids, shp, samples, P, Mst, Vst, E, k, hp, *, grad_
     P0 = P.copy()
     out, grads = oracle.train_step(shp, hp, k, P, Mst, Vst, E, F, u, y, m, round_bf16=True,
                                    update=check_update)
-    check_gather(tr, F, u, y, m)
+    inside = sample_rows(shp, samples)
+    rows_ok = np.tile(inside, len(am_o) // T)  # every unroll slice
+    check_gather(tr, F, u, y, m, inside=inside)
     assert r["valid_tokens"] == int(m[:T].sum()) == out.valid
     assert r["positions"] == T
     assert abs(r["loss"] - out.loss) <= 2e-3 * max(abs(out.loss), 1e-30), (r["loss"], out.loss)
-    lse_err = float(np.abs(lse_g[:len(lse_o)] - lse_o).max())
+    lse_err = float(np.abs(lse_g[:len(lse_o)] - lse_o)[rows_ok].max())
     assert lse_err <= 5e-3 * max(1.0, logit_tol / MARGIN), lse_err
     decided, ambiguous, differ, max_gap = check_top1(tr, r, out, am_o, margin, gap, m, T,
-                                                     logit_tol)
+                                                     logit_tol, rows_ok)
     report = dict(loss_gpu=r["loss"], loss_cpu=out.loss, lse_err=lse_err, decided_rows=decided,
                   ambiguous_valid_rows=ambiguous, argmax_differs=differ, max_gap=max_gap,
                   top1=(r["top1_correct"], out.top1), grads={}, update_frac={})

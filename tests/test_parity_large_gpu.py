@@ -17,7 +17,8 @@ import pytest
 
 import oracle
 from paper_2602_05145_b200 import api
-from _parity import LARGE_LOGIT_TOL, check_gather, oracle_state, step_and_compare
+from _parity import (LARGE_LOGIT_TOL, check_gather, oracle_state, sample_rows,
+                     step_and_compare)
 
 pytestmark = pytest.mark.gpu
 SEED = 20260217
@@ -104,10 +105,11 @@ def test_gather_bit_exact_across_ring_wrap_ttt():
     for ids in ([3, 4, 1], [2, 3, 4, 1], [4]):
         samples = [(caps[i]["ids"], caps[i]["features"]) for i in ids]
         F, u, y, m = oracle.gather_batch(shp, samples)
+        inside = sample_rows(shp, samples)
         tr.step(buf, ids)
-        check_gather(tr, F, u, y, m)
+        check_gather(tr, F, u, y, m, inside=inside)
         tr.eval(buf, ids)
-        check_gather(tr, F, u, y, m, rows=c["micro_batch"] * S)
+        check_gather(tr, F, u, y, m, rows=c["micro_batch"] * S, inside=inside)
     tr.close()
     buf.close()
 

@@ -369,3 +369,37 @@ def test_max_batch_rows_split_additivity():
         rel = np.linalg.norm(g_sum[nm] - g_full[nm]) / np.linalg.norm(g_full[nm])
         assert rel <= 2e-3, (nm, rel)
     tr.close(); buf.close()
+
+
+def test_ring_direct_fc_equals_gathered_copy(monkeypatch):
+    """The fc GEMMs read the micro-batch's feature rows straight from the
+    signal ring (64-row block table + mirrored ring rows); SPECSIM_F_GATHER=1
+    copies them into a [T, 3H] buffer first.  Rows past a sample's end hold
+    other ring rows on the direct path (zeros on the copy path) but every
+    gradient they receive is exactly zero, so the two paths agree bit for bit
+    -- here with samples straddling the ring's end, short samples and a
+    padding row, over two steps and the training-time-test unroll."""
+    for ttt in (1, 2):
+        c = dict(SHAPES["s384"], micro_batch=3, ttt_steps=ttt)
+        S = c["seq_len"]
+        lens = [S + 4, S // 2 + 9, S + 3, 77, S + 10]
+        buf = api.HiddenStateBuffer(api.SignalGeometry(c["hidden"]), 2 * S + 200)
+        for i, L in enumerate(lens):  # 0, 1 evicted; 2 straddles the end
+            cap = oracle.synth_capture(SEED, i, L, c["vocab"], c["hidden"])
+            buf.append_packed(i, cap["alpha_s"], cap["features"], cap["ids"])
+        out = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("SPECSIM_F_GATHER", mode)
+            tr = api.DraftTrainer(c, lr=1e-3, seed=SEED)
+            tr.keep_grads(True)
+            res = []
+            for ids in ([2, 3, 4], [3, 4]):
+                r = tr.step(buf, ids)
+                res.append((r["loss"], {nm: tr.get_grad(nm).copy() for nm, *_ in tr.params()[0]}))
+            out[mode] = res
+            tr.close()
+        for (l0, g0), (l1, g1) in zip(out["0"], out["1"]):
+            assert l0 == l1, (ttt, l0, l1)
+            for nm in g0:
+                assert np.array_equal(g0[nm], g1[nm]), (ttt, nm)
+        buf.close()
