@@ -1,8 +1,11 @@
 // HBM-bound kernels of the draft-training step.  See kernels.h.
 #include "common.h"
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace specsim {
 namespace kern {
@@ -529,6 +532,42 @@ __global__ void pack_signals_kernel(LayerPtrs layers, int n_layers, long long ld
   }
 }
 
+// TMA-staged pack: one warp per CTA, lane 0 drives the bulk-copy engine --
+// every accepted row's layer segments are bulk-loaded (cp.async.bulk, no
+// register staging) into shared memory at their packed offsets, then each
+// assembled [layers*H] row is bulk-stored to its ring row.  The SMs issue a
+// handful of instructions per row, so a capture on the serving GPU leaves its
+// compute to verification.  Requires 16-byte aligned rows (H % 8, ld % 8).
+constexpr int kPackRowsMax = 4;
+__global__ void __launch_bounds__(32) pack_signals_tma_kernel(
+    LayerPtrs layers, int n_layers, long long ld, int H, const int32_t* __restrict__ idx, int n,
+    int rows_per_cta, __nv_bfloat16* __restrict__ ring, long long cap, long long pos) {
+  extern __shared__ __align__(128) uint8_t pack_smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const int i0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, n - i0);
+  const uint32_t seg = static_cast<uint32_t>(H) * 2;  // bytes per layer segment
+  const uint32_t row_bytes = seg * n_layers;
+  if (threadIdx.x == 0 && nr > 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_barrier_init();
+    ptx::mbar_arrive_expect_tx(&bar, row_bytes * nr);
+    for (int r = 0; r < nr; ++r) {
+      const long long src_row = idx ? idx[i0 + r] : i0 + r;
+      for (int l = 0; l < n_layers; ++l)
+        ptx::bulk_load(pack_smem + r * row_bytes + l * seg, layers.p[l] + src_row * ld, seg, &bar);
+    }
+    ptx::mbar_wait(&bar, 0);
+    for (int r = 0; r < nr; ++r) {
+      const long long dst_row = (pos + i0 + r) % cap;
+      ptx::bulk_store(reinterpret_cast<uint8_t*>(ring) + dst_row * row_bytes,
+                      pack_smem + r * row_bytes, row_bytes);
+    }
+    ptx::bulk_commit();
+    ptx::bulk_wait_all();
+  }
+}
+
 __global__ void pack_packed_kernel(const uint4* __restrict__ src, int W8, int n,
                                    uint4* __restrict__ ring, long long cap, long long pos) {
   const int i = blockIdx.x;
@@ -730,6 +769,29 @@ void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, co
                   int n, __nv_bfloat16* ring_feat, long long cap, long long pos, cudaStream_t s) {
   if (n <= 0) return;
   count_launches();
+  static const bool tma = [] {
+    const char* e = std::getenv("SPECSIM_PACK_SM");  // A/B: SM-copy pack kernel
+    return !(e && e[0] == '1');
+  }();
+  const long long row_bytes = 2ll * H * n_layers;
+  bool aligned = (ld % 8) == 0 && (H % 8) == 0 && reinterpret_cast<uintptr_t>(ring_feat) % 16 == 0;
+  for (int l = 0; l < n_layers; ++l)
+    aligned = aligned && reinterpret_cast<uintptr_t>(layers.p[l]) % 16 == 0;
+  if (tma && aligned && row_bytes <= 96 * 1024) {
+    const int rows = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(kPackRowsMax, (96 * 1024) / row_bytes)));
+    const int smem = static_cast<int>(rows * row_bytes);
+    static int smem_set = 0;
+    if (smem > smem_set) {
+      SPECSIM_CUDA(cudaFuncSetAttribute(pack_signals_tma_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+      smem_set = 200 * 1024;
+    }
+    pack_signals_tma_kernel<<<(n + rows - 1) / rows, 32, smem, s>>>(
+        layers, n_layers, ld, H, idx, n, rows, ring_feat, cap, pos);
+    return;
+  }
   pack_signals_kernel<<<n, 128, 0, s>>>(layers, n_layers, ld, H / 8, idx,
                                         n, reinterpret_cast<uint4*>(ring_feat), cap, pos);
 }

@@ -136,6 +136,24 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 // 2-D tiled load for a CTA pair (cta_group::2): each CTA writes its own smem
 // but the transaction bytes complete on the LEADER CTA's mbarrier (peer bit of
 // the barrier address cleared).
+// Plain bulk copy shared -> global (TMA engine, bulk-group completion).
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// every committed bulk store has finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// every committed bulk store has completed (writes performed)
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, uint64_t* bar,
                                                  void* smem_dst, int32_t c0, int32_t c1,
                                                  uint64_t policy) {

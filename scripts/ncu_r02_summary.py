@@ -60,11 +60,11 @@ def load(path):
 
 
 def short(name):
-    n = name.split("(")[0]
-    for pre in ("void ", "specsim::kern::(anonymous namespace)::", "specsim::attn::",
-                "specsim::gemm::", "specsim::kern::", "(anonymous namespace)::"):
-        n = n.replace(pre, "")
-    return n.strip()
+    """kernel name without namespaces / parameters, template arguments kept"""
+    n = name.split("(")[0].replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+    n = n.replace("void ", "").strip()
+    head, _, tmpl = n.partition("<")
+    return head.split("::")[-1] + (("<" + tmpl) if tmpl else "")
 
 
 def last_step(rows):
