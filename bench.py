@@ -54,6 +54,8 @@ def parse():
                          "(0 = weak scaling, the config's per-rank micro-batch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ce-probe", action="store_true",
+                    help="skip the logit-free (recompute) LM-head backward probe leg")
     ap.add_argument("--cpu-sample-seq", type=int, default=256,
                     help="positions in the bounded CPU sample (one sequence)")
     return ap.parse_args()
@@ -126,16 +128,26 @@ class ClockSampler:
                     reasons=sorted(reasons), samples=len(rows))
 
 
-def ncu_traffic():
-    """dram bytes per GEMM launch from the committed ncu capture, if present."""
-    for p in sorted((ROOT / "profiles").glob("*gemm_ncu*.json")):
-        try:
-            d = json.loads(p.read_text())
-            if d.get("dram_bytes_per_launch"):
-                return d
-        except Exception:
-            pass
-    return None
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per GEMM launch, averaged over every GEMM
+    launch of one step like `achieved` -- from the committed ncu metric capture
+    of this workload (profiles/r02_step_ncu_<config>.json, made by
+    scripts/ncu_r02.sh; ncu cannot run inside a timed bench), or None."""
+    p = ROOT / "profiles" / f"r02_step_ncu_{config}.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        g = d["gemms"]
+        dram = sum(x["dram_gb"] for x in g) * 1e9
+        alg = sum(x["algorithmic_gb"] for x in g) * 1e9
+        return dict(dram_bytes_per_launch=round(dram / len(g)), launches=len(g),
+                    dram_over_algorithmic=round(dram / alg, 3),
+                    source=f"profiles/{p.name} (ncu --metrics dram__bytes_read.sum,"
+                           "dram__bytes_write.sum over one step's GEMM launches; "
+                           "scripts/ncu_r02.sh)")
+    except Exception:
+        return None
 
 
 def cpu_sample(cfg, seq, threads_note=True):
@@ -469,14 +481,16 @@ def run_ours(args):
     gemm_ms = phase_acc["gemm"]["ms"] + phase_acc["lm_head_ce"]["ms"]
     gemm_alg = phase_acc["gemm"]["flops"] + phase_acc["lm_head_ce"]["flops"]
     achieved = gemm_alg / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.config) if cfg.get("ttt_steps", 1) == 1 else None
     roofline = dict(bound="tensor", kernel="gemm_kernel<tcgen05> (all GEMM launches of the step)",
                     achieved=round(achieved, 1) if achieved else None,
                     peak=pk["bf16_sustained"], unit="TFLOP/s",
                     frac=round(achieved / pk["bf16_sustained"], 4) if achieved else None,
                     peak_source=f"{pk['src']} bf16_tflops_sustained (kernel timed inside a long step)",
                     traffic=traffic.get("dram_bytes_per_launch") if traffic else None,
-                    traffic_kernel=traffic.get("kernel") if traffic else None,
+                    traffic_over_algorithmic=traffic.get("dram_over_algorithmic") if traffic
+                    else None,
+                    traffic_source=traffic.get("source") if traffic else None,
                     algorithmic="SURVEY §8(d): sum of GEMM FLOPs excluding the CE-backward logit "
                                 "recompute, over the summed device time of every GEMM launch "
                                 "(recompute time included)",
@@ -506,6 +520,36 @@ def run_ours(args):
                 phases=phases,
                 loss_mean_value_leg=round(sum(value_losses) / len(value_losses), 4),
                 clocks=clk)
+
+    # ------------------------------------------------------------ CE probe
+    # north_star (3) asks that full logits never reach HBM.  The default step
+    # stores them as fp16 offsets (2 B x T x V) because that beats recomputing
+    # them in the backward (DESIGN.md §3 K6, §10); the logit-free path
+    # (SPECSIM_CE_RECOMPUTE=1: the CE-backward GEMM recomputes each logit tile
+    # in TMEM and writes the bf16 gradient tile directly) is timed here on a
+    # second trainer so every bench line reports both.
+    if rank == 0 and world == 1 and not args.no_ce_probe:
+        try:
+            os.environ["SPECSIM_CE_RECOMPUTE"] = "1"
+            tr2 = api.DraftTrainer(cfg, seed=SEED, device=local)
+            os.environ.pop("SPECSIM_CE_RECOMPUTE")
+            for k in range(2):
+                tr2.step(buf, batch(k))
+            tr2.set_timing(True)
+            acc, st = 0.0, 0.0
+            for k in range(3):
+                st += tr2.step(buf, batch(k))["ms"]
+                acc += tr2.phase_times()["lm_head_ce"]["ms"]
+            tr2.close()
+            line["ce_recompute_probe"] = dict(
+                lm_head_ce_ms_per_step=round(acc / 3, 3), step_ms=round(st / 3, 3),
+                default_lm_head_ce_ms_per_step=phases["lm_head_ce"]["ms_per_step"],
+                note="logit-free LM-head + CE backward (no [T, V] logits in HBM); 3 timed "
+                     "single steps after 2 warm-up, phase events on; the default path stores "
+                     "fp16 logit offsets instead (DESIGN.md §3 K6)")
+        except Exception as e:  # reported, never required
+            os.environ.pop("SPECSIM_CE_RECOMPUTE", None)
+            line["ce_recompute_probe"] = dict(error=str(e)[:200])
 
     # ------------------------------------------------------------ CPU baseline
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -7,9 +7,11 @@
 // all later query blocks) and a dQ kernel (one CTA per 64-query block), so
 // every gradient element is written exactly once — deterministic, no atomics.
 //
-// Attention is ~1% of the step's FLOPs; this version uses
-// warp-level mma.sync m16n8k16 bf16 with ldmatrix from XOR-swizzled shared
-// memory and cp.async double buffering.  A tcgen05 version is future work.
+// This file is the FALLBACK path: warp-level mma.sync m16n8k16 bf16 with
+// ldmatrix from XOR-swizzled shared memory and cp.async double buffering,
+// used when S % 128 != 0 (or SPECSIM_ATTN_MMA_SYNC=1).  Every benchmarked
+// configuration (S % 128 == 0) runs the tcgen05 / TMEM / TMA kernels of
+// attention_tc.cu; the dispatch is in forward() / backward() below.
 //
 // Layouts: qkv [T, NQ] bf16 (T = B*S token rows; q head h at column h*HD, k
 // head g at Q + g*HD, v head g at Q + KV + g*HD); o / dO [T, Q]; lse / D

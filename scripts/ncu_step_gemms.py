@@ -17,7 +17,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 def gemm_list(T=8192, H=4096, V=128256, Q=4096, KV=1024, I=14336, Vc=32768):
     L = [("fc fwd", T, H, 3 * H), ("qkv fwd + RoPE", T, Q + 2 * KV, 2 * H),
          ("o fwd + residual", T, H, Q), ("gate_up fwd", T, 2 * I, H),
-         ("down fwd + residual", T, H, I), ("LM head CE fwd (stats + fp32 logits)", T, V, H)]
+         ("down fwd + residual", T, H, I), ("LM head CE fwd (stats + fp16 logits)", T, V, H)]
     for c in range(0, V, Vc):
         vn = min(Vc, V - c)
         L += [(f"LM head dX chunk {c // Vc}", T, H, vn),
@@ -49,16 +49,20 @@ def main(rep, out):
         ms = get(r, "gpu__time_duration.sum")
         rd = get(r, "dram__bytes_read.sum")
         wr = get(r, "dram__bytes_write.sum")
-        out_b = 4 if ("AdamW" in label or "dX chunk" in label or "dz" in label or "dU" in label
-                      or "logits" in label) else 2
+        out_b = 4 if ("dX chunk" in label or "dz" in label or "dU" in label) else 2
         alg = 2 * (M * K + N * K) + out_b * M * N
         if "AdamW" in label:
             alg = 2 * (M * K + N * K) + 26 * M * N  # p m v read, p m v p16 written
+        if "CE fwd" in label:  # fp16 logit offsets + one 16-byte partial per 128-column half tile
+            alg = 2 * (M * K + N * K) + 2 * M * N + 2 * ((N + 255) // 256) * M * 16
         launches.append(dict(
             launch=label, kernel=r[hdr.index("Kernel Name")][:60], M=M, N=N, K=K, ms=ms,
             tflops=round(2 * M * N * K / (ms * 1e-3) / 1e12, 1), dram_read=rd, dram_write=wr,
             algorithmic_bytes=alg,
-            tensor_active_pct=get(r, "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime"
+            # the tcgen05 pipe: this counter equals FLOPs / (148 x 8192 x clock x
+            # time) launch for launch (profiles/r02_step_ncu_C2.txt); the
+            # TriageCompute realtime counter used in round 1 does not
+            tensor_active_pct=get(r, "sm__pipe_tensor_subpipe_hmma_cycles_active"
                                      ".avg.pct_of_peak_sustained_elapsed"),
             sm_ghz=round(get(r, "sm__cycles_elapsed.avg.per_second") / 1e9, 3)))
     ce = [l for l in launches if l["launch"].startswith("LM head CE fwd")]
@@ -66,7 +70,7 @@ def main(rep, out):
         source=rep, note="ncu --set full --clock-control none, one C2 step (second step of "
         "`bench.py --steps 1 --warmup 1`); kernels serialised and replayed, so absolute "
         "times are cold-cache / unthrottled -- shares, bytes and pipe activity are the signal",
-        kernel="gemm_kernel<0,0,EPI_CE_FWD,2> (LM head + CE forward, C2)",
+        kernel="gemm_kernel<0,0,EPI_CE_FWD,2> (LM head + CE forward, C2; logits stored as fp16)",
         dram_bytes_per_launch=(ce[0]["dram_read"] + ce[0]["dram_write"]) if ce else None,
         algorithmic_bytes=ce[0]["algorithmic_bytes"] if ce else None,
         total_ms=round(sum(l["ms"] for l in launches), 3), launches=launches)
