@@ -287,19 +287,20 @@ def run_ours(args):
     pool_n = 2 * B
     L = S + 1 + cfg.get("ttt_steps", 1)  # every unroll pass fully unmasked
     W = 3 * H
-    # ring: the resident pool + the batches of one e2e train(job) (<= 16 steps
-    # and <= 2 GiB of captured states) + one batch of slack; an e2e job may
-    # evict the pool (FIFO), which is then re-appended outside the timed
-    # regions.  Larger jobs queue more asynchronous DMA than the driver's
-    # per-stream work queue holds: the host then blocks inside the appends
-    # until the DMA drains and the job's steps stop overlapping it (measured
-    # at C2: 6 GB jobs read e2e 9% below the device number, 1.6-3.2 GB jobs
-    # 2%; C4 / C5 4-6 GB jobs 6-8%).  SPECSIM_BENCH_E2E_JOB overrides the job
+    # ring: the resident pool + the batches of TWO e2e train(job)s (the next
+    # job's captured states are appended while the current one trains, <= 16
+    # steps and <= 1 GiB each) + one batch of slack; an e2e job may evict the
+    # pool (FIFO), which is then re-appended outside the timed regions.  More
+    # queued asynchronous DMA than the driver's per-stream work queue holds
+    # makes the host block inside the appends until the DMA drains and the
+    # steps stop overlapping it (measured at C2: 6 GB jobs read e2e 9% below
+    # the device number, 1.6-3.2 GB jobs 2%); with the next job prefetched,
+    # at most ~2 GiB are queued.  SPECSIM_BENCH_E2E_JOB overrides the job
     # length (that experiment).
     step_bytes = B * L * (W * 2 + 4)
     per_job = int(os.environ.get("SPECSIM_BENCH_E2E_JOB", "0")) or \
-        max(1, min(16, (2 << 30) // step_bytes))
-    buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + (per_job + 1) * B) * L,
+        max(1, min(16, (1 << 30) // step_bytes))
+    buf = api.HiddenStateBuffer(geom, capacity_tokens=(pool_n + (2 * per_job + 1) * B) * L,
                                 device=local)
     # synthetic captured requests; generated by the library in
     # parallel threads (ctypes releases the GIL)
@@ -365,24 +366,31 @@ def run_ours(args):
     h2d = B * L * (W * 2 + 4)
     losses = []
 
+    def append_job(first, n):
+        """this rank's captured states of steps first .. first+n-1 (async pinned
+        DMA on the buffer's stream); returns the global job's sample ids"""
+        base = next_id[0]
+        for k in range(n):
+            for j in range(B):
+                t, idt, a = pinned[((first + k) * B + j) % pool_n]
+                _lib.call("specsim_hsbuf_append_packed", buf.h,
+                          rank * RID + base + k * B + j, a, t.data_ptr(), idt.data_ptr(), L, 2)
+        next_id[0] += n * B
+        return global_job(n, lambda r, k, j: r * RID + base + k * B + j)
+
     def run_e2e(nsteps):
-        # jobs of <= per_job steps bound the ring: each job's batches are appended
-        # (asynchronously, this rank's own samples), then the global job trains
-        done = 0
-        while done < nsteps:
-            n = min(per_job, nsteps - done)
-            base = next_id[0]
-            for k in range(n):
-                for j in range(B):
-                    t, idt, a = pinned[((done + k) * B + j) % pool_n]
-                    _lib.call("specsim_hsbuf_append_packed", buf.h,
-                              rank * RID + base + k * B + j, a, t.data_ptr(), idt.data_ptr(),
-                              L, 2)
-            next_id[0] += n * B
-            ids = global_job(n, lambda r, k, j: r * RID + base + k * B + j)
-            o = tr.train(buf, ids, [], epochs=1)  # the job's loss comes back to the host
+        # jobs of <= per_job steps bound the ring.  Each job's batches are
+        # appended (asynchronously, this rank's own samples) BEFORE the previous
+        # job trains, so their DMA runs under that job's steps: only the very
+        # first batch's copy is exposed.  train(job) returns the job's loss.
+        sizes = [min(per_job, nsteps - d) for d in range(0, nsteps, per_job)]
+        firsts = [sum(sizes[:i]) for i in range(len(sizes))]
+        pending = append_job(firsts[0], sizes[0])
+        for i in range(len(sizes)):
+            nxt = append_job(firsts[i + 1], sizes[i + 1]) if i + 1 < len(sizes) else None
+            o = tr.train(buf, pending, [], epochs=1)
             losses.append(o.mean_loss)
-            done += n
+            pending = nxt
 
     # ------------------------------------------------------------ timed legs
     # Device-timed leg: K optimiser steps through train(job) -- the entry point
@@ -439,8 +447,9 @@ def run_ours(args):
                    ms_per_step=round(1e3 * dt_e2e / args.steps, 2),
                    device_ms_per_step=round(e2e_dev_ms / args.steps, 3),
                    timing="host wall clock around the async pinned-host appends + train(job) "
-                          "of the K steps, run between the two halves of the device-timed leg, "
-                          "max over ranks")
+                          "of the K steps (jobs of <= 1 GiB of captured states; job i+1's appends "
+                          "are issued before job i trains, so its DMA overlaps job i's steps), "
+                          "run between the two halves of the device-timed leg, max over ranks")
         # ingest alone (reported separately): one job's worth of
         # pinned-host appends with nothing else running, host wall clock
         n_in = per_job * B
