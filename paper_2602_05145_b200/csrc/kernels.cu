@@ -798,12 +798,16 @@ void pack_signals(const LayerPtrs& layers, int n_layers, long long ld, int H, co
 
 __global__ void fetch_mapped_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                                     int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcv(src + i);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = __ldcv(src + i);
 }
 
 void fetch_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s) {
   count_launches();
-  fetch_mapped_kernel<<<1, 128, 0, s>>>(src, dst, n_words);
+  // one block per ~1k words (a whole train(job) table moves in one launch;
+  // PCIe reads are latency-bound, so more lanes in flight)
+  const int blocks = std::max(1, std::min(64, (n_words + 1023) / 1024));
+  fetch_mapped_kernel<<<blocks, 128, 0, s>>>(src, dst, n_words);
 }
 
 void store_mapped(const uint32_t* src, uint32_t* dst, int n_words, cudaStream_t s) {

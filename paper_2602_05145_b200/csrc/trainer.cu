@@ -275,6 +275,13 @@ class DraftTrainerImpl {
   };
   StepInputs* d_in = nullptr;
   StepInputs* h_in = nullptr;  // pinned, 2 slots
+  // train(job): every step's inputs are built up front into a mapped pinned
+  // table, moved to the device ONCE (one SM fetch over PCIe), and each step's
+  // slot is copied device-to-device into d_in -- no per-step PCIe read, which
+  // would queue behind the ingest DMA a caller streams during the job
+  StepInputs* h_job = nullptr;
+  StepInputs* d_job = nullptr;
+  size_t job_cap = 0;
   cudaEvent_t in_ev[2] = {nullptr, nullptr};
   int in_slot = 0;
   gemm::AdamDev* adam_dev = nullptr;  // = &d_in->hp
@@ -509,6 +516,8 @@ class DraftTrainerImpl {
     if (h_nglobal) cudaFreeHost(h_nglobal);
     if (h_stats) cudaFreeHost(h_stats);
     if (h_in) cudaFreeHost(h_in);
+    if (h_job) cudaFreeHost(h_job);
+    if (d_job) cudaFree(d_job);
     if (hist_buf) cudaFreeHost(hist_buf);
     for (auto e : in_ev)
       if (e) cudaEventDestroy(e);
@@ -1104,8 +1113,8 @@ class DraftTrainerImpl {
     version = snap_version;  // the restored model is the snapshot's version
   }
 
-  kern::AdamHyper next_hyper() const {
-    const int64_t k = step_count + 1;
+  kern::AdamHyper next_hyper() const { return hyper_for(step_count + 1); }
+  kern::AdamHyper hyper_for(int64_t k) const {
     const double bc1 = 1.0 - std::pow(static_cast<double>(opt.beta1), static_cast<double>(k));
     const double bc2 = 1.0 - std::pow(static_cast<double>(opt.beta2), static_cast<double>(k));
     kern::AdamHyper hp;
@@ -1122,6 +1131,19 @@ class DraftTrainerImpl {
   // Host: fill the next pinned slot and enqueue its fetch into d_in (stream
   // ordered before the step's launch, after the previous step).  A slot is
   // reused only once the fetch issued from it two steps ago has executed.
+  StepInputs make_inputs(const kern::BatchSpec& spec, int64_t global_valid, bool train,
+                         int64_t step_k) const {
+    StepInputs s{};
+    s.spec = spec;
+    s.nglobal = global_valid > 0 ? global_valid : 0;
+    if (train) {
+      const kern::AdamHyper hp = hyper_for(step_k);
+      s.hp = gemm::AdamDev{hp.lr, hp.beta1, hp.beta2, hp.eps, hp.decay, hp.step_size,
+                           hp.bc2_sqrt, 0.f};
+    }
+    return s;
+  }
+
   void stage(const kern::BatchSpec& spec, int64_t global_valid, bool train) {
     in_slot ^= 1;
     SPECSIM_CUDA(cudaEventSynchronize(in_ev[in_slot]));
@@ -1374,23 +1396,52 @@ class DraftTrainerImpl {
       hist_cap = need * 2;
     }
     double* hist = hist_buf;
-    std::vector<int64_t> mine;
-    long long k = 0;
-    for (int ep = 0; ep < job.epochs; ++ep) {
-      for (long long s0 = 0, j = 0; s0 < n; s0 += per_step, ++j) {
-        shard(n, j, mine, job.train_ids);
-        prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, true);
-        launch(buf, true);
-        step_count += 1;
-        stats_to_host(hist + 3 * k++);
+    // every launch's inputs up front (mapped pinned table -> device once)
+    if (static_cast<size_t>(total_launch) > job_cap) {
+      SPECSIM_CUDA(cudaStreamSynchronize(stream));
+      if (h_job) cudaFreeHost(h_job);
+      if (d_job) cudaFree(d_job);
+      h_job = nullptr;
+      d_job = nullptr;
+      job_cap = static_cast<size_t>(total_launch) * 2;
+      SPECSIM_CUDA(cudaHostAlloc(&h_job, sizeof(StepInputs) * job_cap, cudaHostAllocMapped));
+      SPECSIM_CUDA(cudaMalloc(&d_job, sizeof(StepInputs) * job_cap));
+    }
+    std::vector<int64_t> mine, waits(static_cast<size_t>(total_launch));
+    std::vector<char> is_train(static_cast<size_t>(total_launch));
+    {
+      long long k = 0;
+      int64_t sc = step_count;
+      for (int ep = 0; ep < job.epochs; ++ep)
+        for (long long s0 = 0, j = 0; s0 < n; s0 += per_step, ++j, ++k) {
+          shard(n, j, mine, job.train_ids);
+          const kern::BatchSpec spec = batch_spec(buf, mine.data(), static_cast<int>(mine.size()));
+          waits[k] = wait_seq;
+          is_train[k] = 1;
+          h_job[k] = make_inputs(spec, 0, true, ++sc);
+        }
+      for (long long s0 = 0, j = 0; s0 < ne; s0 += per_step, ++j, ++k) {
+        shard(ne, j, mine, job.eval_ids);
+        const kern::BatchSpec spec = batch_spec(buf, mine.data(), static_cast<int>(mine.size()));
+        waits[k] = wait_seq;
+        is_train[k] = 0;
+        h_job[k] = make_inputs(spec, 0, false, 0);
       }
     }
-    // alpha_eval = top-1 accuracy of the new draft on D_eval
-    for (long long s0 = 0, j = 0; s0 < ne; s0 += per_step, ++j) {
-      shard(ne, j, mine, job.eval_ids);
-      prepare(buf, mine.data(), static_cast<int>(mine.size()), 0, false);
-      launch(buf, false);
-      stats_to_host(hist + 3 * k++);
+    if (f_direct) cur_ring = &ring_plans_for(buf);
+    last_ring = buf.ring_features();
+    static_assert(sizeof(StepInputs) % 4 == 0, "StepInputs is copied in words");
+    const int words = static_cast<int>(sizeof(StepInputs) / 4);
+    kern::fetch_mapped(reinterpret_cast<const uint32_t*>(h_job), reinterpret_cast<uint32_t*>(d_job),
+                       words * static_cast<int>(total_launch), stream);
+    for (long long k = 0; k < total_launch; ++k) {
+      if (void* ev = buf.event_for(waits[k]))
+        SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(ev), 0));
+      kern::fetch_mapped(reinterpret_cast<const uint32_t*>(d_job + k),
+                         reinterpret_cast<uint32_t*>(d_in), words, stream);  // device -> device
+      launch(buf, is_train[k] != 0);
+      if (is_train[k]) step_count += 1;
+      stats_to_host(hist + 3 * k);
     }
     SPECSIM_CHECK_LAUNCH();
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
