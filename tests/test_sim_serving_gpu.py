@@ -58,7 +58,9 @@ def test_speculation_off_latency_model_and_conservation():
     assert (rows[:, 2] == 0).all() and (rows[:, 4] == b).all()
     # throughput for batch b is b / T(b) exactly (SPEC invariant)
     np.testing.assert_allclose(dt, [lat(x) for x in b], rtol=1e-12)
-    assert abs(dt[0] - 3.416) < 1e-12  # SPEC example: off, b = 1 -> 3.416 ms (concurrency 4: b = 4)
+    # SPEC example: speculation off, b = 1 -> clock += 3.416 ms, 1 token
+    _, one = run("speculation_off", requests=3, concurrency=1, mean_tokens=5, emit_iterations=1)
+    assert abs(one[0, 0] - 3.416) < 1e-12 and one[0, 4] == 1
 
 
 def test_speculation_on_iteration_latency_example():
