@@ -162,6 +162,7 @@ struct Engine {
   int64_t trainings = 0, deploys = 0, rejects = 0;
   double train_ms_total = 0;
   std::vector<double> phase_tokens, phase_ms;
+  std::string train_log;  // JSON objects of the training jobs
   double wall0;
 
   Engine(const Args& args, const WorkloadScript& script)
@@ -291,6 +292,16 @@ struct Engine {
     } else if (dec.action == -1) {
       ++rejects;
     }
+    char x[400];
+    std::snprintf(x, sizeof x,
+                  "%s{\"clock_ms\": %.3f, \"phase\": %d, \"n_train\": %lld, \"alpha_train\": "
+                  "%.4f, \"alpha_eval\": %.4f, \"duration_ms\": %.3f, \"action\": %d, "
+                  "\"alpha_deployed\": [%.4f, %.4f]}",
+                  train_log.empty() ? "" : ", ", clock, r.phase_index,
+                  static_cast<long long>(dec.n_train), dec.alpha_train, dec.outcome.alpha_eval,
+                  dur_ms, dec.action, dec.action == 1 ? pending_alpha[0] : -1.0,
+                  dec.action == 1 && pending_alpha.size() > 1 ? pending_alpha[1] : -1.0);
+    train_log += x;
   }
 
   // SPEC step: one decode iteration of the whole batch
@@ -385,7 +396,7 @@ int main(int argc, char** argv) {
         "\"collection_duty\": %.4f, \"flushes\": %lld, \"cumulative_storage_bytes\": %lld, "
         "\"buffer_bytes\": %lld, \"signal_records\": %lld, \"trainings\": %lld, \"deploys\": %lld, \"rejects\": %lld, "
         "\"train_ms\": %.3f, \"draft_version\": %lld, \"alpha_domain\": [%.4f, %.4f], "
-        "\"wall_s\": %.3f}\n",
+        "\"wall_s\": %.3f, \"jobs\": [%s]}\n",
         a.mode.c_str(), e.clock, static_cast<long long>(e.tokens),
         static_cast<long long>(script.total_output_tokens()), static_cast<long long>(e.iterations),
         1e3 * static_cast<double>(e.tokens) / e.clock,
@@ -398,7 +409,7 @@ int main(int argc, char** argv) {
         static_cast<long long>(e.trainings),
         static_cast<long long>(e.deploys), static_cast<long long>(e.rejects), e.train_ms_total,
         static_cast<long long>(e.ctrl.draft_version()), e.alpha_dom[0], e.alpha_dom[1],
-        Engine::now() - e.wall0);
+        Engine::now() - e.wall0, e.train_log.c_str());
     return 0;
   } catch (const ConfigError& e) {
     std::fprintf(stderr, "config error: %s\n", e.what());
