@@ -1,5 +1,5 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) for
-one step: the launches between the last two gather_batch kernels, grouped by
+one step: the launches between the last two gather kernels, grouped by
 kernel.  Usage: python scripts/launch_table.py launches.csv [--per-launch]"""
 import collections
 import csv
@@ -26,7 +26,8 @@ def short(n):
 
 def main():
     data = load(sys.argv[1])
-    idx = [i for i, d in enumerate(data) if "gather_batch" in d["Kernel Name"]]
+    idx = [i for i, d in enumerate(data)
+           if "gather_batch" in d["Kernel Name"] or "gather_tokens" in d["Kernel Name"]]
     st, en = (idx[-2], idx[-1]) if len(idx) >= 2 else (idx[-1], len(data))
     step = data[st:en]
     agg = collections.OrderedDict()

@@ -68,11 +68,12 @@ def short(name):
 
 
 def last_step(rows):
-    """Launches of the last complete step: from the last gather_batch_kernel to
+    """Launches of the last complete step: from the last gather kernel to
     the end (the step's trailing store_mapped included)."""
-    idx = [i for i, r in enumerate(rows) if "gather_batch_kernel" in r["name"]]
+    idx = [i for i, r in enumerate(rows)
+           if "gather_batch_kernel" in r["name"] or "gather_tokens_kernel" in r["name"]]
     if not idx:
-        raise SystemExit("no gather_batch_kernel launch in the capture")
+        raise SystemExit("no gather kernel launch in the capture")
     return rows[idx[-1]:]
 
 
@@ -89,6 +90,8 @@ def algorithmic(cfg, T):
     norm_fwd = 4 * H * T + 4 * T
     a = {
         "gather_batch_kernel": [("ring -> F rows + u/y/m", 2 * W3 * 2 * T + 8 * T + 12 * T)],
+        # u / y / m of one pass + the ids they read + the 64-row block table
+        "gather_tokens_kernel": [("ring ids -> u/y/m + block table", 24 * T + 4 * (T // 64))],
         "rmsnorm_fwd_kernel": [("a = RMSNorm(E[u])", norm_fwd), ("b = RMSNorm(g)", norm_fwd),
                                ("z = RMSNorm(r)", norm_fwd), ("n = RMSNorm(h)", norm_fwd)],
         "swiglu_fwd_kernel": [("act = silu(g) u", 6 * I * T)],
