@@ -65,6 +65,24 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -432,6 +450,412 @@ __global__ void __launch_bounds__(192, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_free[ob]);
+      lse[h * T + row0 + q] = (m_run + log2f(l_run)) * kLn2;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ======================================================================
+// Forward, two query tiles per CTA (default when the GQA group is even).
+//
+// A work item is (sample, query block, head pair): heads 2p and 2p + 1 of one
+// KV group see the same K / V blocks under the same causal mask, so every
+// K / V tile a CTA stages feeds two S MMAs and two PV MMAs, and two softmax
+// warpgroups (one per head; two warps per SM sub-partition) ping-pong with
+// the tensor pipe: while warpgroup 0 turns S0_n into P0_n, the MMA warp runs
+// PV1_{n-1} and S1_n, and vice versa.
+//   TMEM: S0 | S1 | O0 | O1 (128 columns each).  P_t is written back over the
+//   first 64 columns of S_t as packed bf16 (tcgen05.st) and read from TMEM
+//   by the PV MMA (A operand in tensor memory): no P traffic through shared
+//   memory, no async-proxy fence.  The pipe executes one issuer's MMAs in
+//   order, so S_{t,n+1} (issued after PV_{t,n}) overwrites P_{t,n} only after
+//   PV_{t,n} read it; S_{t,n+1} completing also implies PV_{t,n} completed, so
+//   the lazy O rescale needs no extra wait.
+//   smem: Q0 | Q1, K and V rings (2 slots each at hd 128, 3 at hd 64).
+// SPECSIM_ATTN_POLY_PAIRS of every four exponential pairs (off-diagonal
+// blocks) can run as a degree-4 polynomial on the FMA pipe (relative error
+// 2.6e-6, below the bf16 rounding of P) instead of MUFU.EX2, which issues one
+// warp instruction per 8 cycles per SM sub-partition (scripts/micro/mufu_rate.cu).
+#ifndef SPECSIM_ATTN_POLY_PAIRS
+#define SPECSIM_ATTN_POLY_PAIRS 0
+#endif
+
+template <int HD>
+struct Fwd2Smem {
+  static constexpr int ATOMS = HD / 64;
+  static constexpr int Q = ATOMS * TILE;              // one query tile [128 q x HD]
+  static constexpr int KV = ATOMS * TILE;             // one K or V block [128 keys x HD]
+  static constexpr int NSLOT = HD == 128 ? 2 : 3;     // slots per K / V ring
+  static constexpr int OFF_Q = 0;                     // 2 tiles
+  static constexpr int OFF_K = OFF_Q + 2 * Q;
+  static constexpr int OFF_V = OFF_K + NSLOT * KV;
+  static constexpr int OFF_BAR = OFF_V + NSLOT * KV;  // mbarriers + the TMEM slot
+  static constexpr int BYTES = 1024 + OFF_BAR + 256;
+};
+
+// 2^x for two values on the FMA pipe: x = j + f, j = rint(x) (the 1.5 * 2^23
+// shifter), 2^f by a degree-4 minimax polynomial on [-0.5, 0.5] (relative
+// error 2.6e-6), 2^j added to the exponent field.  x is clamped at -120 so
+// the exponent never underflows (2^-120 stands in for anything smaller).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float x0, x1;
+  ptx::f32x2_split(x2, x0, x1);
+  const uint64_t x = ptx::f32x2(fmaxf(x0, -120.f), fmaxf(x1, -120.f));
+  const uint64_t t = ptx::fadd2(x, ptx::f32x2(12582912.f, 12582912.f));
+  const uint64_t jf = ptx::fadd2(t, ptx::f32x2(-12582912.f, -12582912.f));
+  const uint64_t f = ptx::ffma2(jf, ptx::f32x2(-1.f, -1.f), x);
+  uint64_t p = ptx::ffma2(ptx::f32x2(0.009570068679749966f, 0.009570068679749966f), f,
+                          ptx::f32x2(0.055917806923389435f, 0.055917806923389435f));
+  p = ptx::ffma2(p, f, ptx::f32x2(0.240247443318367f, 0.240247443318367f));
+  p = ptx::ffma2(p, f, ptx::f32x2(0.6931218504905701f, 0.6931218504905701f));
+  p = ptx::ffma2(p, f, ptx::f32x2(0.9999992847442627f, 0.9999992847442627f));
+  float p0, p1, t0, t1;
+  ptx::f32x2_split(p, p0, p1);
+  ptx::f32x2_split(t, t0, t1);
+  return ptx::f32x2(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23)),
+                    __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23)));
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]: A (M x 16, bf16 packed two per 32-bit
+// column, row m in TMEM lane m) read from tensor memory
+__device__ __forceinline__ void umma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+                        float* __restrict__ lse, Dims d) {
+  using L = Fwd2Smem<HD>;
+  constexpr int NS = L::NSLOT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* k_full = bar + 2;        // [NS]
+  uint64_t* k_empty = k_full + NS;   // [NS]
+  uint64_t* v_full = k_empty + NS;   // [NS]
+  uint64_t* v_empty = v_full + NS;   // [NS]
+  uint64_t* s_full = v_empty + NS;   // [2] per tile
+  uint64_t* p_full = s_full + 2;     // [2]
+  uint64_t* o_full = p_full + 2;     // [2]
+  uint64_t* o_free = o_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int nqb = d.S / BQ;
+  const int nhp = d.nh / 2;
+  const int n_items = nqb * nhp * d.B;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nd = d.n_diag;
+  auto decode = [&](int idx, int& qb, int& hp, int& b) {
+    qb = nqb - 1 - idx / (nhp * d.B);
+    const int hb = idx % (nhp * d.B);
+    hp = hb % nhp;
+    b = hb / nhp;
+  };
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm);
+    ptx::mbar_init(q_full, 1);
+    // Q is free after the item's last S MMAs; with training-time-test cache
+    // entries the eight softmax warps' epilogues also read it
+    ptx::mbar_init(q_empty, nd > 0 ? 9 : 1);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 4);
+      ptx::mbar_init(&o_full[t], 1);
+      ptx::mbar_init(&o_free[t], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA
+      constexpr int A = L::ATOMS;
+      int n = 0;  // key block counter across items (K / V ring position)
+      for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+        int qb, hp, b;
+        decode(idx, qb, hp, b);
+        const int h0 = 2 * hp, g = h0 / (d.nh / d.nkv), row0 = b * d.S;
+        ptx::mbar_wait(q_empty, (li & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(q_full, 2 * L::Q);
+        for (int t = 0; t < 2; ++t)
+          for (int a = 0; a < A; ++a)
+            ptx::tma_load_2d(&tm, q_full, sQ + t * L::Q + a * TILE, (h0 + t) * HD + 64 * a,
+                             static_cast<int>(d.q_row_off) + row0 + qb * BQ);
+        for (int j = 0; j <= qb; ++j, ++n) {
+          const int s = n % NS;
+          const uint32_t ph = ((n / NS) & 1) ^ 1;
+          ptx::mbar_wait(&k_empty[s], ph);
+          ptx::mbar_arrive_expect_tx(&k_full[s], L::KV);
+          for (int a = 0; a < A; ++a)
+            ptx::tma_load_2d(&tm, &k_full[s], sK + s * L::KV + a * TILE, d.Q + g * HD + 64 * a,
+                             row0 + j * BKV);
+          ptx::mbar_wait(&v_empty[s], ph);
+          ptx::mbar_arrive_expect_tx(&v_full[s], L::KV);
+          for (int a = 0; a < A; ++a)
+            ptx::tma_load_2d(&tm, &v_full[s], sV + s * L::KV + a * TILE,
+                             d.Q + d.KV + g * HD + 64 * a, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA
+      constexpr uint32_t idS = ptx::make_idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idO = ptx::make_idesc_bf16(BQ, HD, false, true);
+      // S_t = Q_t K_n^T into the S_t columns
+      auto issue_s = [&](int t, int n) {
+        if (t == 0) {
+          ptx::mbar_wait(&k_full[n % NS], (n / NS) & 1);
+          ptx::tc_fence_after();
+        }
+        const uint32_t aQ = ptx::smem_u32(sQ + t * L::Q);
+        const uint32_t aK = ptx::smem_u32(sK + (n % NS) * L::KV);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::umma_bf16(tmem + t * 128, kdesc(aQ, kk), kdesc(aK, kk), idS, kk > 0 ? 1u : 0u);
+        ptx::umma_commit(&s_full[t]);
+        if (t == 1) ptx::umma_commit(&k_empty[n % NS]);
+      };
+      int n = 0;
+      for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+        int qb, hp, b;
+        decode(idx, qb, hp, b);
+        const int nkv = qb + 1;
+        ptx::mbar_wait(q_full, li & 1);
+        issue_s(0, n);
+        issue_s(1, n);
+        if (nkv == 1) ptx::umma_commit(q_empty);
+        for (int j = 0; j < nkv; ++j, ++n) {
+          ptx::mbar_wait(&v_full[n % NS], (n / NS) & 1);
+          const uint32_t aV = ptx::smem_u32(sV + (n % NS) * L::KV);
+          for (int t = 0; t < 2; ++t) {
+            // O_t was last read by the epilogue of the previous item
+            if (j == 0) ptx::mbar_wait(&o_free[t], (li & 1) ^ 1);
+            ptx::mbar_wait(&p_full[t], n & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk)
+              umma_bf16_ta(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mndesc(aV, kk), idO,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+            if (t == 1) ptx::umma_commit(&v_empty[n % NS]);
+            if (j == nkv - 1) {
+              ptx::umma_commit(&o_full[t]);
+            } else {
+              // S_{t,n+1} overwrites P_{t,n}: issued after PV_{t,n} (in-order pipe)
+              issue_s(t, n + 1);
+              if (t == 1 && j + 1 == nkv - 1) ptx::umma_commit(q_empty);
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int tile = (warp - 2) >> 2;  // warpgroup = head of the pair
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;    // query row within the block (= TMEM lane)
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + tile * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + tile * 128 + lane_off;
+    const uint8_t* sQt = sQ + tile * L::Q;
+    const float sl2 = d.scale * kLog2e;
+    const long long T = static_cast<long long>(d.B) * d.S;
+    int n = 0;
+    for (int li = 0, idx = blockIdx.x; idx < n_items; ++li, idx += gridDim.x) {
+      int qb, hp, b;
+      decode(idx, qb, hp, b);
+      const int h = 2 * hp + tile, g = h / (d.nh / d.nkv), row0 = b * d.S;
+      const int q = qb * BQ + r;
+      const int nkv = qb + 1;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nkv; ++j, ++n) {
+        ptx::mbar_wait(&s_full[tile], n & 1);
+        ptx::tc_fence_after();
+        uint32_t v[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x32(tS + c * 32, v[c]);
+        ptx::tmem_ld_wait();
+        const bool diag = j == qb;
+        if (diag) {  // keys after the query are masked
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i > r) v[c][i] = __float_as_uint(-INFINITY);
+        }
+        float mxp[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            mxp[0] = ptx::max3f(mxp[0], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
+            mxp[1] =
+                ptx::max3f(mxp[1], __uint_as_float(v[c][i + 2]), __uint_as_float(v[c][i + 3]));
+            mxp[2] =
+                ptx::max3f(mxp[2], __uint_as_float(v[c][i + 4]), __uint_as_float(v[c][i + 5]));
+            mxp[3] =
+                ptx::max3f(mxp[3], __uint_as_float(v[c][i + 6]), __uint_as_float(v[c][i + 7]));
+          }
+        const float mx = ptx::max3f(mxp[0], mxp[1], fmaxf(mxp[2], mxp[3])) * sl2;
+        // lazy rescale (see attn_fwd_tc_kernel): only when the row max grows
+        // by more than 2^8.  S_{t,n} complete implies PV_{t,n-1} complete.
+        const bool need = mx > m_run + 8.f;
+        float corr = 1.f;
+        if (need) {
+          corr = exp2f(m_run - mx);  // 0 on the first block
+          l_run *= corr;
+          m_run = mx;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          // 16-column pieces: the 128 scores stay live in registers meanwhile
+#pragma unroll 1
+          for (int c = 0; c < HD / 16; ++c) {
+            uint32_t o[16];
+            tmem_ld_32x32b_x16(tO + c * 16, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st_32x32b_x16(tO + c * 16, o);
+          }
+        }
+        // P = 2^(s * scale * log2e - m) -> packed bf16, written over S_t
+        // columns [0, 64) in two 64-key halves
+        const uint64_t scale2 = ptx::f32x2(sl2, sl2), negm2 = ptx::f32x2(-m_run, -m_run);
+        uint64_t lp2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hf + cc;
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const bool poly = !diag && ((i >> 1) & 3) < SPECSIM_ATTN_POLY_PAIRS;
+              const uint64_t x2 = ptx::ffma2(
+                  ptx::f32x2(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])), scale2,
+                  negm2);
+              uint64_t p2;
+              if (poly) {
+                p2 = exp2_poly2(x2);
+              } else {
+                float x0, x1;
+                ptx::f32x2_split(x2, x0, x1);
+                p2 = ptx::f32x2(ptx::ex2_ftz(x0), ptx::ex2_ftz(x1));
+              }
+              lp2[(i >> 1) & 3] = ptx::fadd2(lp2[(i >> 1) & 3], p2);
+              pk[cc * 16 + (i >> 1)] = ptx::pack_bf16x2_2(p2);
+            }
+          }
+          tmem_st_32x32b_x32(tS + hf * 32, pk);
+        }
+        {
+          float a0, a1;
+          ptx::f32x2_split(ptx::fadd2(ptx::fadd2(lp2[0], lp2[1]), ptx::fadd2(lp2[2], lp2[3])),
+                           a0, a1);
+          l_run += a0 + a1;
+        }
+        tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[tile]);
+      }
+      // ---- epilogue of the item: O_t -> bf16 rows, lse
+      ptx::mbar_wait(&o_full[tile], li & 1);
+      ptx::tc_fence_after();
+      float pd[kMaxDiag];
+      float corr = 1.f;
+      if (nd > 0) {  // training-time-test cache entries (see attn_fwd_tc_kernel)
+        float mnew = m_run;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          const uint4* kr = reinterpret_cast<const uint4*>(
+              d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + g * HD);
+          float dot = 0.f;
+#pragma unroll
+          for (int c8 = 0; c8 < HD / 8; ++c8) {
+            const uint4 qv = *reinterpret_cast<const uint4*>(
+                sQt + (c8 >> 3) * TILE + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
+            const uint4 kv = __ldg(kr + c8);
+            dot += ptx::dot_bf16x8(qv, kv);
+          }
+          pd[i] = dot * sl2;
+          mnew = fmaxf(mnew, pd[i]);
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(q_empty);
+        corr = exp2f(m_run - mnew);
+        l_run *= corr;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          pd[i] = exp2f(pd[i] - mnew);
+          l_run += pd[i];
+        }
+        m_run = mnew;
+      }
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* orow = out + static_cast<long long>(row0 + q) * d.Q + h * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        ptx::tmem_ld_32x32b_x32(tO + c * 32, o);
+        ptx::tmem_ld_wait();
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(o[i]) * corr;
+#pragma unroll 1
+        for (int i = 0; i < nd; ++i) {
+          const uint4* vr = reinterpret_cast<const uint4*>(
+              d.diag_qkv + (static_cast<long long>(i + 1) * T + row0 + q) * d.NQ + d.Q + d.KV +
+              g * HD + c * 32);
+#pragma unroll
+          for (int v8 = 0; v8 < 4; ++v8) {
+            float vf[8];
+            ptx::unpack_bf16x8(__ldg(vr + v8), vf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[v8 * 8 + e] += pd[i] * vf[e];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          ptx::st_global_v4(orow + c * 32 + i, ptx::pack_bf16x2(acc[i] * inv, acc[i + 1] * inv),
+                            ptx::pack_bf16x2(acc[i + 2] * inv, acc[i + 3] * inv),
+                            ptx::pack_bf16x2(acc[i + 4] * inv, acc[i + 5] * inv),
+                            ptx::pack_bf16x2(acc[i + 6] * inv, acc[i + 7] * inv));
+      }
+      // O_t read: the next item's first PV may overwrite it
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&o_free[tile]);
       lse[h * T + row0 + q] = (m_run + log2f(l_run)) * kLn2;
     }
   }
@@ -1035,10 +1459,30 @@ void forward_tc_t(const __nv_bfloat16* qkv, __nv_bfloat16* o, float* lse, const 
     const char* e = std::getenv("SPECSIM_ATTN_FWD_GRID");
     return e && std::string(e) == "items";
   }();
-  const int n_items = (d.S / BQ) * d.nh * d.B;
+  // two query tiles (a head pair of one KV group) per CTA unless the GQA
+  // group is odd (SPECSIM_ATTN_FWD1=1: the one-tile kernel)
+  static const bool one_tile = [] {
+    const char* e = std::getenv("SPECSIM_ATTN_FWD1");
+    return e && e[0] == '1';
+  }();
   int dev = 0, sms = 0;
   SPECSIM_CUDA(cudaGetDevice(&dev));
   SPECSIM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (!one_tile && !per_item && (d.nh / d.nkv) % 2 == 0) {
+    constexpr int smem2 = Fwd2Smem<HD>::BYTES;
+    static_assert(smem2 <= 232448, "attention smem budget");
+    static bool init2 = false;
+    if (!init2) {
+      SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd2_tc_kernel<HD>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      init2 = true;
+    }
+    const int n_items2 = (d.S / BQ) * (d.nh / 2) * d.B;
+    count_launches();
+    attn_fwd2_tc_kernel<HD><<<std::min(n_items2, sms), 320, smem2, s>>>(tm, o, lse, d);
+    return;
+  }
+  const int n_items = (d.S / BQ) * d.nh * d.B;
   const int grid = per_item ? n_items : std::min(n_items, sms);
   count_launches();
   attn_fwd_tc_kernel<HD><<<grid, 192, smem, s>>>(tm, o, lse, d);
@@ -1269,14 +1713,21 @@ void prepare_tc(int hd) {
     prepare_bwd_t<128>();
   else
     prepare_bwd_t<64>();
-  if (hd == 128)
+  if (hd == 128) {
     SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<128>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FwdSmem<128>::BYTES));
-  else
+    SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd2_tc_kernel<128>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Fwd2Smem<128>::BYTES));
+  } else {
     SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<64>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FwdSmem<64>::BYTES));
+    SPECSIM_CUDA(cudaFuncSetAttribute(attn_fwd2_tc_kernel<64>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Fwd2Smem<64>::BYTES));
+  }
 }
 
 }  // namespace attn
