@@ -44,6 +44,11 @@
 // while chunk c is processed
 #define SPECSIM_ADAMW_PREFETCH 0
 #endif
+#ifndef SPECSIM_ADAMW_LDNA
+// 1: optimizer-state loads of the 256-bit epilogue bypass L1 allocation
+// (ld.global.L1::no_allocate) instead of the evict-first streaming hint
+#define SPECSIM_ADAMW_LDNA 0
+#endif
 #ifndef SPECSIM_ADAMW_WINDOW
 // probe only (scripts/adamw_probe.sh): > 0 folds every optimizer-state access
 // of the 256-bit epilogue into a window of this many elements (a power of 2),
@@ -522,9 +527,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               gv[it][0] = a.x; gv[it][1] = a.y; gv[it][2] = a.z; gv[it][3] = a.w;
               gv[it][4] = b.x; gv[it][5] = b.y; gv[it][6] = b.z; gv[it][7] = b.w;
               if (ok[it]) {
-                ptx::ld_cs_v8(args.opt_p + e[it], pv[it]);
-                ptx::ld_cs_v8(args.opt_m + e[it], mv[it]);
-                ptx::ld_cs_v8(args.opt_v + e[it], vv[it]);
+                if constexpr (SPECSIM_ADAMW_LDNA) {
+                  ptx::ld_na_v8(args.opt_p + e[it], pv[it]);
+                  ptx::ld_na_v8(args.opt_m + e[it], mv[it]);
+                  ptx::ld_na_v8(args.opt_v + e[it], vv[it]);
+                } else {
+                  ptx::ld_cs_v8(args.opt_p + e[it], pv[it]);
+                  ptx::ld_cs_v8(args.opt_m + e[it], mv[it]);
+                  ptx::ld_cs_v8(args.opt_v + e[it], vv[it]);
+                }
               }
             }
 #pragma unroll

@@ -326,6 +326,13 @@ __device__ __forceinline__ void ld_cs_v8(const float* p, float (&v)[8]) {
                  "=f"(v[6]), "=f"(v[7])
                : "l"(p));
 }
+// same, bypassing L1 allocation (the data goes straight to registers)
+__device__ __forceinline__ void ld_na_v8(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
 __device__ __forceinline__ void st_cs_v8(float* p, const float (&v)[8]) {
   asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
                "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
