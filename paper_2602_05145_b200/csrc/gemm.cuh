@@ -46,8 +46,9 @@
 #endif
 #ifndef SPECSIM_ADAMW_LDNA
 // 1: optimizer-state loads of the 256-bit epilogue bypass L1 allocation
-// (ld.global.L1::no_allocate) instead of the evict-first streaming hint
-#define SPECSIM_ADAMW_LDNA 0
+// (ld.global.L1::no_allocate) instead of the evict-first streaming hint;
+// 2: the same plus an L2 evict-first cache-hint policy
+#define SPECSIM_ADAMW_LDNA 1
 #endif
 #ifndef SPECSIM_ADAMW_WINDOW
 // probe only (scripts/adamw_probe.sh): > 0 folds every optimizer-state access
@@ -527,7 +528,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               gv[it][0] = a.x; gv[it][1] = a.y; gv[it][2] = a.z; gv[it][3] = a.w;
               gv[it][4] = b.x; gv[it][5] = b.y; gv[it][6] = b.z; gv[it][7] = b.w;
               if (ok[it]) {
-                if constexpr (SPECSIM_ADAMW_LDNA) {
+                if constexpr (SPECSIM_ADAMW_LDNA == 2) {
+                  const uint64_t pol = ptx::policy_evict_first();
+                  ptx::ld_na_hint_v8(args.opt_p + e[it], pv[it], pol);
+                  ptx::ld_na_hint_v8(args.opt_m + e[it], mv[it], pol);
+                  ptx::ld_na_hint_v8(args.opt_v + e[it], vv[it], pol);
+                } else if constexpr (SPECSIM_ADAMW_LDNA == 1) {
                   ptx::ld_na_v8(args.opt_p + e[it], pv[it]);
                   ptx::ld_na_v8(args.opt_m + e[it], mv[it]);
                   ptx::ld_na_v8(args.opt_v + e[it], vv[it]);

@@ -333,6 +333,20 @@ __device__ __forceinline__ void ld_na_v8(const float* p, float (&v)[8]) {
                  "=f"(v[6]), "=f"(v[7])
                : "l"(p));
 }
+// no L1 allocation, L2 eviction policy from createpolicy (evict-first streams)
+__device__ __forceinline__ void ld_na_hint_v8(const float* p, float (&v)[8], uint64_t pol) {
+  asm volatile(
+      "ld.global.L1::no_allocate.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], "
+      "%9;"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void st_cs_v8(float* p, const float (&v)[8]) {
   asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
                "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
