@@ -1230,8 +1230,9 @@ __global__ void __launch_bounds__(192, 1)
 
 // dQ kernel: one CTA = (sample, query head, 128-query block); loops over the
 // key blocks up to the diagonal.  S = Q K^T and dP = dO V^T (M = 128 q,
-// N = 128 keys) into TMEM; dS = P (dP - D) as a bf16 K-major smem tile; then
-// dQ += dS K with the K tile doubling as an MN-major B operand.
+// N = 128 keys) into TMEM; dS = P (dP - D) written back over S as packed bf16
+// (tcgen05.st); then dQ += dS K with dS as the TMEM A operand and the K tile
+// doubling as an MN-major B operand.
 template <int HD>
 struct QSmem {
   static constexpr int ATOMS = HD / 64;
@@ -1240,8 +1241,7 @@ struct QSmem {
   static constexpr int OFF_DO = OFF_Q + T128;
   static constexpr int OFF_K = OFF_DO + T128;   // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * T128;  // 2 stages
-  static constexpr int OFF_DS = OFF_V + 2 * T128;
-  static constexpr int OFF_BAR = OFF_DS + 2 * TILE;
+  static constexpr int OFF_BAR = OFF_V + 2 * T128;
   static constexpr int BYTES = 1024 + OFF_BAR + 256;
 };
 
@@ -1260,8 +1260,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* k_full = bar + 1;   // [2]
   uint64_t* k_empty = bar + 3;  // [2]
   uint64_t* s_full = bar + 5;
-  uint64_t* ds_full = bar + 7;  // (bar + 6 unused)
-  uint64_t* ds_free = bar + 8;
+  uint64_t* ds_full = bar + 7;  // (bar + 6, bar + 8 unused)
   uint64_t* all_done = bar + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
@@ -1283,7 +1282,6 @@ __global__ void __launch_bounds__(192, 1)
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(ds_full, 4);
-    ptx::mbar_init(ds_free, 1);
     ptx::mbar_init(all_done, 1);
     ptx::fence_barrier_init();
   }
@@ -1323,7 +1321,6 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idS = ptx::make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idQ = ptx::make_idesc_bf16(BQ, HD, false, true);
       const uint32_t aQ = ptx::smem_u32(smem + L::OFF_Q), adO = ptx::smem_u32(smem + L::OFF_DO);
-      const uint32_t aS = ptx::smem_u32(smem + L::OFF_DS);
       ptx::mbar_wait(q_full, 0);
       // S_j into buffer j & 1; that buffer last held S_{j-2}, released by the
       // s_free of block j-2, which issuing dP_{j-1} already waited for
@@ -1355,10 +1352,13 @@ __global__ void __launch_bounds__(192, 1)
         // dP_{j+1} first, so the softmax of j+1 starts while dQ_j runs
         if (j + 1 < nkv) issue_dp(j + 1);
         const uint32_t aK = ptx::smem_u32(smem + L::OFF_K + st * L::T128);
+        // dS_j (bf16, packed over the first 64 columns of S_j's TMEM buffer)
+        // is the A operand; S_{j+2} overwrites it only after these MMAs (one
+        // issuer's MMAs run in order)
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          ptx::umma_bf16(tdQ, kdesc(aS, kk), mndesc(aK, kk), idQ, (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::umma_commit(ds_free);
+          umma_bf16_ta(tdQ, tS + (j & 1) * 256 + kk * 8, mndesc(aK, kk), idQ,
+                       (j > 0 || kk > 0) ? 1u : 0u);
         ptx::umma_commit(&k_empty[st]);
         // S_{j+2} reuses S_j's buffer and K stage j & 1 (refilled once dQ_j is done)
         if (j + 2 < nkv) issue_s(j + 2);
@@ -1375,15 +1375,15 @@ __global__ void __launch_bounds__(192, 1)
     const float Dr = Dv[h * T + row0 + q];
     const uint64_t sl2x2 = ptx::f32x2(sl2, sl2), nl2x2 = ptx::f32x2(-l2, -l2),
                    nD2 = ptx::f32x2(-Dr, -Dr);
-    uint8_t* sS = smem + L::OFF_DS;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(s_full, j & 1);
       ptx::tc_fence_after();
       const bool diag = (j == qb);
+      const uint32_t tSj = tS + (j & 1) * 256 + lane_off;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t sv[32], pv[32];
-        ptx::tmem_ld_32x32b_x32(tS + (j & 1) * 256 + lane_off + c * 32, sv);
+        ptx::tmem_ld_32x32b_x32(tSj + c * 32, sv);
         ptx::tmem_ld_32x32b_x32(tdP + lane_off + c * 32, pv);
         ptx::tmem_ld_wait();
         uint32_t ddc[4][4];
@@ -1410,21 +1410,18 @@ __global__ void __launch_bounds__(192, 1)
                            nD2)));
           }
         }
-        // dS goes straight into the (single) smem tile: the first chunk's
-        // math above overlaps the dQ MMA of j-1, which must be done reading it
-        if (c == 0) ptx::mbar_wait(ds_free, (j & 1) ^ 1);
+        // dS chunk c (32 keys -> 16 packed columns) over S_j's columns
+        // [16 c, 16 c + 16): this chunk's S values are already in registers and
+        // later chunks read columns >= 32 (c + 1) > 16 c + 16
+        uint32_t dsw[16];
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          const int key = c * 32 + i;
-          const int t = key >> 6, cc = (key & 63) >> 3;
-          *reinterpret_cast<uint4*>(sS + t * TILE + r * 128 + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(ddc[i >> 3][0], ddc[i >> 3][1], ddc[i >> 3][2], ddc[i >> 3][3]);
-        }
+        for (int i = 0; i < 16; ++i) dsw[i] = ddc[i >> 2][i & 3];
+        tmem_st_32x32b_x16(tSj + c * 16, dsw);
       }
+      tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(ds_full);  // also frees S_j and dP for the MMA warp
+      if (lane == 0) ptx::mbar_arrive(ds_full);  // also frees dP for the MMA warp
     }
     ptx::mbar_wait(all_done, 0);
     ptx::tc_fence_after();
