@@ -305,6 +305,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::prefetch_l2_bulk(args.opt_v + e, 4u * ncol);
         }
       }
+      // SwiGLU backward: the gate / up values of the first 32-column chunk are
+      // loaded before the accumulator wait (their DRAM latency hides behind
+      // the tile's mainloop); later chunks are loaded one chunk ahead
+      uint2 sw_g[8], sw_u[8];
+      auto sw_load = [&](int c, uint2 (&g)[8], uint2 (&u)[8]) {
+        const int col = n0 + c + (lane & 7) * 4;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = m0 + quad * 32 + it * 4 + (lane >> 3);
+          if (rr < args.M && col < args.N) {
+            const __nv_bfloat16* gp = args.R + static_cast<long long>(rr) * args.ldr + col;
+            g[it] = *reinterpret_cast<const uint2*>(gp);
+            u[it] = *reinterpret_cast<const uint2*>(gp + args.N);
+          }
+        }
+      };
+      if constexpr (EPI == EPI_SWIGLU_BWD) sw_load(c_begin, sw_g, sw_u);
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const int row_base = m0 + quad * 32;
@@ -476,6 +493,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   make_uint2(ptx::pack_bf16x2(w.x, w.y), ptx::pack_bf16x2(w.z, w.w));
           }
         }
+      } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+        // d act rounded to bf16 (the operand the unfused path stores), then
+        // silu' with the stored bf16 gate / up, as swiglu_bwd_kernel; the
+        // 32x32 chunk is staged through smem (4 columns x 8 rows per lane)
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += 32) {
+          uint32_t r[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(t_row + c, r);
+          ptx::tmem_ld_wait();
+          const int col0 = n0 + c;
+          if (col0 >= args.N) continue;  // warp-uniform
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(stg + lane * 36 + i) =
+                make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                            __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          __syncwarp();
+          uint2 nx_g[8], nx_u[8];
+          if (c + 32 < c_end) sw_load(c + 32, nx_g, nx_u);
+          const int cl = (lane & 7) * 4;
+          const int col = col0 + cl;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + (lane >> 3);
+            const int rr = row_base + rl;
+            if (rr >= args.M || col >= args.N) continue;
+            const float4 w = *reinterpret_cast<const float4*>(stg + rl * 36 + cl);
+            const float wa[4] = {w.x, w.y, w.z, w.w};
+            const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sw_g[it].x));
+            const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sw_g[it].y));
+            const float2 u01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sw_u[it].x));
+            const float2 u23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sw_u[it].y));
+            const float gv[4] = {g01.x, g01.y, g23.x, g23.y};
+            const float uv[4] = {u01.x, u01.y, u23.x, u23.y};
+            float dg[4], du[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float dv = __bfloat162float(__float2bfloat16_rn(wa[j]));
+              const float sg = 1.f / (1.f + __expf(-gv[j]));
+              dg[j] = dv * uv[j] * sg * (1.f + gv[j] * (1.f - sg));
+              du[j] = dv * gv[j] * sg;
+            }
+            __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(args.C) +
+                                static_cast<long long>(rr) * args.ldc + col;
+            *reinterpret_cast<uint2*>(cp) =
+                make_uint2(ptx::pack_bf16x2(dg[0], dg[1]), ptx::pack_bf16x2(dg[2], dg[3]));
+            *reinterpret_cast<uint2*>(cp + args.N) =
+                make_uint2(ptx::pack_bf16x2(du[0], du[1]), ptx::pack_bf16x2(du[2], du[3]));
+          }
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            sw_g[it] = nx_g[it];
+            sw_u[it] = nx_u[it];
+          }
+        }
       } else if constexpr (EPI == EPI_ADAMW && SPECSIM_ADAMW_VARIANT == 0) {
         // Fused AdamW on the gradient tile.  The 32x32 chunk is staged through
         // smem and walked 4 lanes x 8 columns per row (8 rows per warp
@@ -627,14 +700,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 x1[it].x = __uint_as_float(q.x);
                 x1[it].y = __uint_as_float(q.y);
               }
-            } else if constexpr (EPI == EPI_SWIGLU_BWD) {
-              if (okm >> it & 1) {  // gate | up of these 4 columns
-                const __nv_bfloat16* gp = args.R + static_cast<long long>(rr) * args.ldr + col;
-                const uint2 qg = *reinterpret_cast<const uint2*>(gp);
-                const uint2 qu = *reinterpret_cast<const uint2*>(gp + args.N);
-                x1[it] = make_float4(__uint_as_float(qg.x), __uint_as_float(qg.y),
-                                     __uint_as_float(qu.x), __uint_as_float(qu.y));
-              }
             } else if constexpr (EPI == EPI_F32_ACC) {
               if (okm >> it & 1)
                 x1[it] = *reinterpret_cast<const float4*>(static_cast<const float*>(args.C) + e_it);
@@ -667,36 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const long long e_it = SPECSIM_E(it);
             float4 w = v[it];
             float* wa = &w.x;
-            if constexpr (EPI == EPI_SWIGLU_BWD) {
-              // d act rounded to bf16 (the operand the unfused path stores),
-              // then silu' with the stored bf16 gate / up, as swiglu_bwd_kernel
-              uint32_t qb[4] = {__float_as_uint(x1[it].x), __float_as_uint(x1[it].y),
-                                __float_as_uint(x1[it].z), __float_as_uint(x1[it].w)};
-              float gv[4], uv[4], dg[4], du[4];
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const float2 gg =
-                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qb[j]));
-                const float2 uu =
-                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qb[2 + j]));
-                gv[2 * j] = gg.x;
-                gv[2 * j + 1] = gg.y;
-                uv[2 * j] = uu.x;
-                uv[2 * j + 1] = uu.y;
-              }
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float dv = __bfloat162float(__float2bfloat16_rn(wa[j]));
-                const float sg = 1.f / (1.f + __expf(-gv[j]));
-                dg[j] = dv * uv[j] * sg * (1.f + gv[j] * (1.f - sg));
-                du[j] = dv * gv[j] * sg;
-              }
-              __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(args.C) + e_it;
-              *reinterpret_cast<uint2*>(cp) =
-                  make_uint2(ptx::pack_bf16x2(dg[0], dg[1]), ptx::pack_bf16x2(dg[2], dg[3]));
-              *reinterpret_cast<uint2*>(cp + args.N) =
-                  make_uint2(ptx::pack_bf16x2(du[0], du[1]), ptx::pack_bf16x2(du[2], du[3]));
-            } else if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
+            if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RESID || EPI == EPI_CE_BWD) {
               if constexpr (EPI == EPI_BF16_RESID) {
                 uint32_t q0 = __float_as_uint(x1[it].x), q1 = __float_as_uint(x1[it].y);
                 const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q0));

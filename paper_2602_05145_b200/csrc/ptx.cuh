@@ -176,11 +176,22 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // Arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster.
+// SPECSIM_REMOTE_ARRIVE_CTA: release at CTA scope (the PTX default) instead of
+// cluster scope -- the arrive then does not wait for this thread's earlier
+// global stores to be performed cluster-wide; the GEMM's accumulator hand-off
+// (tcgen05.ld -> wait::ld -> tcgen05.fence::before_thread_sync -> arrive)
+// only needs the tensor-memory reads ordered, which the tcgen05 fence does
+#ifndef SPECSIM_REMOTE_ARRIVE_CTA
+#define SPECSIM_REMOTE_ARRIVE_CTA 1
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
-               : "memory");
+  if (SPECSIM_REMOTE_ARRIVE_CTA)
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  else
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                 : "memory");
 }
 
 // ---------------------------------------------------------------- tcgen05
