@@ -66,7 +66,7 @@ def leg_jobs_resident():
 
 
 out = {}
-for rep in range(2):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
     for _ in range(3):
         tr.train(buf, append_job(JOB, 0), [], epochs=1)  # warm-up
     out[f"a_e2e_{rep}"] = region(leg_e2e)
