@@ -1002,8 +1002,11 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * QS);
   float* sLD = reinterpret_cast<float*>(smem + L::OFF_LD);
 
-  const int kb = blockIdx.x;  // key block; early keys see the most queries
-  const int g = blockIdx.y, b = blockIdx.z;
+  // key block on the slowest grid axis: CTAs are dispatched in launch order,
+  // so every early key block (the most queries, up to 16x the work of the
+  // last) starts in the first waves instead of some of them forming the tail
+  const int kb = blockIdx.z;
+  const int g = blockIdx.x, b = blockIdx.y;
   const int rep = d.nh / d.nkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = b * d.S;
@@ -1264,8 +1267,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* all_done = bar + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
-  const int qb = gridDim.x - 1 - blockIdx.x;  // most keys first
-  const int h = blockIdx.y, b = blockIdx.z;
+  // query block on the slowest grid axis, most keys first (see the dK/dV kernel)
+  const int qb = gridDim.z - 1 - blockIdx.z;
+  const int h = blockIdx.x, b = blockIdx.y;
   const int g = h / (d.nh / d.nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = b * d.S;
@@ -1614,7 +1618,7 @@ void bwd_dq_t(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout, const flo
   const CUtensorMap kv = gemm::make_tensor_map(qkv_all, d.q_row_off + T, d.NQ, d.NQ, 64, 128);
   const CUtensorMap do128 = gemm::make_tensor_map(dout, T, d.Q, d.Q, 64, 128);
   count_launches();
-  attn_bwd_q_tc_kernel<HD><<<dim3(d.S / BQ, d.nh, d.B), 192, QSmem<HD>::BYTES, s>>>(
+  attn_bwd_q_tc_kernel<HD><<<dim3(d.nh, d.B, d.S / BQ), 192, QSmem<HD>::BYTES, s>>>(
       kv, do128, lse, D, dq_add, dqkv_step, d);
 }
 
@@ -1627,7 +1631,7 @@ void bwd_dkdv_t(const __nv_bfloat16* qkv_all, const __nv_bfloat16* dout_all, con
   const CUtensorMap q64 = gemm::make_tensor_map(qkv_all, n_steps * T, d.NQ, d.NQ, 64, 64);
   const CUtensorMap do64 = gemm::make_tensor_map(dout_all, n_steps * T, d.Q, d.Q, 64, 64);
   count_launches();
-  attn_bwd_kv_tc_kernel<HD><<<dim3(d.S / BKV, d.nkv, d.B), 192, KvSmem<HD>::BYTES, s>>>(
+  attn_bwd_kv_tc_kernel<HD><<<dim3(d.nkv, d.B, d.S / BKV), 192, KvSmem<HD>::BYTES, s>>>(
       kv, q64, do64, lse_all, D_all, dqkv0, d, n_steps);
 }
 
