@@ -9,4 +9,4 @@ timeout 600 python -m pytest tests/test_attention_gpu.py -x -q -p no:cacheprovid
 run base SPECSIM_LIB=$PWD/probe/libbase.so
 run head SPECSIM_X=1
 timeout 900 python -m pytest tests/test_ttt_gpu.py tests/test_trainer_gpu.py -x -q -p no:cacheprovider 2>&1 | tail -2
-STEPS=40 WARM=10 bash scripts/ab_r01.sh 2 "SPECSIM_LIB=$PWD/probe/libbase.so" "SPECSIM_X=0"
+
