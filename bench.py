@@ -470,14 +470,22 @@ def run_ours(args):
 
     # ------------------------------------------------------------ roofline leg
     # Per-phase device time with CUDA events around every launch (a graph with
-    # timestamp nodes), over a short timed leg of single steps right after.
-    n_prof = min(args.steps, 5)
+    # timestamp nodes).  Measured on the LAST step of back-to-back train(job)
+    # jobs -- the same steady-state power / clock regime as the value leg
+    # (single synchronous steps leave idle gaps that let the clock recover and
+    # would read several % fast).  A first job captures the timing graph.
+    n_prof = min(args.steps, 3)
+    prof_job = max(4, min(args.steps, 8))
     tr.set_timing(True)
     phase_acc = {p: dict(ms=0.0, flops=0.0, launches=0) for p in api.DraftTrainer.PHASES}
     barrier()
+    tr.train(buf, global_job(2, lambda r, k, j: pool_id(r, k * B + j)), [], epochs=1)
     prof_step_ms = 0.0
     for k in range(n_prof):
-        prof_step_ms += tr.step(buf, batch(k))["ms"]
+        job = global_job(prof_job, lambda r, kk, j, o=k: pool_id(r, (o * prof_job + kk) * B + j))
+        tr.region_begin()
+        tr.train(buf, job, [], epochs=1)
+        prof_step_ms += max_over_ranks(tr.region_end()) / prof_job
         for p, v in tr.phase_times().items():
             for f in ("ms", "flops", "launches"):
                 phase_acc[p][f] += v[f]
@@ -503,14 +511,15 @@ def run_ours(args):
                     algorithmic="SURVEY §8(d): sum of GEMM FLOPs excluding the CE-backward logit "
                                 "recompute, over the summed device time of every GEMM launch "
                                 "(recompute time included)",
-                    measured=f"CUDA events around every GEMM launch over a {n_prof}-step timed "
-                             "leg run right after the value leg (same process, same clocks)")
+                    measured=f"CUDA events around every GEMM launch of the last step of "
+                             f"{n_prof} back-to-back {prof_job}-step train(job) jobs run right "
+                             "after the value leg (steady-state clock, as the value leg)")
     step_ms = region_ms / args.steps
     phases = {p: dict(ms_per_step=round(v["ms"] / n_prof, 3),
                       launches_per_step=v["launches"] // max(1, n_prof))
               for p, v in phase_acc.items()}
-    # device time of the profiled steps not inside any timed launch (launch
-    # gaps, event nodes, staging copies)
+    # device time per step of the profiled jobs not inside any timed launch
+    # (launch gaps, event nodes, per-step input fetch / result store)
     phases["untimed_gaps"] = dict(
         ms_per_step=round((prof_step_ms - sum(v["ms"] for v in phase_acc.values())) / n_prof, 3),
         launches_per_step=0)
@@ -542,20 +551,25 @@ def run_ours(args):
             os.environ["SPECSIM_CE_RECOMPUTE"] = "1"
             tr2 = api.DraftTrainer(cfg, seed=SEED, device=local)
             os.environ.pop("SPECSIM_CE_RECOMPUTE")
-            for k in range(2):
-                tr2.step(buf, batch(k))
+            # same method as the roofline leg: last step of back-to-back jobs
+            tr2.train(buf, global_job(2, lambda r, k, j: pool_id(r, k * B + j)), [], epochs=1)
             tr2.set_timing(True)
+            tr2.train(buf, global_job(2, lambda r, k, j: pool_id(r, k * B + j)), [], epochs=1)
             acc, st = 0.0, 0.0
-            for k in range(3):
-                st += tr2.step(buf, batch(k))["ms"]
+            for k in range(n_prof):
+                job = global_job(prof_job, lambda r, kk, j, o=k: pool_id(r, (o * prof_job + kk) * B + j))
+                tr2.region_begin()
+                tr2.train(buf, job, [], epochs=1)
+                st += tr2.region_end() / prof_job
                 acc += tr2.phase_times()["lm_head_ce"]["ms"]
             tr2.close()
             line["ce_recompute_probe"] = dict(
-                lm_head_ce_ms_per_step=round(acc / 3, 3), step_ms=round(st / 3, 3),
+                lm_head_ce_ms_per_step=round(acc / n_prof, 3), step_ms=round(st / n_prof, 3),
                 default_lm_head_ce_ms_per_step=phases["lm_head_ce"]["ms_per_step"],
-                note="logit-free LM-head + CE backward (no [T, V] logits in HBM); 3 timed "
-                     "single steps after 2 warm-up, phase events on; the default path stores "
-                     "fp16 logit offsets instead (DESIGN.md §3 K6)")
+                note=f"logit-free LM-head + CE backward (no [T, V] logits in HBM); last step of "
+                     f"{n_prof} back-to-back {prof_job}-step jobs, phase events on (as the "
+                     "default's phases); the default path stores fp16 logit offsets instead "
+                     "(DESIGN.md §3 K6)")
         except Exception as e:  # reported, never required
             os.environ.pop("SPECSIM_CE_RECOMPUTE", None)
             line["ce_recompute_probe"] = dict(error=str(e)[:200])

@@ -387,7 +387,9 @@ int specsim_trainer_set_embedding(specsim_trainer* t, const uint16_t* host_bf16)
 int specsim_trainer_get_embedding(const specsim_trainer* t, uint16_t* host_bf16);
 int specsim_trainer_set_step_count(specsim_trainer* t, int64_t step);
 
-/* Per-phase device timing of the last step (CUDA events on the step stream).
+/* Per-phase device timing of the last step (CUDA events on the step stream) --
+ * after specsim_trainer_train, of the job's last step, which ran back to back
+ * with the steps before it.
  * Phases: 0 ingest/gather, 1 GEMMs (sum over all tcgen05 GEMM launches),
  * 2 attention, 3 norms/elementwise, 4 LM-head+CE GEMMs, 5 AdamW,
  * 6 all-reduce.  flops[i] = algorithmic FLOPs of the phase (GEMM phases). */

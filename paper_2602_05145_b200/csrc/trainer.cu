@@ -1200,13 +1200,9 @@ class DraftTrainerImpl {
                        reinterpret_cast<uint32_t*>(dst_mapped), 6, stream);
   }
 
-  StepResult end_step() {
-    SPECSIM_CUDA(cudaEventRecord(ev_end, stream));
-    stats_to_host(h_stats);
-    SPECSIM_CHECK_LAUNCH();
-    SPECSIM_CUDA(cudaStreamSynchronize(stream));
-    float ms = 0;
-    SPECSIM_CUDA(cudaEventElapsedTime(&ms, ev_begin, ev_end));
+  // per-phase device time of the last launch (its timestamp events are the
+  // last replay's when the step ran as a graph); call after a stream sync
+  void collect_phases() {
     for (int i = 0; i < PH_N; ++i) {
       phase_ms[i] = 0;
       phase_flops[i] = rec->flops[i];
@@ -1218,6 +1214,16 @@ class DraftTrainerImpl {
         SPECSIM_CUDA(cudaEventElapsedTime(&tm, mk.second.first, mk.second.second));
         phase_ms[mk.first] += tm;
       }
+  }
+
+  StepResult end_step() {
+    SPECSIM_CUDA(cudaEventRecord(ev_end, stream));
+    stats_to_host(h_stats);
+    SPECSIM_CHECK_LAUNCH();
+    SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    float ms = 0;
+    SPECSIM_CUDA(cudaEventElapsedTime(&ms, ev_begin, ev_end));
+    collect_phases();
     StepResult res;
     res.loss = h_stats[0];
     res.valid_tokens = static_cast<int64_t>(h_stats[1]);
@@ -1445,6 +1451,9 @@ class DraftTrainerImpl {
     }
     SPECSIM_CHECK_LAUNCH();
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    // phase times of the job's last step (back-to-back with the steps before
+    // it, i.e. at the steady-state clock of a long job)
+    if (total_launch > 0) collect_phases();
     double loss_sum = 0;
     for (long long i = 0; i < train_steps; ++i) loss_sum += hist[3 * i];
     double valid = 0, correct = 0;
