@@ -155,3 +155,48 @@ def test_large_logit_range_rescale():
     O, LSE, _ = ref(q, do, B, S, nh, nkv, hd)
     assert rel(bf16_bits_to_f32(o), O) < 1e-2
     np.testing.assert_allclose(lse, LSE, rtol=1e-4, atol=2e-3)
+
+
+_TWO_TILE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+from paper_2602_05145_b200 import _lib
+from _util import rand_bf16
+B, S, nh, nkv, hd = (int(x) for x in sys.argv[3:8])
+rng = np.random.default_rng(11)
+NQ = (nh + 2 * nkv) * hd
+qkv_bits, _ = rand_bf16(rng, (B * S, NQ))
+do_bits, _ = rand_bf16(rng, (B * S, nh * hd))
+o = np.zeros((B * S, nh * hd), np.uint16)
+lse = np.zeros((nh, B * S), np.float32)
+dqkv = np.zeros((B * S, NQ), np.uint16)
+_lib.call("specsim_debug_attention", B, S, nh, nkv, hd, _lib.ptr(qkv_bits), _lib.ptr(do_bits),
+          _lib.ptr(o), _lib.ptr(lse), _lib.ptr(dqkv))
+np.savez(sys.argv[2], o=o, lse=lse)
+"""
+
+
+@pytest.mark.parametrize("B,S,nh,nkv,hd", [(2, 512, 8, 2, 128), (1, 1024, 4, 2, 64),
+                                           (1, 2048, 32, 8, 128)])
+def test_two_tile_forward_bit_identical_to_one_tile(tmp_path, B, S, nh, nkv, hd):
+    """The default forward (attn_fwd2_tc_kernel: a head pair per CTA, P in TMEM)
+    runs the same per-row arithmetic in the same order as the one-tile kernel
+    (SPECSIM_ATTN_FWD1=1), so O and lse must match bit for bit."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    root = pathlib.Path(__file__).resolve().parents[1]
+    script = tmp_path / "fwd.py"
+    script.write_text(_TWO_TILE_SCRIPT)
+    outs = {}
+    for one in ("0", "1"):
+        out = tmp_path / f"fwd{one}.npz"
+        env = dict(os.environ, SPECSIM_ATTN_FWD1=one)
+        r = subprocess.run([sys.executable, str(script), str(root), str(out), str(B), str(S),
+                            str(nh), str(nkv), str(hd)], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[one] = np.load(out)
+    assert np.array_equal(outs["0"]["o"], outs["1"]["o"])
+    assert np.array_equal(outs["0"]["lse"], outs["1"]["lse"])
