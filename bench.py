@@ -385,6 +385,13 @@ def run_ours(args):
         # first batch's copy is exposed.  train(job) returns the job's loss.
         sizes = [min(per_job, nsteps - d) for d in range(0, nsteps, per_job)]
         firsts = [sum(sizes[:i]) for i in range(len(sizes))]
+        if os.environ.get("SPECSIM_BENCH_E2E_PROBE") == "resident":
+            # diagnostic only: the same job structure on the resident pool (no
+            # host -> HBM copies), to separate the DMA from the job structure
+            for i in range(len(sizes)):
+                job = global_job(sizes[i], lambda r, k, j, o=firsts[i]: pool_id(r, (o + k) * B + j))
+                losses.append(tr.train(buf, job, [], epochs=1).mean_loss)
+            return
         pending = append_job(firsts[0], sizes[0])
         for i in range(len(sizes)):
             nxt = append_job(firsts[i + 1], sizes[i + 1]) if i + 1 < len(sizes) else None
