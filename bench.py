@@ -490,9 +490,8 @@ def run_ours(args):
     prof_step_ms = 0.0
     for k in range(n_prof):
         job = global_job(prof_job, lambda r, kk, j, o=k: pool_id(r, (o * prof_job + kk) * B + j))
-        tr.region_begin()
         tr.train(buf, job, [], epochs=1)
-        prof_step_ms += max_over_ranks(tr.region_end()) / prof_job
+        prof_step_ms += max_over_ranks(tr.last_step_ms())
         for p, v in tr.phase_times().items():
             for f in ("ms", "flops", "launches"):
                 phase_acc[p][f] += v[f]
@@ -525,7 +524,7 @@ def run_ours(args):
     phases = {p: dict(ms_per_step=round(v["ms"] / n_prof, 3),
                       launches_per_step=v["launches"] // max(1, n_prof))
               for p, v in phase_acc.items()}
-    # device time per step of the profiled jobs not inside any timed launch
+    # device time of the profiled (last) steps not inside any timed launch
     # (launch gaps, event nodes, per-step input fetch / result store)
     phases["untimed_gaps"] = dict(
         ms_per_step=round((prof_step_ms - sum(v["ms"] for v in phase_acc.values())) / n_prof, 3),
@@ -565,9 +564,8 @@ def run_ours(args):
             acc, st = 0.0, 0.0
             for k in range(n_prof):
                 job = global_job(prof_job, lambda r, kk, j, o=k: pool_id(r, (o * prof_job + kk) * B + j))
-                tr2.region_begin()
                 tr2.train(buf, job, [], epochs=1)
-                st += tr2.region_end() / prof_job
+                st += tr2.last_step_ms()
                 acc += tr2.phase_times()["lm_head_ce"]["ms"]
             tr2.close()
             line["ce_recompute_probe"] = dict(

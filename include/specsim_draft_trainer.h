@@ -400,6 +400,9 @@ int specsim_trainer_set_timing(specsim_trainer* t, int enabled);
 int specsim_trainer_region(specsim_trainer* t, int end, double* ms);
 int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
                                 int32_t* launches7);
+/* Device time (ms) of the last step: the last step()/eval(), or the last step
+ * of the last specsim_trainer_train job (from its graph launch to its end). */
+int specsim_trainer_last_step_ms(const specsim_trainer* t, double* ms);
 
 /* Per-row device state of the last step / eval, copied to the host (parity
  * tests: the target gather and top-1 are checked bit-exact against the

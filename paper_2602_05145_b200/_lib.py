@@ -141,6 +141,7 @@ SIGNATURES = {
     "specsim_trainer_set_timing": [P, C.c_int],
     "specsim_trainer_region": [P, C.c_int, PF64],
     "specsim_trainer_phase_times": [P, PF64, PF64, PI32],
+    "specsim_trainer_last_step_ms": [P, PF64],
     "specsim_trainer_read_rows": [P, C.c_char_p, P, I64, PI64],
     "specsim_capture_create": [C.POINTER(SignalGeometry), C.c_char_p, I64, C.c_int, C.POINTER(P)],
     "specsim_capture_destroy": [P],

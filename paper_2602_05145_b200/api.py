@@ -459,6 +459,11 @@ class DraftTrainer:
     def set_timing(self, on: bool):
         call("specsim_trainer_set_timing", self.h, 1 if on else 0)
 
+    def last_step_ms(self):
+        v = C.c_double(0)
+        call("specsim_trainer_last_step_ms", self.h, C.byref(v))
+        return v.value
+
     def phase_times(self):
         ms = (C.c_double * 7)()
         fl = (C.c_double * 7)()

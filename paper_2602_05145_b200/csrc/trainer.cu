@@ -326,6 +326,7 @@ class DraftTrainerImpl {
   bool use_graphs = true;
   bool capturing = false;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  float last_ms = 0.f;  // device time of the last step (step(), eval(), or a job's last)
   long long* n_counted = nullptr;
   cudaEvent_t ev_region[2] = {nullptr, nullptr};
 
@@ -1223,6 +1224,7 @@ class DraftTrainerImpl {
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
     float ms = 0;
     SPECSIM_CUDA(cudaEventElapsedTime(&ms, ev_begin, ev_end));
+    last_ms = ms;
     collect_phases();
     StepResult res;
     res.loss = h_stats[0];
@@ -1445,12 +1447,14 @@ class DraftTrainerImpl {
         SPECSIM_CUDA(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(ev), 0));
       kern::fetch_mapped(reinterpret_cast<const uint32_t*>(d_job + k),
                          reinterpret_cast<uint32_t*>(d_in), words, stream);  // device -> device
-      launch(buf, is_train[k] != 0);
+      launch(buf, is_train[k] != 0);  // records ev_begin right before the graph launch
       if (is_train[k]) step_count += 1;
       stats_to_host(hist + 3 * k);
     }
+    SPECSIM_CUDA(cudaEventRecord(ev_end, stream));  // last launch: ev_begin .. ev_end
     SPECSIM_CHECK_LAUNCH();
     SPECSIM_CUDA(cudaStreamSynchronize(stream));
+    if (total_launch > 0) SPECSIM_CUDA(cudaEventElapsedTime(&last_ms, ev_begin, ev_end));
     // phase times of the job's last step (back-to-back with the steps before
     // it, i.e. at the steady-state clock of a long job)
     if (total_launch > 0) collect_phases();
@@ -1786,6 +1790,13 @@ int specsim_trainer_keep_grads(specsim_trainer* t, int enabled) {
 
 int specsim_trainer_set_timing(specsim_trainer* t, int enabled) {
   return guard([&] { impl_of(t).timing = enabled != 0; });
+}
+
+int specsim_trainer_last_step_ms(const specsim_trainer* t, double* ms) {
+  return guard([&] {
+    if (!ms) throw std::invalid_argument("null output");
+    *ms = impl_of(t).last_ms;
+  });
 }
 
 int specsim_trainer_phase_times(const specsim_trainer* t, double* ms7, double* flops7,
